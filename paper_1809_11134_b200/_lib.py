@@ -1,0 +1,92 @@
+"""ctypes binding of libisq.so (include/isq.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+usable, calls raise instead of computing anything on the host.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import ConfigurationError, InvariantViolation
+
+LIB_PATH = Path(__file__).resolve().parent / "libisq.so"
+
+ISQ_OK = 0
+ISQ_ERR_CONFIG = 1
+ISQ_ERR_INVARIANT = 2
+ISQ_ERR_CUDA = 3
+ISQ_ERR_COMM = 4
+ISQ_ERR_UNSUPPORTED = 5
+
+MIN_WIRES = 2
+MAX_WIRES = 5
+
+_lock = threading.Lock()
+_lib = None
+
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_u64 = ctypes.c_uint64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+c_dp = ctypes.POINTER(ctypes.c_double)
+c_u8p = ctypes.POINTER(ctypes.c_uint8)
+
+# name -> (restype, argtypes).  Kept in sync with include/isq.h (a CPU test
+# checks that every declared symbol is exported and listed here).
+SIGNATURES: dict[str, tuple] = {
+    "isq_last_error": (ctypes.c_char_p, []),
+    "isq_abi_version": (c_i32, []),
+    "isq_fitness_batch": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "isq_fitness_batch_device": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "isq_philox_block": (None, [c_u64, c_u64, c_u64, c_u64, c_u64, c_u64, c_vp]),
+    "isq_fma_peak": (c_i32, [c_i32, c_i32, c_vp]),
+    "isq_fitness_of_unitaries": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_i32]),
+}
+
+
+class IsqError(RuntimeError):
+    """Device-side failure reported by libisq (CUDA/NCCL error)."""
+
+
+def load(path: Path | None = None):
+    """Load and bind libisq.so; raises ImportError when it has not been built."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise ImportError(
+                f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(status: int) -> None:
+    if status == ISQ_OK:
+        return
+    msg = load().isq_last_error()
+    msg = msg.decode() if msg else "unknown error"
+    if status in (ISQ_ERR_CONFIG, ISQ_ERR_UNSUPPORTED):
+        raise ConfigurationError(msg)
+    if status == ISQ_ERR_INVARIANT:
+        raise InvariantViolation(msg)
+    raise IsqError(f"libisq status {status}: {msg}")
+
+
+def ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    return a.ctypes.data_as(c_vp)

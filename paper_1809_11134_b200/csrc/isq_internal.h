@@ -1,0 +1,38 @@
+// Internal declarations shared by the CUDA translation units of libisq.
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <cuda_runtime.h>
+
+#include "../../include/isq.h"
+
+namespace isq {
+
+// Thread-local last error (isq_last_error).
+void set_error(const std::string& msg);
+
+#define ISQ_CUDA_TRY(expr)                                                                 \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      ::isq::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                \
+      return ISQ_ERR_CUDA;                                                                 \
+    }                                                                                      \
+  } while (0)
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kThreadsPerBlock = 32 * kWarpsPerBlock;
+
+// Number of resident blocks for a persistent grid of `kernel` (blocks of 128 threads).
+int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps);
+
+// fitness / compose over explicit gate lists (device pointers).
+isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* codes,
+                                const double* thetas, const double* target_dev,
+                                double* fitness_dev, double* unitary_dev, cudaStream_t stream);
+
+isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, const double* T,
+                                  double* out, cudaStream_t stream);
+
+}  // namespace isq

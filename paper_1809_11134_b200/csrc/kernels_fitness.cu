@@ -1,0 +1,166 @@
+// Fitness / composition of explicit gate lists (GA genomes, best-circuit
+// readout, the functional API).  Replaces compose_gates + fitness_value
+// (gates.py:187-195, fitness.py:36-49) for a batch of circuits.
+#include "isq_internal.h"
+#include "unitary_warp.cuh"
+
+namespace isq {
+
+struct ChunkShared {
+  int op[32];
+  double a[32];
+  double b[32];
+};
+
+template <int NQ>
+__global__ void __launch_bounds__(kThreadsPerBlock)
+    fitness_batch_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
+                         const double* __restrict__ thetas, const double2* __restrict__ target,
+                         double* __restrict__ fitness, double2* __restrict__ unitary) {
+  using G = Geo<NQ>;
+  __shared__ double2 Ts[G::D * G::D];
+  __shared__ ChunkShared sh[kWarpsPerBlock];
+  for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  ChunkShared& cs = sh[wib];
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t c = (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < count; c += nwarps) {
+    WarpUnitary<NQ> st;
+    st.set_identity(lane);
+    double mant = 1.0, phase = 0.0;
+    const uint8_t* cc = codes + c * (int64_t)L;
+    const double* ct = thetas + c * (int64_t)L;
+    for (int base = 0; base < L; base += 32) {
+      const int p = base + lane;
+      GateParam g;
+      if (p < L) {
+        g = gate_param<NQ>((int)cc[p], ct[p]);
+      } else {
+        g.op = -1;
+        g.a = g.b = 0.0;
+        g.scale = 1.0;
+        g.phase = 0.0;
+      }
+      int ex;
+      mant = frexp(mant * warp_prod(g.scale), &ex);
+      st.scale_all(ldexp(1.0, ex));
+      if (unitary) phase += warp_sum(g.phase);
+      cs.op[lane] = g.op;
+      cs.a[lane] = g.a;
+      cs.b[lane] = g.b;
+      __syncwarp();
+      const int nq = min(32, L - base);
+      for (int q = 0; q < nq; ++q) st.apply(cs.op[q], cs.a[q], cs.b[q], lane);
+      __syncwarp();
+    }
+    double ore, oim;
+    st.overlap(Ts, lane, ore, oim);
+    const double ov = fabs(mant) * hypot(ore, oim);
+    if (lane == 0) fitness[c] = fitness_from_overlap(ov, G::D);
+    if (unitary != nullptr && lane < G::ACTIVE) {
+      double ps, pc;
+      sincos(phase, &ps, &pc);
+      const double fr = mant * pc, fi = mant * ps;
+      const int j = lane & (G::D - 1);
+      const int h = (lane >> NQ) & (G::LPC - 1);
+      double2* U = unitary + c * (int64_t)(G::D * G::D);
+#pragma unroll
+      for (int r = 0; r < G::E; ++r) {
+        const double xr = st.re[r], xi = st.im[r];
+        U[(h * G::E + r) * G::D + j] = make_double2(fr * xr - fi * xi, fr * xi + fi * xr);
+      }
+    }
+  }
+}
+
+// fitness_value on explicit matrices (fitness.py:36-49): one block per pair
+// (S_c, T); block reduction of conj(S) * T in a fixed order.
+__global__ void __launch_bounds__(256)
+    overlap_fitness_kernel(int64_t D, int64_t count, const double2* __restrict__ S,
+                           const double2* __restrict__ T, double* __restrict__ out) {
+  __shared__ double red_r[256], red_i[256];
+  const int64_t DD = D * D;
+  for (int64_t c = blockIdx.x; c < count; c += gridDim.x) {
+    const double2* s = S + c * DD;
+    double ar = 0.0, ai = 0.0;
+    for (int64_t i = threadIdx.x; i < DD; i += blockDim.x) {
+      const double2 x = s[i], t = T[i];
+      ar = fma(x.x, t.x, ar);
+      ar = fma(x.y, t.y, ar);
+      ai = fma(x.x, t.y, ai);
+      ai = fma(-x.y, t.x, ai);
+    }
+    red_r[threadIdx.x] = ar;
+    red_i[threadIdx.x] = ai;
+    __syncthreads();
+    for (int off = 128; off >= 1; off >>= 1) {
+      if (threadIdx.x < off) {
+        red_r[threadIdx.x] += red_r[threadIdx.x + off];
+        red_i[threadIdx.x] += red_i[threadIdx.x + off];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = fitness_from_overlap(hypot(red_r[0], red_i[0]), (int)D);
+    __syncthreads();
+  }
+}
+
+isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, const double* T,
+                                  double* out, cudaStream_t stream) {
+  if (count <= 0) return ISQ_OK;
+  const int grid = (int)(count < 65535 ? count : 65535);
+  overlap_fitness_kernel<<<grid, 256, 0, stream>>>(D, count, reinterpret_cast<const double2*>(S),
+                                                   reinterpret_cast<const double2*>(T), out);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps) {
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreadsPerBlock, dyn_smem);
+  if (per_sm <= 0) per_sm = 1;
+  const int64_t need = (work_warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int64_t full = (int64_t)num_sms * per_sm;
+  int64_t g = need < full ? need : full;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <int NQ>
+static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const double* thetas,
+                            const double* target, double* fitness, double* unitary,
+                            cudaStream_t stream) {
+  const void* k = (const void*)fitness_batch_kernel<NQ>;
+  const int grid = persistent_grid(k, 0, count);
+  fitness_batch_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
+      count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness,
+      reinterpret_cast<double2*>(unitary));
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* codes,
+                                const double* thetas, const double* target, double* fitness,
+                                double* unitary, cudaStream_t stream) {
+  if (count <= 0) return ISQ_OK;
+  switch (n) {
+    case 2: return launch_nq<2>(L, count, codes, thetas, target, fitness, unitary, stream);
+    case 3: return launch_nq<3>(L, count, codes, thetas, target, fitness, unitary, stream);
+    case 4: return launch_nq<4>(L, count, codes, thetas, target, fitness, unitary, stream);
+    case 5: return launch_nq<5>(L, count, codes, thetas, target, fitness, unitary, stream);
+    default:
+      set_error("numberOfWires=" + std::to_string(n) + " is outside the compiled range 2..5");
+      return ISQ_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace isq

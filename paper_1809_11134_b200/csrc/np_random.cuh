@@ -1,0 +1,273 @@
+// Counter-based RNG streams that reproduce numpy's Generator(Philox(...)) bit for bit.
+//
+// The reference engine draws every random number from numpy Generators
+// (engine.py:105-112 init, :167-170 Born measurement, :174-184 circuit
+// sampling, :241-242 mutation mask/coin; encoding.py:52,127-128 mutation
+// steps; ga.py:68-138 GA operators).  This build replaces each sequential
+// Generator with one independent Philox4x64-10 stream per unit of work
+// (circuit, slot, gene, ...), keyed
+//
+//     key     = (seed, domain)
+//     counter = (0, generation, index, sub)
+//
+// exactly as numpy.random.Philox(key=[seed, domain], counter=[0, gen, index,
+// sub]) would: the counter is incremented BEFORE each 4x64 block, so the
+// first block of every stream is philox(ctr = (1, gen, index, sub)).
+//
+// numpy semantics reproduced here (numpy/random/src):
+//   next_uint64  : buffered 4-word blocks                (philox.h philox_next)
+//   next_uint32  : low half first, high half buffered and persisting across
+//                  calls; next_uint64/next_double do NOT touch that buffer
+//   next_double  : (u64 >> 11) * 2^-53
+//   integers(b)  : Lemire on u32 with rejection, rng = b - 1
+//                  (distributions.c buffered_bounded_lemire_uint32)
+//   uniform(l,h) : l + (h - l) * next_double
+//   binomial     : inversion for n*min(p,1-p) <= 30     (random_binomial_inversion)
+//   multinomial  : sequential binomials                  (random_multinomial)
+//
+// All floating point that must be bit-exact is written with explicit
+// round-to-nearest intrinsics so nvcc never contracts it into an FMA
+// (numpy's random C code is compiled for the SSE baseline, without FMA).
+#pragma once
+#include <cstdint>
+
+namespace isq {
+
+// Stream domains (counter[1..3] meaning in brackets).  Shared with oracle/streams.py.
+enum : uint64_t {
+  DOM_SAMPLE = 1,    // (gen, circuit, 0)  integers(P, L) then integers(K, L)
+  DOM_MEASURE = 2,   // (gen, slot, 0)     multinomial(n_meas, born(qutrit))
+  DOM_MUTATE = 3,    // (gen, slot, 0)     mask, coin, [integers(8), uniform] | [random]
+  DOM_INIT = 4,      // (0, slot, 0)       theta = uniform(0, 2pi), 6 Box-Muller uniforms
+  DOM_GA_INIT = 5,   // (0, genome, gene)  integers(n_choices), uniform(0, 2pi)
+  DOM_GA_SUS = 6,    // (gen, 0, 0)        uniform(0, spacing) | P x integers(P)
+  DOM_GA_PAIR = 7,   // (gen, pair, 0)     integers(0, L+1, size=2)
+  DOM_GA_MUT = 8,    // (gen, child, gene) random, [random, integers(n_choices) | uniform(-r, r)]
+};
+
+constexpr uint64_t PHILOX_M0 = 0xD2E7470EE14C6C93ULL;
+constexpr uint64_t PHILOX_M1 = 0xCA5A826395121157ULL;
+constexpr uint64_t PHILOX_W0 = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t PHILOX_W1 = 0xBB67AE8584CAA73BULL;
+
+// Random123 philox4x64 with 10 rounds (numpy's philox4x64_R(10, ...)).
+__host__ __device__ __forceinline__ void philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2,
+                                                       uint64_t c3, uint64_t k0, uint64_t k1,
+                                                       uint64_t out[4]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += PHILOX_W0;
+      k1 += PHILOX_W1;
+    }
+#ifdef __CUDA_ARCH__
+    const uint64_t hi0 = __umul64hi(PHILOX_M0, c0);
+    const uint64_t hi1 = __umul64hi(PHILOX_M1, c2);
+#else
+    const uint64_t hi0 = (uint64_t)(((unsigned __int128)PHILOX_M0 * c0) >> 64);
+    const uint64_t hi1 = (uint64_t)(((unsigned __int128)PHILOX_M1 * c2) >> 64);
+#endif
+    const uint64_t lo0 = PHILOX_M0 * c0;
+    const uint64_t lo1 = PHILOX_M1 * c2;
+    const uint64_t n0 = hi1 ^ c1 ^ k0;
+    const uint64_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+// Block `b` (1-based, i.e. after b counter increments) of stream (seed, dom, gen, idx, sub).
+__host__ __device__ __forceinline__ void stream_block(uint64_t seed, uint64_t dom, uint64_t gen,
+                                                      uint64_t idx, uint64_t sub, uint64_t b,
+                                                      uint64_t out[4]) {
+  philox4x64_10(b, gen, idx, sub, seed, dom, out);
+}
+
+__host__ __device__ __forceinline__ double u64_to_double(uint64_t w) {
+  return (double)(w >> 11) * (1.0 / 9007199254740992.0);
+}
+
+#ifdef __CUDA_ARCH__
+#define ISQ_DMUL(a, b) __dmul_rn((a), (b))
+#define ISQ_DADD(a, b) __dadd_rn((a), (b))
+#define ISQ_DSUB(a, b) __dsub_rn((a), (b))
+#define ISQ_DDIV(a, b) __ddiv_rn((a), (b))
+#else
+#define ISQ_DMUL(a, b) ((a) * (b))
+#define ISQ_DADD(a, b) ((a) + (b))
+#define ISQ_DSUB(a, b) ((a) - (b))
+#define ISQ_DDIV(a, b) ((a) / (b))
+#endif
+
+// Sequential numpy-compatible stream.  Used where consumption is data dependent
+// (rejections, binomial redraws, GA operators); hot fast paths compute the
+// blocks they need directly with stream_block().
+struct NpStream {
+  uint64_t seed, dom, gen, idx, sub;
+  uint64_t ctr;  // number of blocks generated so far
+  uint64_t buf[4];
+  int pos;       // next word in buf; 4 = empty
+  uint32_t u32buf;
+  bool has32;
+
+  __host__ __device__ __forceinline__ void init(uint64_t seed_, uint64_t dom_, uint64_t gen_,
+                                                uint64_t idx_, uint64_t sub_) {
+    seed = seed_;
+    dom = dom_;
+    gen = gen_;
+    idx = idx_;
+    sub = sub_;
+    ctr = 0;
+    pos = 4;
+    has32 = false;
+    u32buf = 0;
+  }
+  __host__ __device__ __forceinline__ uint64_t next64() {
+    if (pos >= 4) {
+      ++ctr;
+      stream_block(seed, dom, gen, idx, sub, ctr, buf);
+      pos = 0;
+    }
+    return buf[pos++];
+  }
+  __host__ __device__ __forceinline__ uint32_t next32() {
+    if (has32) {
+      has32 = false;
+      return u32buf;
+    }
+    const uint64_t w = next64();
+    has32 = true;
+    u32buf = (uint32_t)(w >> 32);
+    return (uint32_t)(w & 0xffffffffULL);
+  }
+  __host__ __device__ __forceinline__ double random() { return u64_to_double(next64()); }
+  __host__ __device__ __forceinline__ double uniform(double lo, double hi) {
+    return ISQ_DADD(lo, ISQ_DMUL(ISQ_DSUB(hi, lo), random()));
+  }
+  // numpy buffered_bounded_lemire_uint32 with rng = bound - 1 (rng < 0xFFFFFFFF).
+  __host__ __device__ __forceinline__ uint32_t lemire32(uint32_t rng) {
+    const uint32_t rng_excl = rng + 1u;
+    uint64_t m = (uint64_t)next32() * (uint64_t)rng_excl;
+    uint32_t leftover = (uint32_t)(m & 0xffffffffULL);
+    if (leftover < rng_excl) {
+      const uint32_t threshold = (0xffffffffu - rng) % rng_excl;
+      while (leftover < threshold) {
+        m = (uint64_t)next32() * (uint64_t)rng_excl;
+        leftover = (uint32_t)(m & 0xffffffffULL);
+      }
+    }
+    return (uint32_t)(m >> 32);
+  }
+  // Generator.integers(bound) for 1 <= bound <= 2^32 (default int64 dtype).
+  __host__ __device__ __forceinline__ int64_t integers(int64_t bound) {
+    const uint64_t rng = (uint64_t)bound - 1u;
+    if (rng == 0) return 0;
+    if (rng == 0xffffffffULL) return (int64_t)next32();
+    return (int64_t)lemire32((uint32_t)rng);
+  }
+};
+
+// Lemire rejection predicate for one u32 draw against bound (= rng + 1):
+// true when numpy would discard this draw and take another.
+__host__ __device__ __forceinline__ bool lemire_rejects(uint32_t u, uint32_t rng) {
+  const uint32_t rng_excl = rng + 1u;
+  const uint32_t leftover = (uint32_t)(((uint64_t)u * rng_excl) & 0xffffffffULL);
+  if (leftover >= rng_excl) return false;
+  const uint32_t threshold = (0xffffffffu - rng) % rng_excl;
+  return leftover < threshold;
+}
+__host__ __device__ __forceinline__ uint32_t lemire_value(uint32_t u, uint32_t rng) {
+  return (uint32_t)(((uint64_t)u * (uint64_t)(rng + 1u)) >> 32);
+}
+
+// numpy random_binomial_inversion (distributions.c).  Returns -1 never; the
+// bound/redraw loop is reproduced exactly, exp/log are the device versions
+// (last-ulp differences from glibc can flip a draw only when U
+// lies within an ulp of a CDF boundary).
+__device__ __forceinline__ int64_t binomial_inversion(NpStream& s, int64_t n, double p) {
+  const double q = ISQ_DSUB(1.0, p);
+  const double qn = exp(ISQ_DMUL((double)n, log(q)));
+  const double np_ = ISQ_DMUL((double)n, p);
+  const double bnd = ISQ_DADD(np_, ISQ_DMUL(10.0, sqrt(ISQ_DADD(ISQ_DMUL(np_, q), 1.0))));
+  const int64_t bound = (int64_t)((double)n < bnd ? (double)n : bnd);
+  int64_t X = 0;
+  double px = qn;
+  double U = s.random();
+  while (U > px) {
+    X++;
+    if (X > bound) {
+      X = 0;
+      px = qn;
+      U = s.random();
+    } else {
+      U = ISQ_DSUB(U, px);
+      px = ISQ_DDIV(ISQ_DMUL(ISQ_DMUL((double)(n - X + 1), p), px), ISQ_DMUL((double)X, q));
+    }
+  }
+  return X;
+}
+
+// numpy random_binomial restricted to the inversion branch; *ok = false when
+// numpy would take the BTPE branch (n * min(p, 1-p) > 30), which this build
+// rejects at configuration time (n_meas <= 60 guarantees inversion).
+__device__ __forceinline__ int64_t binomial(NpStream& s, double p, int64_t n, bool* ok) {
+  if (n == 0 || p == 0.0) return 0;
+  if (p <= 0.5) {
+    if (ISQ_DMUL(p, (double)n) <= 30.0) return binomial_inversion(s, n, p);
+    *ok = false;
+    return 0;
+  }
+  const double q = ISQ_DSUB(1.0, p);
+  if (ISQ_DMUL(q, (double)n) <= 30.0) return n - binomial_inversion(s, n, q);
+  *ok = false;
+  return 0;
+}
+
+// numpy |z| for complex128 (SIMD loop, loops_unary_complex.dispatch.c.src):
+// larger * sqrt(fma(ratio, ratio, 1)), ratio = smaller / larger.
+__device__ __forceinline__ double np_cabs(double re, double im) {
+  const double a = fabs(re), b = fabs(im);
+  const double larger = fmax(a, b), smaller = fmin(a, b);
+  if (larger == 0.0) return 0.0;
+  if (isinf(larger)) return larger;
+  const double ratio = __ddiv_rn(smaller, larger);
+  return __dmul_rn(__dsqrt_rn(__fma_rn(ratio, ratio, 1.0)), larger);
+}
+
+// construct_segments for one qutrit (engine.py:167-170): Born probabilities
+// np.abs(q)**2 normalised by the (left-to-right) row sum, one multinomial
+// draw of n_meas measurements, argmax with ties to the lower axis.
+__device__ __forceinline__ int measure_axis(const double qre[3], const double qim[3], int n_meas,
+                                            NpStream& s, bool* ok) {
+  double pr[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double a = np_cabs(qre[j], qim[j]);
+    pr[j] = __dmul_rn(a, a);
+  }
+  const double sum = __dadd_rn(__dadd_rn(pr[0], pr[1]), pr[2]);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) pr[j] = __ddiv_rn(pr[j], sum);
+  int64_t cnt[3] = {0, 0, 0};
+  double remaining = 1.0;
+  int64_t dn = n_meas;
+  for (int j = 0; j < 2; ++j) {
+    cnt[j] = binomial(s, __ddiv_rn(pr[j], remaining), dn, ok);
+    dn -= cnt[j];
+    if (dn <= 0) break;
+    remaining = __dsub_rn(remaining, pr[j]);
+  }
+  if (dn > 0) cnt[2] = dn;
+  int best = 0;
+  if (cnt[1] > cnt[best]) best = 1;
+  if (cnt[2] > cnt[best]) best = 2;
+  return best;
+}
+
+}  // namespace isq

@@ -1,0 +1,51 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol
+include/isq.h declares, the ctypes table matches, and the host-side Philox
+core equals numpy's Philox."""
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = ROOT / "include" / "isq.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(isq_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1809_11134_b200 import _lib
+
+    lib = _lib.load()
+    syms = declared_symbols()
+    assert len(syms) >= 5
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
+    assert lib.isq_abi_version() == 1
+
+
+@pytest.mark.parametrize("key", [(0, 1, 0, 0, 0), (7, 3, 12, 999, 0), (2**63 + 5, 8, 2**40, 3, 17)])
+def test_host_philox_matches_numpy(key):
+    from paper_1809_11134_b200 import _lib
+
+    lib = _lib.load()
+    seed, dom, gen, idx, sub = key
+    ref = np.random.Philox(key=np.array([seed, dom], dtype=np.uint64),
+                           counter=np.array([0, gen, idx, sub], dtype=np.uint64))
+    raw = ref.random_raw(12)
+    out = np.zeros(4, dtype=np.uint64)
+    for b in range(3):
+        lib.isq_philox_block(seed, dom, gen, idx, sub, b + 1, out.ctypes.data_as(ctypes.c_void_p))
+        assert list(out) == list(raw[4 * b:4 * b + 4])
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = ROOT / "paper_1809_11134_b200"
+    for p in pkg.rglob("*.py"):
+        assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", p.read_text(), flags=re.M), p

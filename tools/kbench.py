@@ -1,0 +1,53 @@
+"""Kernel micro-benchmarks (device-resident inputs, CUDA events)."""
+import ctypes
+import json
+import math
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np
+import torch
+
+from paper_1809_11134_b200 import _lib
+
+
+def main():
+    lib = _lib.load()
+    res = {}
+    for fp64 in (1, 0):
+        v = ctypes.c_double()
+        _lib.check(lib.isq_fma_peak(fp64, 0, ctypes.cast(ctypes.pointer(v), ctypes.c_void_p)))
+        res["fp64_peak_tflops" if fp64 else "fp32_peak_tflops"] = v.value / 1e12
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.current_stream()
+    for n, L, count in [(3, 16, 1 << 20), (4, 32, 1 << 18), (5, 64, 1 << 16), (5, 64, 1 << 18)]:
+        nc = 3 * n + n * (n - 1) // 2
+        g = torch.Generator(device=dev).manual_seed(1)
+        codes = torch.randint(0, nc, (count, L), device=dev, dtype=torch.uint8, generator=g)
+        thetas = torch.rand((count, L), device=dev, dtype=torch.float64, generator=g) * 2 * math.pi
+        T = torch.eye(2 ** n, dtype=torch.complex128, device=dev)
+        out = torch.empty(count, dtype=torch.float64, device=dev)
+        args = (n, L, count, codes.data_ptr(), thetas.data_ptr(), T.data_ptr(), out.data_ptr(), None,
+                stream.cuda_stream)
+        for _ in range(3):
+            _lib.check(lib.isq_fitness_batch_device(*args))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record()
+        for _ in range(reps):
+            lib.isq_fitness_batch_device(*args)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        evals = count / (ms * 1e-3)
+        flop = (6 * L + 8) * 4 ** n
+        res[f"n{n}_L{L}_P{count}"] = {"ms": ms, "evals_per_s": evals,
+                                     "canon_tflops": evals * flop / 1e12,
+                                     "frac_fp64": evals * flop / 1e12 / res["fp64_peak_tflops"]}
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
