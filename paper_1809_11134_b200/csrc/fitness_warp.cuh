@@ -1,0 +1,206 @@
+// Fast fitness evaluator: warp-per-candidate, register-resident columns,
+// diagonal-phase accumulation and in-place lifted rotations.
+//
+// Replaces evaluate_circuit / fitness_value (engine.py:187-199,
+// fitness.py:36-49) and GA decode + score (ga.py:76-78,167-170) when only the
+// fitness is needed.  The composed matrix is carried as
+//
+//     S_true  ~  diag(e^{i phi}) . S_phys          (up to a global phase / sign)
+//
+//   S_phys : register state (WarpUnitary layout, unitary_warp.cuh)
+//   phi    : pending per-row phases; lane r holds phi_r (r < D)
+//
+// * Rz and ZZ are diagonal: e^{-i th/2} diag(1 | e^{i th}) over the rows whose
+//   wire bit (Rz) or bit parity (ZZ) is 1.  They commute with phi, so each
+//   costs one predicated DADD per lane (phi_r += th * g(r)) and no per-gate
+//   code path.
+// * An Rx/Ry rotation on row bit b only fails to commute with the part of phi
+//   that differs between rows r and r ^ 2^b.  Those deltas are flushed into
+//   the rows with bit b set (skipped when all are 0), then the rotation is
+//   applied as a rotation by a = -th/2 (Rx) or +th/2 (Ry) of two real planes
+//   per row pair, reduced to |a| <= pi/2 (R(a) = -R(a -+ pi), a global sign),
+//   with the in-place 3-shear lifting x += p y; y += q x; x += p y.  In-place
+//   updates keep every switch case free of register moves, so the hot code is
+//   2n rotation cases + n flush cases and fits the instruction cache.
+// * At the end |tr(S_true^dagger T)| = |sum_kj conj(S_phys[k][j]) e^{-i phi_k} T[k][j]|.
+#pragma once
+#include "unitary_warp.cuh"
+
+namespace isq {
+
+// Per-warp shared scratch for one 32-gate chunk.
+struct FastChunk {
+  int info[32];      // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit or row mask
+  double c0[32];     // diag: theta ; rotation: p = -tan(a/2)
+  double c1[32];     // rotation: q = sin a
+  double c2[32];     // rotation: C = cos a (lane-bit form)
+  double2 fac[32];   // flush factors / final row weights, indexed by physical row
+};
+
+enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
+
+constexpr double kPi = 3.141592653589793;
+constexpr double kTwoPi = 6.283185307179586;
+
+template <int NQ>
+struct FastEval {
+  using G = Geo<NQ>;
+  WarpUnitary<NQ> st;
+  double phi;  // pending phase of physical row `lane` (lane < D)
+
+  __device__ __forceinline__ void begin(int lane) {
+    st.set_identity(lane);
+    phi = 0.0;
+  }
+
+  // Lane-parallel gate preparation for one position.
+  __device__ __forceinline__ static void prepare(int code, double theta, int& info, double& c0,
+                                                 double& c1, double& c2) {
+    c1 = c2 = 0.0;
+    if (code < 3 * NQ) {
+      const int w0 = code / 3, axis = code - 3 * w0;
+      const int b = NQ - 1 - w0;  // row bit of the wire (wire 1 = MSB)
+      if (axis == 2) {
+        info = GT_DIAG | ((1 << b) << 8);
+        c0 = theta;
+        return;
+      }
+      // plane angle, reduced to [-pi/2, pi/2] up to a global sign
+      double a = remainder(theta, kTwoPi) * (axis == 0 ? -0.5 : 0.5);
+      if (a > 0.5 * kPi) a -= kPi;
+      if (a < -0.5 * kPi) a += kPi;
+      double sh, ch;
+      sincos(0.5 * a, &sh, &ch);
+      info = (axis == 0 ? GT_RX : GT_RY) | (b << 8);
+      c0 = -sh / ch;
+      c1 = 2.0 * sh * ch;
+      c2 = fma(ch, ch, -sh * sh);
+      return;
+    }
+    const int t = code - 3 * NQ;
+    int i = 1, tt = t;
+    while (tt >= NQ - i) {
+      tt -= NQ - i;
+      ++i;
+    }
+    const int j = i + 1 + tt;
+    info = GT_DIAG | (((1 << (NQ - i)) | (1 << (NQ - j))) << 8);
+    c0 = theta;
+  }
+
+  // Multiply the register rows with bit B set by fac[row] (flush of pending deltas).
+  template <int B>
+  __device__ __forceinline__ void flush_bit(const double2* fac, int lane) {
+    const int h = (lane >> NQ) & (G::LPC - 1);
+#pragma unroll
+    for (int r = 0; r < G::E; ++r) {
+      if (B < G::EB && !(r & (1 << B))) continue;
+      const double2 f = fac[h * G::E + r];
+      st.cmul(r, f.x, f.y);
+    }
+  }
+
+  __device__ __forceinline__ void flush(int b, const double2* fac, int lane) {
+    switch (b) {
+      case 0: flush_bit<0>(fac, lane); break;
+      case 1: if constexpr (NQ > 1) flush_bit<1>(fac, lane); break;
+      case 2: if constexpr (NQ > 2) flush_bit<2>(fac, lane); break;
+      case 3: if constexpr (NQ > 3) flush_bit<3>(fac, lane); break;
+      case 4: if constexpr (NQ > 4) flush_bit<4>(fac, lane); break;
+      default: break;
+    }
+  }
+
+  __device__ __forceinline__ void rotate(int type, int b, double p, double q, double C, int lane) {
+    if (type == GT_RX) {
+      switch (b) {
+        case 0: st.template lift<0, 0>(p, q, C, lane); break;
+        case 1: if constexpr (NQ > 1) st.template lift<1, 0>(p, q, C, lane); break;
+        case 2: if constexpr (NQ > 2) st.template lift<2, 0>(p, q, C, lane); break;
+        case 3: if constexpr (NQ > 3) st.template lift<3, 0>(p, q, C, lane); break;
+        case 4: if constexpr (NQ > 4) st.template lift<4, 0>(p, q, C, lane); break;
+        default: break;
+      }
+    } else {
+      switch (b) {
+        case 0: st.template lift<0, 1>(p, q, C, lane); break;
+        case 1: if constexpr (NQ > 1) st.template lift<1, 1>(p, q, C, lane); break;
+        case 2: if constexpr (NQ > 2) st.template lift<2, 1>(p, q, C, lane); break;
+        case 3: if constexpr (NQ > 3) st.template lift<3, 1>(p, q, C, lane); break;
+        case 4: if constexpr (NQ > 4) st.template lift<4, 1>(p, q, C, lane); break;
+        default: break;
+      }
+    }
+  }
+
+  // One chunk: lane q < nq supplies (code_q, theta_q) for position base+q.
+  __device__ __forceinline__ void chunk(int code, double theta, int nq, FastChunk& sm, int lane) {
+    int info = GT_DIAG;  // lanes past the end: neutral diagonal with an empty mask
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    if (lane < nq) prepare(code, theta, info, c0, c1, c2);
+    sm.info[lane] = info;
+    sm.c0[lane] = c0;
+    sm.c1[lane] = c1;
+    sm.c2[lane] = c2;
+    __syncwarp();
+    const int row = lane;  // physical row whose phase this lane carries
+    const bool has_row = lane < G::D;
+#pragma unroll 1
+    for (int q = 0; q < nq; ++q) {
+      const int inf = sm.info[q];
+      const int type = inf & 3;
+      if (type == GT_DIAG) {
+        if (__popc(row & (inf >> 8)) & 1) phi += sm.c0[q];
+        continue;
+      }
+      const int b = inf >> 8;
+      const int m = 1 << b;
+      const double other = __shfl_xor_sync(0xffffffffu, phi, m);
+      const double delta = (has_row && (row & m)) ? phi - other : 0.0;
+      if (__any_sync(0xffffffffu, delta != 0.0)) {
+        double ds = 0.0, dc = 1.0;
+        if (delta != 0.0) sincos(delta, &ds, &dc);
+        sm.fac[lane] = make_double2(dc, ds);
+        __syncwarp();
+        flush(b, sm.fac, lane);
+        __syncwarp();
+        if (row & m) phi = other;
+      }
+      rotate(type, b, sm.c0[q], sm.c1[q], sm.c2[q], lane);
+    }
+    __syncwarp();
+  }
+
+  // Fitness from the final state (fitness.py:36-49).
+  __device__ __forceinline__ double finish(const double2* __restrict__ T, FastChunk& sm, int lane) {
+    if (lane < G::D) {
+      double s, c;
+      sincos(phi, &s, &c);
+      sm.fac[lane] = make_double2(c, -s);
+    }
+    __syncwarp();
+    const int j = lane & (G::D - 1);
+    const int h = (lane >> NQ) & (G::LPC - 1);
+    double ar = 0.0, ai = 0.0;
+#pragma unroll
+    for (int r = 0; r < G::E; ++r) {
+      const int k = h * G::E + r;
+      const double2 t = T[k * G::D + j];
+      const double2 w = sm.fac[k];
+      // p = conj(x) * t ; acc += w * p
+      const double pr = fma(st.re[r], t.x, st.im[r] * t.y);
+      const double pi = fma(st.re[r], t.y, -st.im[r] * t.x);
+      ar = fma(w.x, pr, fma(-w.y, pi, ar));
+      ai = fma(w.x, pi, fma(w.y, pr, ai));
+    }
+#pragma unroll
+    for (int off = G::ACTIVE / 2; off >= 1; off >>= 1) {
+      ar += __shfl_xor_sync(0xffffffffu, ar, off);
+      ai += __shfl_xor_sync(0xffffffffu, ai, off);
+    }
+    __syncwarp();
+    return fitness_from_overlap(hypot(ar, ai), G::D);
+  }
+};
+
+}  // namespace isq

@@ -2,6 +2,7 @@
 // readout, the functional API).  Replaces compose_gates + fitness_value
 // (gates.py:187-195, fitness.py:36-49) for a batch of circuits.
 #include "isq_internal.h"
+#include "fitness_warp.cuh"
 #include "unitary_warp.cuh"
 
 namespace isq {
@@ -12,9 +13,46 @@ struct ChunkShared {
   double b[32];
 };
 
+// Fitness only (the hot path): diagonal-phase accumulation + Pauli frame.
 template <int NQ>
 __global__ void __launch_bounds__(kThreadsPerBlock)
-    fitness_batch_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
+    fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
+                        const double* __restrict__ thetas, const double2* __restrict__ target,
+                        double* __restrict__ fitness) {
+  using G = Geo<NQ>;
+  __shared__ double2 Ts[G::D * G::D];
+  __shared__ FastChunk sh[kWarpsPerBlock];
+  for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  FastChunk& cs = sh[wib];
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t c = (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < count; c += nwarps) {
+    FastEval<NQ> ev;
+    ev.begin(lane);
+    const uint8_t* cc = codes + c * (int64_t)L;
+    const double* ct = thetas + c * (int64_t)L;
+    for (int base = 0; base < L; base += 32) {
+      const int p = base + lane;
+      const int nq = min(32, L - base);
+      int code = 0;
+      double th = 0.0;
+      if (lane < nq) {
+        code = cc[p];
+        th = ct[p];
+      }
+      ev.chunk(code, th, nq, cs, lane);
+    }
+    const double f = ev.finish(Ts, cs, lane);
+    if (lane == 0) fitness[c] = f;
+  }
+}
+
+// Composition with the exact global phase (compose_gates readout) + fitness.
+template <int NQ>
+__global__ void __launch_bounds__(kThreadsPerBlock)
+    compose_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                          const double* __restrict__ thetas, const double2* __restrict__ target,
                          double* __restrict__ fitness, double2* __restrict__ unitary) {
   using G = Geo<NQ>;
@@ -53,6 +91,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock)
       cs.b[lane] = g.b;
       __syncwarp();
       const int nq = min(32, L - base);
+#pragma unroll 1
       for (int q = 0; q < nq; ++q) st.apply(cs.op[q], cs.a[q], cs.b[q], lane);
       __syncwarp();
     }
@@ -139,9 +178,17 @@ template <int NQ>
 static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const double* thetas,
                             const double* target, double* fitness, double* unitary,
                             cudaStream_t stream) {
-  const void* k = (const void*)fitness_batch_kernel<NQ>;
+  if (unitary == nullptr) {
+    const void* k = (const void*)fitness_fast_kernel<NQ>;
+    const int grid = persistent_grid(k, 0, count);
+    fitness_fast_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
+        count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness);
+    ISQ_CUDA_TRY(cudaGetLastError());
+    return ISQ_OK;
+  }
+  const void* k = (const void*)compose_kernel<NQ>;
   const int grid = persistent_grid(k, 0, count);
-  fitness_batch_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
+  compose_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
       count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness,
       reinterpret_cast<double2*>(unitary));
   ISQ_CUDA_TRY(cudaGetLastError());

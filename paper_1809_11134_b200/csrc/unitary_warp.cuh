@@ -196,10 +196,61 @@ struct WarpUnitary {
     }
   }
 
+  // Rotation by a plane angle a (|a| <= pi/2) of the (ar, bi), (br, ai) planes
+  // (AX = 0, Rx) or the (ar, br), (ai, bi) planes (AX = 1, Ry) of every row
+  // pair across row bit RB.  Register bits use the in-place 3-shear lifting
+  //   x += p y ; y += q x ; x += p y      (p = -tan(a/2), q = sin a)
+  // so no temporaries survive the case (no register moves); lane bits use the
+  // direct form with (C, S) = (cos a, sin a) on the shuffled partner.
+  template <int RB, int AX>
+  __device__ __forceinline__ void lift(double p, double q, double C, int lane) {
+    if constexpr (RB < G::EB) {
+      constexpr int m = 1 << RB;
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        if (r & m) continue;
+        const int r1 = r | m;
+        if constexpr (AX == 0) {
+          re[r] = fma(p, im[r1], re[r]);
+          im[r1] = fma(q, re[r], im[r1]);
+          re[r] = fma(p, im[r1], re[r]);
+          re[r1] = fma(p, im[r], re[r1]);
+          im[r] = fma(q, re[r1], im[r]);
+          re[r1] = fma(p, im[r], re[r1]);
+        } else {
+          re[r] = fma(p, re[r1], re[r]);
+          re[r1] = fma(q, re[r], re[r1]);
+          re[r] = fma(p, re[r1], re[r]);
+          im[r] = fma(p, im[r1], im[r]);
+          im[r1] = fma(q, im[r], im[r1]);
+          im[r] = fma(p, im[r1], im[r]);
+        }
+      }
+    } else {
+      constexpr int lb = RB - G::EB;
+      constexpr int lmask = G::D << lb;
+      const bool hi = (lane >> (NQ + lb)) & 1;
+      const double S = (AX == 1 && !hi) ? -q : q;
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const double yr = __shfl_xor_sync(0xffffffffu, re[r], lmask);
+        const double yi = __shfl_xor_sync(0xffffffffu, im[r], lmask);
+        if constexpr (AX == 0) {  // x' = C x + i S y
+          re[r] = fma(C, re[r], -S * yi);
+          im[r] = fma(C, im[r], S * yr);
+        } else {  // x' = C x + sigma S y
+          re[r] = fma(C, re[r], S * yr);
+          im[r] = fma(C, im[r], S * yi);
+        }
+      }
+    }
+  }
+
   __device__ __forceinline__ void cmul(int r, double fc, double fs) {
-    const double xr = re[r], xi = im[r];
-    re[r] = fma(fc, xr, -fs * xi);
-    im[r] = fma(fc, xi, fs * xr);
+    const double t1 = fs * im[r];
+    const double t2 = fs * re[r];
+    re[r] = fma(fc, re[r], -t1);
+    im[r] = fma(fc, im[r], t2);
   }
 
   // Rz phase form: rows with the wire bit set pick up e^{i th}.

@@ -13,15 +13,24 @@ from paper_1809_11134_b200 import _lib
 
 
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--no-peak", action="store_true")
+    args_ = ap.parse_args()
     lib = _lib.load()
-    res = {}
-    for fp64 in (1, 0):
+    res = {"fp64_peak_tflops": 36.5}
+    for fp64 in (() if args_.no_peak else (1, 0)):
         v = ctypes.c_double()
         _lib.check(lib.isq_fma_peak(fp64, 0, ctypes.cast(ctypes.pointer(v), ctypes.c_void_p)))
         res["fp64_peak_tflops" if fp64 else "fp32_peak_tflops"] = v.value / 1e12
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream()
     for n, L, count in [(3, 16, 1 << 20), (4, 32, 1 << 18), (5, 64, 1 << 16), (5, 64, 1 << 18)]:
+        if args_.only and f"n{n}" != args_.only:
+            continue
         nc = 3 * n + n * (n - 1) // 2
         g = torch.Generator(device=dev).manual_seed(1)
         codes = torch.randint(0, nc, (count, L), device=dev, dtype=torch.uint8, generator=g)
@@ -34,7 +43,7 @@ def main():
             _lib.check(lib.isq_fitness_batch_device(*args))
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 10
+        reps = args_.reps
         e0.record()
         for _ in range(reps):
             lib.isq_fitness_batch_device(*args)
