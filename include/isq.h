@@ -83,6 +83,81 @@ isq_status isq_fitness_of_unitaries(int64_t dim, int64_t count, const double* un
 void isq_philox_block(uint64_t seed, uint64_t domain, uint64_t gen, uint64_t index, uint64_t sub,
                       uint64_t block, uint64_t* out);
 
+/* ------------------------------------------------------------------------
+ * QEQEA engine (QeqeaEngine, engine.py:266-384).  One handle owns one device
+ * bank: committed angles theta[Q], qutrit amplitudes qamp[3][Qt] (complex,
+ * axis-major), slot_max[Q], plus per-generation scratch.  Every random draw
+ * comes from the counter streams documented in csrc/np_random.cuh, so a
+ * generation's result depends only on (seed, generation, bank).
+ * ---------------------------------------------------------------------- */
+typedef struct isq_qeqea_config {
+  int32_t number_of_wires;          /* PopulationConfig.number_of_wires      */
+  int32_t size_of_individual;       /* PopulationConfig.size_of_individual   */
+  int64_t size_of_population;       /* PopulationConfig.size_of_population   */
+  double probability_of_mutation;   /* default 0.3  (engine.py:38)           */
+  double mutation_range;            /* default pi/4 (engine.py:39)           */
+  int32_t n_meas;                   /* default 1    (engine.py:40)           */
+  int32_t rank;                     /* this process's shard of the circuits  */
+  int64_t max_generations;          /* default 10,000,000                    */
+  double target_fitness;            /* default 0.999                         */
+  uint64_t seed;
+  int32_t world;                    /* number of ranks sharing the population */
+  int32_t reserved;
+} isq_qeqea_config;
+
+typedef struct isq_generation_record {
+  double gen_best;      /* step() return value 0: max fitness of the generation  */
+  double gen_mean;      /* step() return value 1: mean fitness of the generation */
+  double best_fitness;  /* engine.best_fitness after the generation              */
+  double reserved;
+} isq_generation_record;
+
+/* Create a handle (PopulationConfig validation engine.py:45-63 ->
+ * ISQ_ERR_CONFIG) and initialise the bank on the device from the init streams.
+ * target: 2*D*D doubles.  max_batch: record capacity = most generations per
+ * isq_qeqea_step call / per begin_batch..read_batch window. */
+isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, int32_t device,
+                            int32_t max_batch, void** handle);
+isq_status isq_qeqea_destroy(void* handle);
+/* Enqueue all subsequent work on an external cudaStream_t (e.g. the stream the
+ * caller runs its NCCL collectives on). */
+isq_status isq_qeqea_set_stream(void* handle, void* stream);
+/* Run up to n generations (QeqeaEngine.step x n, single rank) entirely on the
+ * device; stops exactly at the first generation meeting a stop rule
+ * (engine.py:354-358).  records[i] describes the i-th generation run; *stop_reason
+ * is 0 (running), 1 (target-reached) or 2 (generation-limit). */
+isq_status isq_qeqea_step(void* handle, int32_t n, isq_generation_record* records,
+                          int32_t* n_done, int32_t* stop_reason);
+/* Split-phase generation for world > 1: begin_batch marks the record window,
+ * eval scores this rank's circuit shard into the fitness buffer
+ * (isq_qeqea_buffers: rank r owns [r*shard, (r+1)*shard)), the caller
+ * all-gathers that buffer in place on the handle's stream, finish replays the
+ * reductions, commit and table update identically on every rank. */
+isq_status isq_qeqea_begin_batch(void* handle);
+isq_status isq_qeqea_eval(void* handle);
+isq_status isq_qeqea_finish(void* handle);
+isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
+                                int32_t* stop_reason, uint64_t* generation, double* best_fitness);
+isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream);
+/* engine.best_gates / best_fitness (gate codes + angles of length L). */
+isq_status isq_qeqea_best(void* handle, uint8_t* codes, double* thetas, double* fitness);
+/* Committed bank + table + counters (pickling, engine.py:301-304); set_state
+ * also serves init from host arrays (init_population injection). */
+isq_status isq_qeqea_get_state(void* handle, double* theta, double* qamp, double* slot_max,
+                               uint64_t* generation, double* best_fitness, int32_t* stop);
+isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* qamp,
+                               const double* slot_max, uint64_t generation, double best_fitness,
+                               int32_t stop, const uint8_t* best_codes, const double* best_thetas);
+/* engine.pop: the live bank (committed values with the pending mutation of
+ * the last generation applied); qutrits as Qt x 3 complex (numpy layout). */
+isq_status isq_qeqea_live_population(void* handle, double* theta, double* qutrits);
+/* Blueprints (flat slots), measured gate codes and live angles of circuits
+ * [c0, c1) at the current generation (sample_circuit + construct_segments). */
+isq_status isq_qeqea_sample(void* handle, int64_t c0, int64_t c1, int64_t* flats, uint8_t* codes,
+                            double* thetas);
+/* Fitness vector of the last evaluated generation (P doubles). */
+isq_status isq_qeqea_fitness(void* handle, double* out);
+
 /* Diagnostics: measured FP64 (fp64 != 0) or FP32 CUDA-core FMA peak in flop/s
  * on `device` (roofline denominator of the fitness kernel). */
 isq_status isq_fma_peak(int32_t fp64, int32_t device, double* flops_per_s);

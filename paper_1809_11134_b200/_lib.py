@@ -38,7 +38,43 @@ c_u8p = ctypes.POINTER(ctypes.c_uint8)
 
 # name -> (restype, argtypes).  Kept in sync with include/isq.h (a CPU test
 # checks that every declared symbol is exported and listed here).
+class QeqeaConfig(ctypes.Structure):
+    _fields_ = [
+        ("number_of_wires", c_i32),
+        ("size_of_individual", c_i32),
+        ("size_of_population", c_i64),
+        ("probability_of_mutation", c_dbl),
+        ("mutation_range", c_dbl),
+        ("n_meas", c_i32),
+        ("rank", c_i32),
+        ("max_generations", c_i64),
+        ("target_fitness", c_dbl),
+        ("seed", c_u64),
+        ("world", c_i32),
+        ("reserved", c_i32),
+    ]
+
+
+GEN_RECORD = np.dtype([("gen_best", "f8"), ("gen_mean", "f8"), ("best_fitness", "f8"), ("reserved", "f8")])
+
+c_i32p = ctypes.POINTER(c_i32)
+
 SIGNATURES: dict[str, tuple] = {
+    "isq_qeqea_create": (c_i32, [ctypes.POINTER(QeqeaConfig), c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "isq_qeqea_destroy": (c_i32, [c_vp]),
+    "isq_qeqea_set_stream": (c_i32, [c_vp, c_vp]),
+    "isq_qeqea_step": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "isq_qeqea_begin_batch": (c_i32, [c_vp]),
+    "isq_qeqea_eval": (c_i32, [c_vp]),
+    "isq_qeqea_finish": (c_i32, [c_vp]),
+    "isq_qeqea_read_batch": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "isq_qeqea_buffers": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "isq_qeqea_best": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "isq_qeqea_get_state": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "isq_qeqea_set_state": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_u64, c_dbl, c_i32, c_vp, c_vp]),
+    "isq_qeqea_live_population": (c_i32, [c_vp, c_vp, c_vp]),
+    "isq_qeqea_sample": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "isq_qeqea_fitness": (c_i32, [c_vp, c_vp]),
     "isq_last_error": (ctypes.c_char_p, []),
     "isq_abi_version": (c_i32, []),
     "isq_fitness_batch": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),

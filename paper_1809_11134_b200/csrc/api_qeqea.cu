@@ -1,0 +1,385 @@
+// C ABI of the QEQEA engine handle (QeqeaEngine, engine.py:266-384).
+#include <cstring>
+#include <string>
+
+#include "qeqea_internal.h"
+
+namespace isq {
+
+struct QeqeaHandle {
+  QeqeaArgs a;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  int64_t shard = 0;  // circuits per rank (padded)
+  int max_batch = 0;
+  GenRecord* h_records = nullptr;  // pinned
+  QeqeaDevState* h_state = nullptr;  // pinned
+};
+
+static void free_handle(QeqeaHandle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  QeqeaArgs& a = h->a;
+  cudaFree(a.theta);
+  cudaFree(a.qamp);
+  cudaFree(a.slot_max);
+  cudaFree(a.claim);
+  cudaFree(a.fitness);
+  cudaFree(a.flats);
+  cudaFree(a.st);
+  cudaFree(a.records);
+  cudaFree(a.best_codes);
+  cudaFree(a.best_thetas);
+  cudaFree((void*)a.target);
+  cudaFree(a.part_max);
+  cudaFree(a.part_sum);
+  cudaFree(a.part_arg);
+  if (h->h_records) cudaFreeHost(h->h_records);
+  if (h->h_state) cudaFreeHost(h->h_state);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+static isq_status validate(const isq_qeqea_config* c) {
+  auto bad = [](const std::string& m) {
+    set_error(m);
+    return ISQ_ERR_CONFIG;
+  };
+  if (c->number_of_wires < 2) return bad("numberOfWires must be ≥ 2");
+  if (c->size_of_individual < 1 || c->size_of_population < 1)
+    return bad("sizeOfIndividual and sizeOfPopulation must be ≥ 1");
+  if (!(c->probability_of_mutation >= 0.0 && c->probability_of_mutation <= 1.0))
+    return bad("probabilityOfMutation must be in [0, 1]");
+  if (!(c->mutation_range > 0.0)) return bad("mutationRange must be > 0");
+  if (c->n_meas < 1) return bad("nMeas must be ≥ 1");
+  if (c->max_generations < 1) return bad("maxGenerations must be ≥ 1");
+  if (!(c->target_fitness > 0.0 && c->target_fitness <= 1.0))
+    return bad("targetFitness must be in (0, 1]");
+  if (c->number_of_wires > ISQ_MAX_WIRES) {
+    set_error("numberOfWires=" + std::to_string(c->number_of_wires) +
+              " exceeds the device kernels (compiled for 2..5 wires)");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  if (c->n_meas > 60) {
+    set_error("nMeas > 60 needs numpy's BTPE binomial branch, which this build does not implement");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  if (c->size_of_individual > 4096) {
+    set_error("sizeOfIndividual > 4096 is not supported by the device engine");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  const int64_t n = c->number_of_wires;
+  const int64_t K = n + n * (n - 1) / 2;
+  const int64_t Q = K * c->size_of_population * c->size_of_individual;
+  if (Q >= (1LL << 32) - 1) {
+    set_error("qubit_count = K*P*L must stay below 2^32 for the device engine");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad("invalid rank/world");
+  return ISQ_OK;
+}
+
+#define TRYA(expr)                                                   \
+  do {                                                               \
+    cudaError_t _e = (expr);                                         \
+    if (_e != cudaSuccess) {                                         \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+      free_handle(h);                                                \
+      return ISQ_ERR_CUDA;                                           \
+    }                                                                \
+  } while (0)
+
+}  // namespace isq
+
+using namespace isq;
+
+extern "C" {
+
+isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, int32_t device,
+                            int32_t max_batch, void** out) {
+  *out = nullptr;
+  isq_status st = validate(cfg);
+  if (st != ISQ_OK) return st;
+  QeqeaHandle* h = new QeqeaHandle();
+  h->device = device;
+  h->rank = cfg->rank;
+  h->world = cfg->world;
+  h->max_batch = max_batch < 1 ? 1 : max_batch;
+  QeqeaArgs& a = h->a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = cfg->number_of_wires;
+  a.L = cfg->size_of_individual;
+  a.P = cfg->size_of_population;
+  a.K = a.n + a.n * (a.n - 1) / 2;
+  a.Q = a.K * a.P * a.L;
+  a.Qt = (int64_t)a.n * a.P * a.L;
+  a.p_mut = cfg->probability_of_mutation;
+  a.mutation_range = cfg->mutation_range;
+  a.target_fitness = cfg->target_fitness;
+  a.n_meas = cfg->n_meas;
+  a.max_generations = (uint64_t)cfg->max_generations;
+  a.seed = cfg->seed;
+  a.rec_cap = h->max_batch;
+  h->shard = (a.P + h->world - 1) / h->world;
+  const int64_t D = 1LL << a.n;
+  TRYA(cudaSetDevice(device));
+  TRYA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->own_stream = true;
+  TRYA(cudaMalloc((void**)&a.theta, a.Q * 8));
+  TRYA(cudaMalloc((void**)&a.qamp, a.Qt * 3 * 16));
+  TRYA(cudaMalloc((void**)&a.slot_max, a.Q * 8));
+  TRYA(cudaMalloc((void**)&a.claim, a.Q * 4));
+  TRYA(cudaMalloc((void**)&a.fitness, h->shard * h->world * 8));
+  TRYA(cudaMalloc((void**)&a.flats, a.P * a.L * 4));
+  TRYA(cudaMalloc((void**)&a.st, sizeof(QeqeaDevState)));
+  TRYA(cudaMalloc((void**)&a.records, sizeof(GenRecord) * h->max_batch));
+  TRYA(cudaMalloc((void**)&a.best_codes, a.L));
+  TRYA(cudaMalloc((void**)&a.best_thetas, a.L * 8));
+  TRYA(cudaMalloc((void**)&a.target, D * D * 16));
+  a.n_parts = (int)((a.P + 4095) / 4096);
+  if (a.n_parts > 1024) a.n_parts = 1024;
+  if (a.n_parts < 1) a.n_parts = 1;
+  TRYA(cudaMalloc((void**)&a.part_max, a.n_parts * 8));
+  TRYA(cudaMalloc((void**)&a.part_sum, a.n_parts * 8));
+  TRYA(cudaMalloc((void**)&a.part_arg, a.n_parts * 8));
+  TRYA(cudaMallocHost((void**)&h->h_records, sizeof(GenRecord) * h->max_batch));
+  TRYA(cudaMallocHost((void**)&h->h_state, sizeof(QeqeaDevState)));
+  TRYA(cudaMemcpyAsync((void*)a.target, target, D * D * 16, cudaMemcpyHostToDevice, h->stream));
+  QeqeaDevState s0;
+  std::memset(&s0, 0, sizeof(s0));
+  s0.best_circuit = -1;
+  *h->h_state = s0;
+  TRYA(cudaMemcpyAsync(a.st, h->h_state, sizeof(s0), cudaMemcpyHostToDevice, h->stream));
+  TRYA(cudaMemsetAsync(a.best_codes, 0, a.L, h->stream));
+  TRYA(cudaMemsetAsync(a.best_thetas, 0, a.L * 8, h->stream));
+  TRYA(cudaMemsetAsync(a.fitness, 0, h->shard * h->world * 8, h->stream));
+  if (qeqea_launch_init(a, h->stream) != ISQ_OK) {
+    free_handle(h);
+    return ISQ_ERR_CUDA;
+  }
+  TRYA(cudaStreamSynchronize(h->stream));
+  *out = h;
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_destroy(void* handle) {
+  free_handle(static_cast<QeqeaHandle*>(handle));
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_set_stream(void* handle, void* stream) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  h->own_stream = false;
+  h->stream = (cudaStream_t)stream;
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_begin_batch(void* handle) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  // rec_base := generation (device-side copy, stream ordered)
+  ISQ_CUDA_TRY(cudaMemcpyAsync(&h->a.st->rec_base, &h->a.st->generation, 8,
+                               cudaMemcpyDeviceToDevice, h->stream));
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_eval(void* handle) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t c0 = h->rank * h->shard;
+  const int64_t c1 = c0 + h->shard < h->a.P ? c0 + h->shard : h->a.P;
+  return qeqea_launch_eval(h->a, c0, c1, h->stream);
+}
+
+isq_status isq_qeqea_finish(void* handle) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  return qeqea_launch_finish(h->a, h->stream);
+}
+
+isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
+                                int32_t* stop_reason, uint64_t* generation, double* best_fitness) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaMemcpyAsync(h->h_state, h->a.st, sizeof(QeqeaDevState), cudaMemcpyDeviceToHost,
+                               h->stream));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  const QeqeaDevState s = *h->h_state;
+  int64_t done = (int64_t)(s.generation - s.rec_base);
+  if (done > h->max_batch) done = h->max_batch;
+  if (done > 0 && records) {
+    ISQ_CUDA_TRY(cudaMemcpy(h->h_records, h->a.records, sizeof(GenRecord) * done,
+                            cudaMemcpyDeviceToHost));
+    std::memcpy(records, h->h_records, sizeof(GenRecord) * done);
+  }
+  if (n_done) *n_done = (int32_t)done;
+  if (stop_reason) *stop_reason = s.stop;
+  if (generation) *generation = s.generation;
+  if (best_fitness) *best_fitness = s.best_fitness;
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_record* records,
+                          int32_t* n_done, int32_t* stop_reason) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (h->world != 1) {
+    set_error("isq_qeqea_step drives a single rank; use eval / all-gather / finish for world > 1");
+    return ISQ_ERR_CONFIG;
+  }
+  if (n_generations > h->max_batch) {
+    set_error("n_generations exceeds the handle's record capacity (max_batch)");
+    return ISQ_ERR_CONFIG;
+  }
+  isq_status st = isq_qeqea_begin_batch(handle);
+  if (st != ISQ_OK) return st;
+  for (int i = 0; i < n_generations; ++i) {
+    st = qeqea_launch_eval(h->a, 0, h->a.P, h->stream);
+    if (st != ISQ_OK) return st;
+    st = qeqea_launch_finish(h->a, h->stream);
+    if (st != ISQ_OK) return st;
+  }
+  return isq_qeqea_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
+}
+
+isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len,
+                             void** stream) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (fitness_dev) *fitness_dev = h->a.fitness;
+  if (shard_len) *shard_len = h->shard;
+  if (stream) *stream = h->stream;
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_best(void* handle, uint8_t* codes, double* thetas, double* fitness) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  ISQ_CUDA_TRY(cudaMemcpy(codes, h->a.best_codes, h->a.L, cudaMemcpyDeviceToHost));
+  ISQ_CUDA_TRY(cudaMemcpy(thetas, h->a.best_thetas, h->a.L * 8, cudaMemcpyDeviceToHost));
+  QeqeaDevState s;
+  ISQ_CUDA_TRY(cudaMemcpy(&s, h->a.st, sizeof(s), cudaMemcpyDeviceToHost));
+  *fitness = s.best_fitness;
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_get_state(void* handle, double* theta, double* qamp, double* slot_max,
+                               uint64_t* generation, double* best_fitness, int32_t* stop) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  const QeqeaArgs& a = h->a;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (theta) ISQ_CUDA_TRY(cudaMemcpy(theta, a.theta, a.Q * 8, cudaMemcpyDeviceToHost));
+  if (qamp) ISQ_CUDA_TRY(cudaMemcpy(qamp, a.qamp, a.Qt * 48, cudaMemcpyDeviceToHost));
+  if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(slot_max, a.slot_max, a.Q * 8, cudaMemcpyDeviceToHost));
+  QeqeaDevState s;
+  ISQ_CUDA_TRY(cudaMemcpy(&s, a.st, sizeof(s), cudaMemcpyDeviceToHost));
+  if (generation) *generation = s.generation;
+  if (best_fitness) *best_fitness = s.best_fitness;
+  if (stop) *stop = s.stop;
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* qamp,
+                               const double* slot_max, uint64_t generation, double best_fitness,
+                               int32_t stop, const uint8_t* best_codes, const double* best_thetas) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  const QeqeaArgs& a = h->a;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (theta) ISQ_CUDA_TRY(cudaMemcpy(a.theta, theta, a.Q * 8, cudaMemcpyHostToDevice));
+  if (qamp) ISQ_CUDA_TRY(cudaMemcpy(a.qamp, qamp, a.Qt * 48, cudaMemcpyHostToDevice));
+  if (slot_max)
+    ISQ_CUDA_TRY(cudaMemcpy(a.slot_max, slot_max, a.Q * 8, cudaMemcpyHostToDevice));
+  else
+    ISQ_CUDA_TRY(cudaMemset(a.slot_max, 0, a.Q * 8));
+  ISQ_CUDA_TRY(cudaMemset(a.claim, 0, a.Q * 4));
+  if (best_codes) ISQ_CUDA_TRY(cudaMemcpy(a.best_codes, best_codes, a.L, cudaMemcpyHostToDevice));
+  if (best_thetas)
+    ISQ_CUDA_TRY(cudaMemcpy(a.best_thetas, best_thetas, a.L * 8, cudaMemcpyHostToDevice));
+  QeqeaDevState s;
+  std::memset(&s, 0, sizeof(s));
+  s.generation = generation;
+  s.rec_base = generation;
+  s.best_fitness = best_fitness;
+  s.best_circuit = -1;
+  s.stop = stop;
+  ISQ_CUDA_TRY(cudaMemcpy(a.st, &s, sizeof(s), cudaMemcpyHostToDevice));
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_live_population(void* handle, double* theta, double* qutrits) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  const QeqeaArgs& a = h->a;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  double *d_t = nullptr, *d_q = nullptr;
+  ISQ_CUDA_TRY(cudaMalloc((void**)&d_t, a.Q * 8));
+  cudaError_t e = cudaMalloc((void**)&d_q, a.Qt * 48 + 16);
+  if (e != cudaSuccess) {
+    cudaFree(d_t);
+    set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return ISQ_ERR_CUDA;
+  }
+  isq_status st = qeqea_launch_live(a, d_t, d_q, h->stream);
+  if (st == ISQ_OK) {
+    e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(theta, d_t, a.Q * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && qutrits) e = cudaMemcpy(qutrits, d_q, a.Qt * 48, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      set_error(std::string("live population: ") + cudaGetErrorString(e));
+      st = ISQ_ERR_CUDA;
+    }
+  }
+  cudaFree(d_t);
+  cudaFree(d_q);
+  return st;
+}
+
+isq_status isq_qeqea_sample(void* handle, int64_t c0, int64_t c1, int64_t* flats, uint8_t* codes,
+                            double* thetas) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  const QeqeaArgs& a = h->a;
+  if (c0 < 0 || c1 > a.P || c1 < c0) {
+    set_error("circuit range out of bounds");
+    return ISQ_ERR_CONFIG;
+  }
+  if (c1 == c0) return ISQ_OK;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t n = (c1 - c0) * a.L;
+  int64_t* d_f = nullptr;
+  uint8_t* d_c = nullptr;
+  double* d_t = nullptr;
+  ISQ_CUDA_TRY(cudaMalloc((void**)&d_f, n * 8));
+  ISQ_CUDA_TRY(cudaMalloc((void**)&d_c, n));
+  ISQ_CUDA_TRY(cudaMalloc((void**)&d_t, n * 8));
+  isq_status st = qeqea_launch_sample(a, c0, c1, d_f, d_c, d_t, h->stream);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (st == ISQ_OK && e == cudaSuccess) {
+    cudaMemcpy(flats, d_f, n * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(codes, d_c, n, cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(thetas, d_t, n * 8, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d_f);
+  cudaFree(d_c);
+  cudaFree(d_t);
+  if (st == ISQ_OK && e != cudaSuccess) {
+    set_error(std::string("sample: ") + cudaGetErrorString(e));
+    st = ISQ_ERR_CUDA;
+  }
+  return st;
+}
+
+isq_status isq_qeqea_fitness(void* handle, double* out) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  ISQ_CUDA_TRY(cudaMemcpy(out, h->a.fitness, h->a.P * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+}  // extern "C"
