@@ -1,0 +1,335 @@
+"""Benchmark of the QEQEA generation loop (BASELINE.json metric: circuit
+fitness evals/sec, whole box; generations/sec).
+
+Workload (config C5 of BASELINE.json, the largest single-GPU configuration):
+one step = one full QEQEA generation (sample + measure + lazy mutation +
+compose + score 2^20 circuits of 64 gates on 5 qubits, reductions, commit,
+table update) over a device-resident bank of 1.0e9 slots (36 GB, far above the
+126 MB L2), Haar-random target.  At N > 1 (torchrun) the 2^20 circuits are
+sharded over the ranks and the per-generation fitness vector is all-gathered
+over NCCL; every rank replays the O(P*L) commit.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference algorithm's CPU path (the oracle port
+of evaluate_circuit, dense kron-matmul per gate) on all host cores for a
+bounded sample of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "circuit fitness evals/sec (whole box) at 3–5 qubits; generations/sec"
+N, L, P = 5, 64, 1 << 20
+
+
+def canonical_flops(n: int, L: int) -> int:
+    """F(n, L) = (6L + 8) 4^n real flops per fitness eval."""
+    return (6 * L + 8) * 4 ** n
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- helpers --
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def cpu_reference_sample(steps: int, warmup: int, per_worker: int):
+    """The reference algorithm's CPU path on all host cores (oracle port)."""
+    from oracle.cpu_baseline import CpuPool, haar_target, qeqea_like_circuits
+
+    pool = CpuPool()
+    T = haar_target(N)
+    count = per_worker * pool.workers
+    times, evals = [], 0
+    for i in range(warmup + steps):
+        codes, thetas = qeqea_like_circuits(N, L, count, seed=1000 + i)
+        _, wall = pool.evaluate(N, codes, thetas, T)
+        if i >= warmup:
+            times.append(wall)
+            evals += count
+    pool.close()
+    total = sum(times)
+    return {
+        "value": evals / total,
+        "unit": "evals/s",
+        "cores": pool.workers,
+        "kind": "port",
+        "sample": (f"{count} C5-shaped circuits (n=5, L=64, QEQEA gate mix, Haar target) per step, "
+                   f"oracle restatement of evaluate_circuit (dense kron matmul per gate), "
+                   f"ProcessPool x{pool.workers}, OPENBLAS_NUM_THREADS=1"),
+        "ms_per_step": 1000.0 * total / max(1, len(times)),
+    }
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cb = cpu_reference_sample(args.steps, args.warmup, per_worker=args.cpu_per_worker)
+    emit({
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5 fitness evals (bounded sample per step)", "n": N, "L": L, "P": P},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
+
+
+class _CAI:
+    """__cuda_array_interface__ wrapper over a libisq-owned device buffer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from oracle.cpu_baseline import haar_target
+    from paper_1809_11134_b200 import _lib
+    from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
+    from paper_1809_11134_b200.fitness import TargetSpec
+
+    lib = _lib.load()
+    peak = ctypes.c_double()
+    _lib.check(lib.isq_fma_peak(1, local, ctypes.cast(ctypes.pointer(peak), ctypes.c_void_p)))
+    fp64_peak = peak.value / 1e12
+
+    T = haar_target(N)
+    cfg = PopulationConfig(number_of_wires=N, size_of_individual=L, size_of_population=P,
+                           max_generations=10_000_000, target_fitness=1.0)
+    eng = QeqeaEngine(cfg, TargetSpec("haar32", N, T), seed=2024, device=local, rank=rank, world=world,
+                      max_batch=max(args.steps + args.warmup, 1) + 1)
+    stream = torch.cuda.Stream(device=local)
+    _lib.check(lib.isq_qeqea_set_stream(eng._h, ctypes.c_void_p(stream.cuda_stream)))
+    fptr, shard = ctypes.c_void_p(), ctypes.c_int64()
+    _lib.check(lib.isq_qeqea_buffers(eng._h, ctypes.byref(fptr), ctypes.byref(shard), None))
+    full = torch.as_tensor(_CAI(fptr.value, shard.value * world), device=f"cuda:{local}")
+    mine = full[rank * shard.value:(rank + 1) * shard.value]
+    send = torch.empty_like(mine)
+
+    def generation():
+        _lib.check(lib.isq_qeqea_eval(eng._h))
+        if world > 1:
+            send.copy_(mine)
+            dist.all_gather_into_tensor(full, send)
+        _lib.check(lib.isq_qeqea_finish(eng._h))
+
+    with torch.cuda.stream(stream):
+        _lib.check(lib.isq_qeqea_begin_batch(eng._h))
+        for _ in range(args.warmup):
+            generation()
+        stream.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+               torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks = ClockSampler(local)
+        clocks.start()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            _lib.check(lib.isq_qeqea_eval(eng._h))
+            ev[i][1].record(stream)
+            if world > 1:
+                send.copy_(mine)
+                dist.all_gather_into_tensor(full, send)
+            _lib.check(lib.isq_qeqea_finish(eng._h))
+            ev[i][2].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    eval_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    fin_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    rec = np.zeros(args.steps + args.warmup, dtype=_lib.GEN_RECORD)
+    nd = ctypes.c_int32()
+    _lib.check(lib.isq_qeqea_read_batch(eng._h, _lib.ptr(rec), ctypes.byref(nd), None, None, None))
+    assert nd.value == args.steps + args.warmup, nd.value
+
+    evals_per_s = P * args.steps / (ms * 1e-3)
+    avg_eval_s = sum(eval_ms) / len(eval_ms) * 1e-3
+    shard_circuits = min(shard.value, P - rank * shard.value)
+    achieved = canonical_flops(N, L) * shard_circuits / avg_eval_s / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "traffic_eval_c5.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+
+    out = {
+        "metric": METRIC, "value": evals_per_s, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "C5: QEQEA generation, n=5 qubits, depth L=64, population 2^20, "
+                               "Haar-random 32x32 target; bank 1.0e9 slots (36 GB) resident in HBM",
+                   "n": N, "L": L, "P": P, "global_batch": P, "parallelism": f"dp{world} (circuit shards)",
+                   "l2": "inputs larger than L2 (36 GB bank vs 126 MB)"},
+        "gens_per_s": args.steps / (ms * 1e-3),
+        "phase_ms": {"eval": sum(eval_ms) / len(eval_ms), "finish": sum(fin_ms) / len(fin_ms)},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": traffic,
+                     "kernel": "qeqea_eval_kernel<5>",
+                     "peak_source": "FP64 CUDA-core FMA peak measured live by isq_fma_peak "
+                                    "(MEASURED_PEAKS.json carries no FP64 figure)",
+                     "work": "canonical F(n,L) = (6L+8) 4^n flop/eval (SURVEY.md §8d) x circuits per launch"},
+        "clocks": clk,
+        "gpu_launches": 6 * args.steps,
+        "best_fitness": float(rec["best_fitness"][-1]),
+    }
+
+    # e2e: the same metric through the C-ABI with host buffers (isq_fitness_batch:
+    # pinned host codes/angles -> device, fitness -> host inside the timed region)
+    if rank == 0 and not args.skip_e2e:
+        flats, codes, thetas = eng.sample(0, P)
+        hc = torch.empty((P, L), dtype=torch.uint8, pin_memory=True).numpy()
+        ht = torch.empty((P, L), dtype=torch.float64, pin_memory=True).numpy()
+        hf = torch.empty(P, dtype=torch.float64, pin_memory=True).numpy()
+        hc[:] = codes
+        ht[:] = thetas
+        Tc = np.ascontiguousarray(T, dtype=np.complex128)
+        for _ in range(max(1, args.warmup)):
+            _lib.check(lib.isq_fitness_batch(N, L, P, _lib.ptr(hc), _lib.ptr(ht), _lib.ptr(Tc), _lib.ptr(hf), None, local))
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _lib.check(lib.isq_fitness_batch(N, L, P, _lib.ptr(hc), _lib.ptr(ht), _lib.ptr(Tc), _lib.ptr(hf), None, local))
+        dt = time.perf_counter() - t0
+        out["e2e"] = {"value": P * args.steps / dt, "unit": "evals/s",
+                      "h2d_bytes_per_step": int(hc.nbytes + ht.nbytes + Tc.nbytes),
+                      "d2h_bytes_per_step": int(hf.nbytes),
+                      "path": "isq_fitness_batch (C ABI, pinned host buffers) on this generation's C5 circuits"}
+        # cross-check: fitness of the same circuits inside the engine generation
+        # (generation `warmup+steps` has not been evaluated yet, so compare the
+        # fitness_batch result against the oracle on a few circuits instead)
+        if not args.skip_cpu:
+            from oracle.cpu_baseline import CpuPool
+
+            pool = CpuPool()
+            m = args.cpu_per_worker * pool.workers
+            cpu_fit, wall = pool.evaluate(N, codes[:m], thetas[:m], T)
+            pool.close()
+            rel = np.abs(cpu_fit - hf[:m]) / np.maximum(np.abs(cpu_fit), 1e-300)
+            out["cpu_baseline"] = {
+                "value": m / wall, "unit": "evals/s", "cores": pool.workers, "kind": "port",
+                "sample": (f"first {m} circuits of the C5 generation, oracle restatement of evaluate_circuit "
+                           f"(dense kron matmul per gate), ProcessPool x{pool.workers}, OPENBLAS_NUM_THREADS=1"),
+                "parity_max_rel_err_vs_gpu": float(rel.max()),
+            }
+    if rank == 0:
+        emit(out)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-per-worker", type=int, default=400)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -29,6 +29,8 @@ static void free_handle(QeqeaHandle* h) {
   cudaFree(a.claim);
   cudaFree(a.fitness);
   cudaFree(a.flats);
+  cudaFree(a.gate_codes);
+  cudaFree(a.gate_thetas);
   cudaFree(a.st);
   cudaFree(a.records);
   cudaFree(a.best_codes);
@@ -134,6 +136,8 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   TRYA(cudaMalloc((void**)&a.claim, a.Q * 4));
   TRYA(cudaMalloc((void**)&a.fitness, h->shard * h->world * 8));
   TRYA(cudaMalloc((void**)&a.flats, a.P * a.L * 4));
+  TRYA(cudaMalloc((void**)&a.gate_codes, h->shard * a.L));
+  TRYA(cudaMalloc((void**)&a.gate_thetas, h->shard * a.L * 8));
   TRYA(cudaMalloc((void**)&a.st, sizeof(QeqeaDevState)));
   TRYA(cudaMalloc((void**)&a.records, sizeof(GenRecord) * h->max_batch));
   TRYA(cudaMalloc((void**)&a.best_codes, a.L));

@@ -56,6 +56,8 @@ struct QeqeaArgs {
   // per generation
   double* fitness;   // P (padded to world * shard)
   uint32_t* flats;   // P * L scratch between commit and table kernels
+  uint8_t* gate_codes;   // shard * L gate codes of the generation (params -> fitness)
+  double* gate_thetas;   // shard * L live angles
   QeqeaDevState* st;
   GenRecord* records;
   uint8_t* best_codes;   // L

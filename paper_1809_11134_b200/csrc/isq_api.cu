@@ -26,6 +26,9 @@ static isq_status check_shape(int32_t n, int32_t length, int64_t count) {
 
 static isq_status check_codes(int32_t n, const uint8_t* codes, int64_t total) {
   const int ncodes = 3 * n + n * (n - 1) / 2;
+  uint8_t mx = 0;
+  for (int64_t i = 0; i < total; ++i) mx = codes[i] > mx ? codes[i] : mx;  // vectorised max
+  if (mx < ncodes) return ISQ_OK;
   for (int64_t i = 0; i < total; ++i) {
     if (codes[i] >= ncodes) {
       set_error("gate code " + std::to_string((int)codes[i]) + " at index " + std::to_string(i) +

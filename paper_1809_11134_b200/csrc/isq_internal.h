@@ -32,6 +32,12 @@ isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* code
                                 const double* thetas, const double* target_dev,
                                 double* fitness_dev, double* unitary_dev, cudaStream_t stream);
 
+// fitness-only batch that skips all work once *stop != 0 (engine generations).
+isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
+                                          const double* thetas, const double* target_dev,
+                                          double* fitness_dev, const int32_t* stop,
+                                          cudaStream_t stream);
+
 isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, const double* T,
                                   double* out, cudaStream_t stream);
 

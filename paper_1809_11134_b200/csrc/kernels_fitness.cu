@@ -18,10 +18,11 @@ template <int NQ>
 __global__ void __launch_bounds__(kThreadsPerBlock)
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
-                        double* __restrict__ fitness) {
+                        double* __restrict__ fitness, const int32_t* __restrict__ stop) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
   __shared__ FastChunk sh[kWarpsPerBlock];
+  if (stop != nullptr && *stop) return;
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -182,7 +183,7 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
     const void* k = (const void*)fitness_fast_kernel<NQ>;
     const int grid = persistent_grid(k, 0, count);
     fitness_fast_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
-        count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness);
+        count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, nullptr);
     ISQ_CUDA_TRY(cudaGetLastError());
     return ISQ_OK;
   }
@@ -193,6 +194,34 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
       reinterpret_cast<double2*>(unitary));
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
+}
+
+template <int NQ>
+static isq_status launch_fast_stoppable(int L, int64_t count, const uint8_t* codes,
+                                        const double* thetas, const double* target, double* fitness,
+                                        const int32_t* stop, cudaStream_t stream) {
+  const void* k = (const void*)fitness_fast_kernel<NQ>;
+  const int grid = persistent_grid(k, 0, count);
+  fitness_fast_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
+      count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
+                                          const double* thetas, const double* target,
+                                          double* fitness, const int32_t* stop,
+                                          cudaStream_t stream) {
+  if (count <= 0) return ISQ_OK;
+  switch (n) {
+    case 2: return launch_fast_stoppable<2>(L, count, codes, thetas, target, fitness, stop, stream);
+    case 3: return launch_fast_stoppable<3>(L, count, codes, thetas, target, fitness, stop, stream);
+    case 4: return launch_fast_stoppable<4>(L, count, codes, thetas, target, fitness, stop, stream);
+    case 5: return launch_fast_stoppable<5>(L, count, codes, thetas, target, fitness, stop, stream);
+    default:
+      set_error("numberOfWires outside the compiled range 2..5");
+      return ISQ_ERR_UNSUPPORTED;
+  }
 }
 
 isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* codes,

@@ -19,41 +19,30 @@
 namespace isq {
 
 // ---------------------------------------------------------------- eval ---
+// Two kernels: `params` turns every (circuit, position) of the shard into a
+// gate (code, live angle) - sampling, lazy mutation, Born measurement - and
+// `fitness_fast_kernel` (kernels_fitness.cu) composes and scores them.
+// Splitting keeps each kernel's hot code inside the instruction cache.
 
-template <int NQ>
-__global__ void __launch_bounds__(kThreadsPerBlock) qeqea_eval_kernel(QeqeaArgs a, int64_t c0, int64_t c1) {
-  using G = Geo<NQ>;
-  __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kWarpsPerBlock];
+__global__ void __launch_bounds__(kThreadsPerBlock)
+    qeqea_params_kernel(QeqeaArgs a, int64_t c0, int64_t c1) {
   extern __shared__ uint32_t dyn_flats[];
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
-  for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = a.target[i];
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  FastChunk& cs = sh[wib];
   uint32_t* flats = dyn_flats + wib * a.L;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
   for (int64_t c = c0 + (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < c1; c += nwarps) {
     sample_circuit_warp(a, g, c, flats, lane);
-    FastEval<NQ> ev;
-    ev.begin(lane);
-    for (int base = 0; base < a.L; base += 32) {
-      const int nq = min(32, a.L - base);
-      int code = 0;
-      double th = 0.0;
-      if (lane < nq) {
-        const int64_t s = flats[base + lane];
-        LiveSlot v;
-        live_slot(a, s, g, v);
-        code = slot_gate_code(a, s, g, v);
-        th = v.theta;
-      }
-      ev.chunk(code, th, nq, cs, lane);
+    for (int p = lane; p < a.L; p += 32) {
+      const int64_t s = flats[p];
+      LiveSlot v;
+      live_slot(a, s, g, v);
+      const int64_t o = (c - c0) * a.L + p;
+      a.gate_codes[o] = (uint8_t)slot_gate_code(a, s, g, v);
+      a.gate_thetas[o] = v.theta;
     }
-    const double f = ev.finish(Ts, cs, lane);
-    if (lane == 0) a.fitness[c] = f;
   }
 }
 
@@ -299,28 +288,17 @@ static int blocks_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
-template <int NQ>
-static isq_status launch_eval_nq(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
-  const size_t dyn = (size_t)kWarpsPerBlock * a.L * sizeof(uint32_t);
-  const void* k = (const void*)qeqea_eval_kernel<NQ>;
-  if (dyn > 48 * 1024) ISQ_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-  const int grid = persistent_grid(k, dyn, c1 - c0);
-  qeqea_eval_kernel<NQ><<<grid, kThreadsPerBlock, dyn, s>>>(a, c0, c1);
-  ISQ_CUDA_TRY(cudaGetLastError());
-  return ISQ_OK;
-}
-
 isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
   if (c1 <= c0) return ISQ_OK;
-  switch (a.n) {
-    case 2: return launch_eval_nq<2>(a, c0, c1, s);
-    case 3: return launch_eval_nq<3>(a, c0, c1, s);
-    case 4: return launch_eval_nq<4>(a, c0, c1, s);
-    case 5: return launch_eval_nq<5>(a, c0, c1, s);
-    default:
-      set_error("numberOfWires outside the compiled range 2..5");
-      return ISQ_ERR_UNSUPPORTED;
-  }
+  const size_t dyn = (size_t)kWarpsPerBlock * a.L * sizeof(uint32_t);
+  const void* k = (const void*)qeqea_params_kernel;
+  if (dyn > 48 * 1024) ISQ_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  const int grid = persistent_grid(k, dyn, c1 - c0);
+  qeqea_params_kernel<<<grid, kThreadsPerBlock, dyn, s>>>(a, c0, c1);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return launch_fitness_batch_stoppable(a.n, a.L, c1 - c0, a.gate_codes, a.gate_thetas,
+                                        reinterpret_cast<const double*>(a.target), a.fitness + c0,
+                                        &a.st->stop, s);
 }
 
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
