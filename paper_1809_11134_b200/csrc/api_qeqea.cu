@@ -23,14 +23,15 @@ static void free_handle(QeqeaHandle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   QeqeaArgs& a = h->a;
-  cudaFree(a.theta);
-  cudaFree(a.qamp);
-  cudaFree(a.slot_max);
+  cudaFree(a.rot);
+  cudaFree(a.inter);
   cudaFree(a.claim);
   cudaFree(a.fitness);
   cudaFree(a.flats);
   cudaFree(a.gate_codes);
   cudaFree(a.gate_thetas);
+  cudaFree(a.touch_fbefore);
+  cudaFree(a.touch_mutated);
   cudaFree(a.st);
   cudaFree(a.records);
   cudaFree(a.best_codes);
@@ -130,14 +131,16 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   TRYA(cudaSetDevice(device));
   TRYA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
-  TRYA(cudaMalloc((void**)&a.theta, a.Q * 8));
-  TRYA(cudaMalloc((void**)&a.qamp, a.Qt * 3 * 16));
-  TRYA(cudaMalloc((void**)&a.slot_max, a.Q * 8));
+  TRYA(cudaMalloc((void**)&a.rot, a.Qt * sizeof(RotRec)));
+  TRYA(cudaMalloc((void**)&a.inter, (a.Q - a.Qt) * sizeof(IntRec)));
   TRYA(cudaMalloc((void**)&a.claim, a.Q * 4));
   TRYA(cudaMalloc((void**)&a.fitness, h->shard * h->world * 8));
   TRYA(cudaMalloc((void**)&a.flats, a.P * a.L * 4));
   TRYA(cudaMalloc((void**)&a.gate_codes, h->shard * a.L));
   TRYA(cudaMalloc((void**)&a.gate_thetas, h->shard * a.L * 8));
+  TRYA(cudaMalloc((void**)&a.touch_fbefore, h->shard * a.L * 8));
+  TRYA(cudaMalloc((void**)&a.touch_mutated, h->shard * a.L));
+  a.fused_commit = h->world == 1 ? 1 : 0;
   TRYA(cudaMalloc((void**)&a.st, sizeof(QeqeaDevState)));
   TRYA(cudaMalloc((void**)&a.records, sizeof(GenRecord) * h->max_batch));
   TRYA(cudaMalloc((void**)&a.best_codes, a.L));
@@ -272,15 +275,38 @@ isq_status isq_qeqea_best(void* handle, uint8_t* codes, double* thetas, double* 
   return ISQ_OK;
 }
 
+// Device temporaries for the reference's array layout.
+struct SoaTemps {
+  double *theta = nullptr, *qamp = nullptr, *smax = nullptr;
+  ~SoaTemps() {
+    cudaFree(theta);
+    cudaFree(qamp);
+    cudaFree(smax);
+  }
+  cudaError_t alloc(const QeqeaArgs& a) {
+    cudaError_t e = cudaMalloc((void**)&theta, a.Q * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&qamp, a.Qt * 48 + 16);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&smax, a.Q * 8);
+    return e;
+  }
+};
+
 isq_status isq_qeqea_get_state(void* handle, double* theta, double* qamp, double* slot_max,
                                uint64_t* generation, double* best_fitness, int32_t* stop) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
   const QeqeaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
-  if (theta) ISQ_CUDA_TRY(cudaMemcpy(theta, a.theta, a.Q * 8, cudaMemcpyDeviceToHost));
-  if (qamp) ISQ_CUDA_TRY(cudaMemcpy(qamp, a.qamp, a.Qt * 48, cudaMemcpyDeviceToHost));
-  if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(slot_max, a.slot_max, a.Q * 8, cudaMemcpyDeviceToHost));
+  if (theta || qamp || slot_max) {
+    SoaTemps t;
+    ISQ_CUDA_TRY(t.alloc(a));
+    isq_status st = qeqea_launch_pack(a, t.theta, t.qamp, t.smax, h->stream);
+    if (st != ISQ_OK) return st;
+    ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (theta) ISQ_CUDA_TRY(cudaMemcpy(theta, t.theta, a.Q * 8, cudaMemcpyDeviceToHost));
+    if (qamp) ISQ_CUDA_TRY(cudaMemcpy(qamp, t.qamp, a.Qt * 48, cudaMemcpyDeviceToHost));
+    if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(slot_max, t.smax, a.Q * 8, cudaMemcpyDeviceToHost));
+  }
   QeqeaDevState s;
   ISQ_CUDA_TRY(cudaMemcpy(&s, a.st, sizeof(s), cudaMemcpyDeviceToHost));
   if (generation) *generation = s.generation;
@@ -296,13 +322,19 @@ isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* 
   const QeqeaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
-  if (theta) ISQ_CUDA_TRY(cudaMemcpy(a.theta, theta, a.Q * 8, cudaMemcpyHostToDevice));
-  if (qamp) ISQ_CUDA_TRY(cudaMemcpy(a.qamp, qamp, a.Qt * 48, cudaMemcpyHostToDevice));
-  if (slot_max)
-    ISQ_CUDA_TRY(cudaMemcpy(a.slot_max, slot_max, a.Q * 8, cudaMemcpyHostToDevice));
-  else
-    ISQ_CUDA_TRY(cudaMemset(a.slot_max, 0, a.Q * 8));
-  ISQ_CUDA_TRY(cudaMemset(a.claim, 0, a.Q * 4));
+  if (theta && qamp) {
+    SoaTemps t;
+    ISQ_CUDA_TRY(t.alloc(a));
+    ISQ_CUDA_TRY(cudaMemcpy(t.theta, theta, a.Q * 8, cudaMemcpyHostToDevice));
+    ISQ_CUDA_TRY(cudaMemcpy(t.qamp, qamp, a.Qt * 48, cudaMemcpyHostToDevice));
+    if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(t.smax, slot_max, a.Q * 8, cudaMemcpyHostToDevice));
+    isq_status st = qeqea_launch_unpack(a, t.theta, t.qamp, slot_max ? t.smax : nullptr, h->stream);
+    if (st != ISQ_OK) return st;
+    ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  } else if (theta || qamp || slot_max) {
+    set_error("set_state needs both theta and qamp");
+    return ISQ_ERR_CONFIG;
+  }
   if (best_codes) ISQ_CUDA_TRY(cudaMemcpy(a.best_codes, best_codes, a.L, cudaMemcpyHostToDevice));
   if (best_thetas)
     ISQ_CUDA_TRY(cudaMemcpy(a.best_thetas, best_thetas, a.L * 8, cudaMemcpyHostToDevice));

@@ -1,12 +1,18 @@
 // Device state and per-slot helpers of the QEQEA generation loop.
 //
-// Reference: QeqeaEngine.step (engine.py:318-361).  The bank lives in HBM as
-// structure-of-arrays over the flat slot index of Eq. 9 (engine.py:82-87):
+// Reference: QeqeaEngine.step (engine.py:318-361).  The bank lives in HBM
+// indexed by the flat slot index of Eq. 9 (engine.py:82-87), as arrays of
+// aligned per-slot records - every generation touches O(P*L) slots at random,
+// so one record per slot is one DRAM transaction instead of one per field:
 //
-//   theta[Q]            committed angles                  f64
-//   qamp[3][Qt]         committed qutrit amplitudes       double2 (re, im) per axis
-//   slot_max[Q]         SegmentFitnessTable.slot_max      f64 (u64 atomicMax; fitness >= 0)
-//   claim[Q]            commit arbitration stamp          u32 (generation + 1)
+//   rot[Qt]     64 B  {q0, q1, q2 (complex), theta, slot_max}   rotation region
+//   inter[Q-Qt] 16 B  {theta, slot_max}                          interaction region
+//   claim[Q]     4 B  commit arbitration stamp (generation + 1)
+//
+// slot_max is SegmentFitnessTable.slot_max (engine.py:202-222), updated with a
+// 64-bit atomicMax (fitness >= 0, so integer order == double order).  The host
+// sees the reference's arrays (thetas[Q], qutrits[Qt,3], slot_max[Q]) through
+// pack/unpack kernels.
 //
 // Lazy mutation.  The reference mutates ~p_mut of all Q slots
 // at the end of every generation and reverts the un-improved ones at the next
@@ -40,6 +46,16 @@ struct GenRecord {
   double pad;
 };
 
+struct alignas(64) RotRec {
+  double2 q[3];
+  double theta;
+  double smax;
+};
+struct alignas(16) IntRec {
+  double theta;
+  double smax;
+};
+
 struct QeqeaArgs {
   // configuration (engine.py:33-43)
   int n, L;
@@ -49,15 +65,17 @@ struct QeqeaArgs {
   uint64_t max_generations;
   uint64_t seed;
   // bank
-  double* theta;
-  double2* qamp;  // 3 * Qt, axis-major
-  double* slot_max;
+  RotRec* rot;     // Qt records
+  IntRec* inter;   // Q - Qt records
   uint32_t* claim;
   // per generation
   double* fitness;   // P (padded to world * shard)
   uint32_t* flats;   // P * L scratch between commit and table kernels
   uint8_t* gate_codes;   // shard * L gate codes of the generation (params -> fitness)
   double* gate_thetas;   // shard * L live angles
+  double* touch_fbefore;  // shard * L slot_max each touch started the generation from
+  uint8_t* touch_mutated; // shard * L pending-mutation flag of each touch
+  int fused_commit;       // 1: single rank, commit+table fused over the touch records
   QeqeaDevState* st;
   GenRecord* records;
   uint8_t* best_codes;   // L
@@ -90,11 +108,35 @@ struct LiveSlot {
   double2 q[3];
 };
 
-__device__ __forceinline__ void load_committed(const QeqeaArgs& a, int64_t s, LiveSlot& v) {
-  v.theta = a.theta[s];
+__device__ __forceinline__ double* smax_ptr(const QeqeaArgs& a, int64_t s) {
+  return s < a.Qt ? &a.rot[s].smax : &a.inter[s - a.Qt].smax;
+}
+
+// Committed value of slot s (one 64 B or 16 B record load); returns slot_max.
+__device__ __forceinline__ double load_committed(const QeqeaArgs& a, int64_t s, LiveSlot& v) {
   if (s < a.Qt) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) v.q[k] = a.qamp[k * a.Qt + s];
+    const double2* r = reinterpret_cast<const double2*>(a.rot + s);
+    v.q[0] = r[0];
+    v.q[1] = r[1];
+    v.q[2] = r[2];
+    const double2 ts = r[3];
+    v.theta = ts.x;
+    return ts.y;
+  }
+  const double2 ts = *reinterpret_cast<const double2*>(a.inter + (s - a.Qt));
+  v.theta = ts.x;
+  return ts.y;
+}
+
+__device__ __forceinline__ void store_committed(const QeqeaArgs& a, int64_t s, const LiveSlot& v) {
+  if (s < a.Qt) {
+    double2* r = reinterpret_cast<double2*>(a.rot + s);
+    r[0] = v.q[0];
+    r[1] = v.q[1];
+    r[2] = v.q[2];
+    a.rot[s].theta = v.theta;
+  } else {
+    a.inter[s - a.Qt].theta = v.theta;
   }
 }
 
@@ -162,9 +204,9 @@ __device__ __forceinline__ bool mutate_slot(const QeqeaArgs& a, int64_t s, uint6
 // mutation drawn at the end of generation g-1).
 __device__ __forceinline__ void live_slot(const QeqeaArgs& a, int64_t s, uint64_t g, LiveSlot& v,
                                           bool* mutated = nullptr) {
-  load_committed(a, s, v);
+  const double f = load_committed(a, s, v);
   bool m = false;
-  if (g > 0) m = mutate_slot(a, s, g - 1, a.slot_max[s], v);
+  if (g > 0) m = mutate_slot(a, s, g - 1, f, v);
   if (mutated) *mutated = m;
 }
 
@@ -187,45 +229,56 @@ __device__ __forceinline__ int slot_gate_code(const QeqeaArgs& a, int64_t s, uin
 
 // sample_circuit (engine.py:174-184) for circuit c at generation g on stream
 // (seed, DOM_SAMPLE, g, c): integers(P, size=L) then integers(K, size=L),
-// flat = kind*L*P + individual*L + position.  Warp-cooperative: every lane
-// computes the u32 draws of its positions directly from the counter (fast
-// path); if any draw would be rejected by numpy's Lemire sampler, lane 0
-// replays the stream sequentially.  Writes flats[0..L).
+// flat = kind*L*P + individual*L + position.  Warp-cooperative: per chunk of
+// 32 positions the (at most 9) distinct Philox blocks holding their u32 draws
+// are computed once by lanes 0..8 into `blk` (shared, 9*4 words) and every
+// lane takes its two draws from there (numpy consumes u32 halves low-first).
+// If any draw would be rejected by numpy's Lemire sampler, lane 0 replays the
+// whole circuit sequentially.  Writes flats[0..L).
 __device__ __forceinline__ void sample_circuit_warp(const QeqeaArgs& a, uint64_t g, int64_t c,
-                                                    uint32_t* flats, int lane) {
+                                                    uint32_t* flats, uint64_t* blk, int lane) {
   const int L = a.L;
   const uint32_t rngP = (uint32_t)(a.P - 1), rngK = (uint32_t)(a.K - 1);
   const int offk = (a.P == 1) ? 0 : L;  // integers(1, ...) consumes no draws
   bool reject = false;
-  for (int p = lane; p < L; p += 32) {
-    uint32_t ind = 0;
-    if (a.P > 1) {
+  for (int base = 0; base < L; base += 32) {
+    const int ib0 = base >> 3;            // first block (0-based) of the individual draws
+    const int kb0 = (offk + base) >> 3;   // first block of the kind draws
+    if (lane < 9) {
+      const int b = lane < 4 ? ib0 + lane : kb0 + (lane - 4);
       uint64_t w[4];
-      stream_block(a.seed, DOM_SAMPLE, g, (uint64_t)c, 0, (uint64_t)(p >> 3) + 1, w);
-      const uint64_t word = w[(p & 7) >> 1];
-      const uint32_t u = (p & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
-      reject |= lemire_rejects(u, rngP);
-      ind = lemire_value(u, rngP);
+      stream_block(a.seed, DOM_SAMPLE, g, (uint64_t)c, 0, (uint64_t)b + 1, w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) blk[lane * 4 + k] = w[k];
     }
-    const int uk = offk + p;
-    uint64_t w[4];
-    stream_block(a.seed, DOM_SAMPLE, g, (uint64_t)c, 0, (uint64_t)(uk >> 3) + 1, w);
-    const uint64_t word = w[(uk & 7) >> 1];
-    const uint32_t u = (uk & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
-    reject |= lemire_rejects(u, rngK);
-    const uint32_t kind = lemire_value(u, rngK);
-    flats[p] = (uint32_t)((int64_t)kind * L * a.P + (int64_t)ind * L + p);
+    __syncwarp();
+    const int p = base + lane;
+    if (p < L) {
+      uint32_t ind = 0;
+      if (a.P > 1) {
+        const uint64_t word = blk[((p >> 3) - ib0) * 4 + ((p & 7) >> 1)];
+        const uint32_t u = (p & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+        reject |= lemire_rejects(u, rngP);
+        ind = lemire_value(u, rngP);
+      }
+      const int uk = offk + p;
+      const uint64_t word = blk[(4 + (uk >> 3) - kb0) * 4 + ((uk & 7) >> 1)];
+      const uint32_t u = (uk & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+      reject |= lemire_rejects(u, rngK);
+      const uint32_t kind = lemire_value(u, rngK);
+      flats[p] = (uint32_t)((int64_t)kind * L * a.P + (int64_t)ind * L + p);
+    }
+    __syncwarp();
   }
   if (__any_sync(0xffffffffu, reject)) {
-    __syncwarp();
     if (lane == 0) {
       NpStream st;
       st.init(a.seed, DOM_SAMPLE, g, (uint64_t)c, 0);
       for (int p = 0; p < L; ++p) flats[p] = (uint32_t)(st.integers(a.P) * L + p);
       for (int p = 0; p < L; ++p) flats[p] += (uint32_t)(st.integers(a.K) * L * a.P);
     }
+    __syncwarp();
   }
-  __syncwarp();
 }
 
 }  // namespace isq

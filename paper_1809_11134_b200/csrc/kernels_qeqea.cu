@@ -19,30 +19,81 @@
 namespace isq {
 
 // ---------------------------------------------------------------- eval ---
-// Two kernels: `params` turns every (circuit, position) of the shard into a
-// gate (code, live angle) - sampling, lazy mutation, Born measurement - and
-// `fitness_fast_kernel` (kernels_fitness.cu) composes and scores them.
-// Splitting keeps each kernel's hot code inside the instruction cache.
+// sample (all circuits, flats -> HBM) | values (shard touches -> gate code +
+// live angle) | fitness_fast_kernel (kernels_fitness.cu).  Separate kernels
+// keep each one's hot code inside the instruction cache and give the random
+// bank gathers thread-level memory parallelism.
 
-__global__ void __launch_bounds__(kThreadsPerBlock)
-    qeqea_params_kernel(QeqeaArgs a, int64_t c0, int64_t c1) {
-  extern __shared__ uint32_t dyn_flats[];
+__global__ void __launch_bounds__(kThreadsPerBlock) qeqea_sample_flats_kernel(QeqeaArgs a) {
+  __shared__ uint64_t blk[kWarpsPerBlock][36];
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  uint32_t* flats = dyn_flats + wib * a.L;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
-  for (int64_t c = c0 + (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < c1; c += nwarps) {
-    sample_circuit_warp(a, g, c, flats, lane);
-    for (int p = lane; p < a.L; p += 32) {
-      const int64_t s = flats[p];
+  for (int64_t c = (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < a.P; c += nwarps)
+    sample_circuit_warp(a, g, c, a.flats + c * a.L, blk[wib], lane);
+}
+
+// One thread per touch of the shard: committed record -> live value (pending
+// mutation of g-1).  Rotation touches (1/3 at C5) additionally need the Born
+// measurement; those are compacted into a shared-memory queue so the costly
+// measurement runs on full warps instead of on the 1/3 of lanes that need it.
+// Also records, per touch, the slot_max the generation started from and
+// whether the slot carries a pending mutation (the fused single-rank commit
+// consumes both).
+constexpr int kValThreads = 256;
+
+struct MeasureTask {
+  double2 q[3];
+  uint32_t s;
+  uint32_t out;
+};
+
+__global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t0, int64_t t1) {
+  __shared__ MeasureTask tasks[kValThreads];
+  __shared__ int ntask;
+  if (a.st->stop) return;
+  const uint64_t g = a.st->generation;
+  for (int64_t base = t0 + (int64_t)blockIdx.x * kValThreads; base < t1;
+       base += (int64_t)gridDim.x * kValThreads) {
+    if (threadIdx.x == 0) ntask = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    if (i < t1) {
+      const uint32_t s = a.flats[i];
       LiveSlot v;
-      live_slot(a, s, g, v);
-      const int64_t o = (c - c0) * a.L + p;
-      a.gate_codes[o] = (uint8_t)slot_gate_code(a, s, g, v);
+      const double f = load_committed(a, s, v);
+      const bool mutated = g > 0 && mutate_slot(a, s, g - 1, f, v);
+      const int64_t o = i - t0;
       a.gate_thetas[o] = v.theta;
+      a.touch_fbefore[o] = f;
+      a.touch_mutated[o] = mutated;
+      const int64_t kind = (int64_t)s / (a.L * a.P);
+      if (kind < a.n) {
+        const int k = atomicAdd(&ntask, 1);
+        tasks[k].q[0] = v.q[0];
+        tasks[k].q[1] = v.q[1];
+        tasks[k].q[2] = v.q[2];
+        tasks[k].s = s;
+        tasks[k].out = (uint32_t)o;
+      } else {
+        a.gate_codes[o] = (uint8_t)(3 * a.n + (kind - a.n));
+      }
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < ntask; k += kValThreads) {
+      const MeasureTask& t = tasks[k];
+      NpStream st;
+      st.init(a.seed, DOM_MEASURE, g, (uint64_t)t.s, 0);
+      double re[3] = {t.q[0].x, t.q[1].x, t.q[2].x};
+      double im[3] = {t.q[0].y, t.q[1].y, t.q[2].y};
+      bool ok = true;
+      const int axis = measure_axis(re, im, a.n_meas, st, &ok);
+      const int64_t kind = (int64_t)t.s / (a.L * a.P);
+      a.gate_codes[t.out] = (uint8_t)(3 * kind + axis);
+    }
+    __syncthreads();
   }
 }
 
@@ -97,7 +148,6 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_partials(QeqeaArgs a
 __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
   __shared__ int s_improved;
   __shared__ int64_t s_best;
-  extern __shared__ uint32_t cap_flats[];
   QeqeaDevState* st = a.st;
   if (st->stop) return;
   if (threadIdx.x == 0) {
@@ -134,9 +184,8 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
   if (!s_improved || threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   const uint64_t g = st->generation;
-  sample_circuit_warp(a, g, s_best, cap_flats, lane);
   for (int p = lane; p < a.L; p += 32) {
-    const int64_t s = cap_flats[p];
+    const int64_t s = a.flats[s_best * a.L + p];
     LiveSlot v;
     live_slot(a, s, g, v);
     a.best_codes[p] = (uint8_t)slot_gate_code(a, s, g, v);
@@ -148,36 +197,48 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
 
 // Elitist accept (engine.py:345-351 + 211-222): a slot mutated at g-1 keeps
 // its mutation iff some circuit of generation g that touched it beat its
-// slot_max.  Only touched slots can be improved, so walk the touches; one
-// touch per slot wins the claim stamp and writes the live value into the
-// committed bank.  Also writes the flats for the table kernel.
-__global__ void __launch_bounds__(kThreadsPerBlock) qeqea_commit_kernel(QeqeaArgs a) {
-  extern __shared__ uint32_t dyn_flats[];
+// slot_max.  Only touched slots can be improved, so walk the touches (thread
+// per touch); one improving touch per slot wins the claim stamp and writes
+// the live value into the committed bank.
+__global__ void __launch_bounds__(256) qeqea_commit_kernel(QeqeaArgs a) {
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  uint32_t* flats = dyn_flats + wib * a.L;
-  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
-  for (int64_t c = (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < a.P; c += nwarps) {
-    sample_circuit_warp(a, g, c, flats, lane);
-    const double fit = a.fitness[c];
-    for (int p = lane; p < a.L; p += 32) {
-      const uint32_t s = flats[p];
-      a.flats[c * a.L + p] = s;
-      if (g == 0) continue;
-      const double f = a.slot_max[s];
-      if (!(fit > f)) continue;
+  if (g == 0) return;
+  const int64_t total = a.P * a.L;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = a.flats[i];
+    const double fit = a.fitness[i / a.L];
+    if (!(fit > *smax_ptr(a, s))) continue;
+    LiveSlot v;
+    const double f = load_committed(a, s, v);
+    if (!mutate_slot(a, s, g - 1, f, v)) continue;
+    if (atomicMax(&a.claim[s], (uint32_t)(g + 1)) >= (uint32_t)(g + 1)) continue;
+    store_committed(a, s, v);
+  }
+}
+
+// Single-rank fused commit + table (every touch of the generation went through
+// qeqea_values_kernel, which recorded the slot_max it started from and the
+// pending-mutation flag): only improving touches do random bank traffic.
+__global__ void __launch_bounds__(256) qeqea_commit_table_kernel(QeqeaArgs a) {
+  if (a.st->stop) return;
+  const uint64_t g = a.st->generation;
+  const int64_t total = a.P * a.L;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double fit = a.fitness[i / a.L];
+    const double fb = a.touch_fbefore[i];
+    if (!(fit > fb)) continue;
+    const uint32_t s = a.flats[i];
+    if (a.touch_mutated[i] && atomicMax(&a.claim[s], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
       LiveSlot v;
-      load_committed(a, s, v);
-      if (!mutate_slot(a, s, g - 1, f, v)) continue;
-      if (atomicMax(&a.claim[s], (uint32_t)(g + 1)) >= (uint32_t)(g + 1)) continue;
-      a.theta[s] = v.theta;
-      if (s < a.Qt) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) a.qamp[k * a.Qt + s] = v.q[k];
-      }
+      load_committed(a, s, v);  // commit writes only theta / qutrit, never slot_max
+      mutate_slot(a, s, g - 1, fb, v);
+      store_committed(a, s, v);
     }
+    atomicMax(reinterpret_cast<unsigned long long*>(smax_ptr(a, s)),
+              (unsigned long long)__double_as_longlong(fit));
   }
 }
 
@@ -190,9 +251,9 @@ __global__ void qeqea_table_kernel(QeqeaArgs a) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t s = a.flats[i];
     const double fit = a.fitness[i / a.L];
-    if (fit > a.slot_max[s])
-      atomicMax(reinterpret_cast<unsigned long long*>(a.slot_max) + s,
-                (unsigned long long)__double_as_longlong(fit));
+    double* sm = smax_ptr(a, s);
+    if (fit > *sm)
+      atomicMax(reinterpret_cast<unsigned long long*>(sm), (unsigned long long)__double_as_longlong(fit));
   }
 }
 
@@ -215,10 +276,14 @@ __global__ void qeqea_init_kernel(QeqeaArgs a) {
        s += (int64_t)gridDim.x * blockDim.x) {
     uint64_t w0[4], w1[4];
     stream_block(a.seed, DOM_INIT, 0, (uint64_t)s, 0, 1, w0);
-    a.theta[s] = __dadd_rn(0.0, __dmul_rn(kTwoPiD, u64_to_double(w0[0])));
-    a.slot_max[s] = 0.0;
+    const double theta = __dadd_rn(0.0, __dmul_rn(kTwoPiD, u64_to_double(w0[0])));
     a.claim[s] = 0;
-    if (s < a.Qt) {
+    if (s >= a.Qt) {
+      a.inter[s - a.Qt].theta = theta;
+      a.inter[s - a.Qt].smax = 0.0;
+    } else {
+      a.rot[s].theta = theta;
+      a.rot[s].smax = 0.0;
       stream_block(a.seed, DOM_INIT, 0, (uint64_t)s, 0, 2, w1);
       const uint64_t u[6] = {w0[1], w0[2], w0[3], w1[0], w1[1], w1[2]};
       double re[3], im[3], nn = 0.0;
@@ -234,7 +299,7 @@ __global__ void qeqea_init_kernel(QeqeaArgs a) {
       }
       const double nrm = sqrt(nn);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) a.qamp[k * a.Qt + s] = make_double2(re[k] / nrm, im[k] / nrm);
+      for (int k = 0; k < 3; ++k) a.rot[s].q[k] = make_double2(re[k] / nrm, im[k] / nrm);
     }
   }
 }
@@ -255,19 +320,51 @@ __global__ void qeqea_live_kernel(QeqeaArgs a, double* theta_out, double2* q_out
   }
 }
 
+// Records <-> the reference's arrays: theta[Q], qamp[3][Qt] (axis-major), slot_max[Q].
+__global__ void qeqea_pack_kernel(QeqeaArgs a, double* theta, double2* qamp, double* smax) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    LiveSlot v;
+    const double f = load_committed(a, s, v);
+    theta[s] = v.theta;
+    smax[s] = f;
+    if (s < a.Qt) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) qamp[k * a.Qt + s] = v.q[k];
+    }
+  }
+}
+
+__global__ void qeqea_unpack_kernel(QeqeaArgs a, const double* theta, const double2* qamp,
+                                    const double* smax) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    LiveSlot v;
+    v.theta = theta[s];
+    if (s < a.Qt) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v.q[k] = qamp[k * a.Qt + s];
+    }
+    store_committed(a, s, v);
+    *smax_ptr(a, s) = smax ? smax[s] : 0.0;
+    a.claim[s] = 0;
+  }
+}
+
 // Blueprints and gate codes of circuits [c0, c1) at the current generation
 // (parity / introspection; same device functions as the eval kernel).
 __global__ void __launch_bounds__(kThreadsPerBlock)
     qeqea_sample_kernel(QeqeaArgs a, int64_t c0, int64_t c1, int64_t* flats_out, uint8_t* codes_out,
                         double* thetas_out) {
   extern __shared__ uint32_t dyn_flats[];
+  __shared__ uint64_t blk[kWarpsPerBlock][36];
   const uint64_t g = a.st->generation;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   uint32_t* flats = dyn_flats + wib * a.L;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
   for (int64_t c = c0 + (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < c1; c += nwarps) {
-    sample_circuit_warp(a, g, c, flats, lane);
+    sample_circuit_warp(a, g, c, flats, blk[wib], lane);
     for (int p = lane; p < a.L; p += 32) {
       const int64_t s = flats[p];
       LiveSlot v;
@@ -288,13 +385,13 @@ static int blocks_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
+
+
 isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
+  const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, a.P);
+  qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a);
   if (c1 <= c0) return ISQ_OK;
-  const size_t dyn = (size_t)kWarpsPerBlock * a.L * sizeof(uint32_t);
-  const void* k = (const void*)qeqea_params_kernel;
-  if (dyn > 48 * 1024) ISQ_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-  const int grid = persistent_grid(k, dyn, c1 - c0);
-  qeqea_params_kernel<<<grid, kThreadsPerBlock, dyn, s>>>(a, c0, c1);
+  qeqea_values_kernel<<<blocks_for((c1 - c0) * a.L, kValThreads), kValThreads, 0, s>>>(a, c0 * a.L, c1 * a.L);
   ISQ_CUDA_TRY(cudaGetLastError());
   return launch_fitness_batch_stoppable(a.n, a.L, c1 - c0, a.gate_codes, a.gate_thetas,
                                         reinterpret_cast<const double*>(a.target), a.fitness + c0,
@@ -303,12 +400,13 @@ isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStr
 
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
   qeqea_reduce_partials<<<a.n_parts, kRedThreads, 0, s>>>(a);
-  const size_t cap = (size_t)a.L * sizeof(uint32_t);
-  qeqea_reduce_final<<<1, kRedThreads, cap, s>>>(a);
-  const size_t dyn = (size_t)kWarpsPerBlock * a.L * sizeof(uint32_t);
-  const int grid_c = persistent_grid((const void*)qeqea_commit_kernel, dyn, a.P);
-  qeqea_commit_kernel<<<grid_c, kThreadsPerBlock, dyn, s>>>(a);
-  qeqea_table_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
+  qeqea_reduce_final<<<1, kRedThreads, 0, s>>>(a);
+  if (a.fused_commit) {
+    qeqea_commit_table_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
+  } else {
+    qeqea_commit_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
+    qeqea_table_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
+  }
   qeqea_advance_kernel<<<1, 1, 0, s>>>(a);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
@@ -316,6 +414,21 @@ isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
 
 isq_status qeqea_launch_init(const QeqeaArgs& a, cudaStream_t s) {
   qeqea_init_kernel<<<blocks_for(a.Q, 256), 256, 0, s>>>(a);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+isq_status qeqea_launch_pack(const QeqeaArgs& a, double* theta, double* qamp, double* smax,
+                             cudaStream_t s) {
+  qeqea_pack_kernel<<<blocks_for(a.Q, 256), 256, 0, s>>>(a, theta, reinterpret_cast<double2*>(qamp), smax);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+isq_status qeqea_launch_unpack(const QeqeaArgs& a, const double* theta, const double* qamp,
+                               const double* smax, cudaStream_t s) {
+  qeqea_unpack_kernel<<<blocks_for(a.Q, 256), 256, 0, s>>>(
+      a, theta, reinterpret_cast<const double2*>(qamp), smax);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }

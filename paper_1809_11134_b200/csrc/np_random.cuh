@@ -111,8 +111,8 @@ __host__ __device__ __forceinline__ double u64_to_double(uint64_t w) {
 struct NpStream {
   uint64_t seed, dom, gen, idx, sub;
   uint64_t ctr;  // number of blocks generated so far
-  uint64_t buf[4];
-  int pos;       // next word in buf; 4 = empty
+  uint64_t b0, b1, b2, b3;  // current block (registers: no dynamic indexing)
+  int pos;       // next word of the block; 4 = empty
   uint32_t u32buf;
   bool has32;
 
@@ -131,10 +131,17 @@ struct NpStream {
   __host__ __device__ __forceinline__ uint64_t next64() {
     if (pos >= 4) {
       ++ctr;
-      stream_block(seed, dom, gen, idx, sub, ctr, buf);
+      uint64_t w[4];
+      stream_block(seed, dom, gen, idx, sub, ctr, w);
+      b0 = w[0];
+      b1 = w[1];
+      b2 = w[2];
+      b3 = w[3];
       pos = 0;
     }
-    return buf[pos++];
+    const uint64_t r = pos == 0 ? b0 : (pos == 1 ? b1 : (pos == 2 ? b2 : b3));
+    ++pos;
+    return r;
   }
   __host__ __device__ __forceinline__ uint32_t next32() {
     if (has32) {
@@ -254,19 +261,24 @@ __device__ __forceinline__ int measure_axis(const double qre[3], const double qi
   const double sum = __dadd_rn(__dadd_rn(pr[0], pr[1]), pr[2]);
 #pragma unroll
   for (int j = 0; j < 3; ++j) pr[j] = __ddiv_rn(pr[j], sum);
-  int64_t cnt[3] = {0, 0, 0};
-  double remaining = 1.0;
+  // random_multinomial with d = 3, written out so nothing is dynamically indexed
+  int64_t c0 = 0, c1 = 0, c2 = 0;
   int64_t dn = n_meas;
-  for (int j = 0; j < 2; ++j) {
-    cnt[j] = binomial(s, __ddiv_rn(pr[j], remaining), dn, ok);
-    dn -= cnt[j];
-    if (dn <= 0) break;
-    remaining = __dsub_rn(remaining, pr[j]);
+  c0 = binomial(s, pr[0], dn, ok);  // pix[0] / remaining_p with remaining_p = 1.0
+  dn -= c0;
+  if (dn > 0) {
+    const double remaining = __dsub_rn(1.0, pr[0]);
+    c1 = binomial(s, __ddiv_rn(pr[1], remaining), dn, ok);
+    dn -= c1;
+    if (dn > 0) c2 = dn;
   }
-  if (dn > 0) cnt[2] = dn;
   int best = 0;
-  if (cnt[1] > cnt[best]) best = 1;
-  if (cnt[2] > cnt[best]) best = 2;
+  int64_t bc = c0;
+  if (c1 > bc) {
+    best = 1;
+    bc = c1;
+  }
+  if (c2 > bc) best = 2;
   return best;
 }
 

@@ -8,6 +8,10 @@ namespace isq {
 isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s);
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_init(const QeqeaArgs& a, cudaStream_t s);
+isq_status qeqea_launch_pack(const QeqeaArgs& a, double* theta, double* qamp, double* smax,
+                             cudaStream_t s);
+isq_status qeqea_launch_unpack(const QeqeaArgs& a, const double* theta, const double* qamp,
+                               const double* smax, cudaStream_t s);
 isq_status qeqea_launch_live(const QeqeaArgs& a, double* theta_out, double* q_out, cudaStream_t s);
 isq_status qeqea_launch_sample(const QeqeaArgs& a, int64_t c0, int64_t c1, int64_t* flats,
                                uint8_t* codes, double* thetas, cudaStream_t s);
