@@ -158,6 +158,47 @@ isq_status isq_qeqea_sample(void* handle, int64_t c0, int64_t c1, int64_t* flats
 /* Fitness vector of the last evaluated generation (P doubles). */
 isq_status isq_qeqea_fitness(void* handle, double* out);
 
+/* ------------------------------------------------------------------------
+ * GA engine (GaEngine, ga.py:141-214).  Genomes are P x L gate codes + angles
+ * resident on the device; same split-phase protocol as the QEQEA handle.
+ * ---------------------------------------------------------------------- */
+typedef struct isq_ga_config {
+  int32_t number_of_wires;   /* GaConfig.number_of_wires                    */
+  int32_t size_of_individual;
+  int64_t population;        /* default 50                                  */
+  double mutation_rate;      /* default 0.1                                 */
+  double mutation_range;     /* default pi/8                                */
+  double structural_rate;    /* default 0.1                                 */
+  int64_t max_generations;
+  double target_fitness;
+  uint64_t seed;
+  int32_t rank;
+  int32_t world;
+} isq_ga_config;
+
+isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t device,
+                         int32_t max_batch, void** handle);
+isq_status isq_ga_destroy(void* handle);
+isq_status isq_ga_set_stream(void* handle, void* stream);
+isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, int32_t* n_done,
+                       int32_t* stop_reason);
+isq_status isq_ga_begin_batch(void* handle);
+isq_status isq_ga_eval(void* handle);
+isq_status isq_ga_finish(void* handle);
+isq_status isq_ga_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
+                             int32_t* stop_reason, uint64_t* generation, double* best_fitness);
+isq_status isq_ga_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream);
+isq_status isq_ga_best(void* handle, uint8_t* codes, double* thetas, double* fitness);
+/* Current genomes (engine.genomes) as P x L codes + angles; set_state injects them. */
+isq_status isq_ga_get_state(void* handle, uint8_t* codes, double* thetas, uint64_t* generation,
+                            double* best_fitness, int32_t* stop);
+isq_status isq_ga_set_state(void* handle, const uint8_t* codes, const double* thetas,
+                            uint64_t generation, double best_fitness, int32_t stop,
+                            const uint8_t* best_codes, const double* best_thetas);
+isq_status isq_ga_fitness(void* handle, double* out);
+/* Parents drawn by SUS in the last finished generation (P int32). */
+isq_status isq_ga_parents(void* handle, int32_t* out);
+
 /* Diagnostics: measured FP64 (fp64 != 0) or FP32 CUDA-core FMA peak in flop/s
  * on `device` (roofline denominator of the fitness kernel). */
 isq_status isq_fma_peak(int32_t fp64, int32_t device, double* flops_per_s);

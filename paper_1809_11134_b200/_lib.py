@@ -55,6 +55,22 @@ class QeqeaConfig(ctypes.Structure):
     ]
 
 
+class GaConfigC(ctypes.Structure):
+    _fields_ = [
+        ("number_of_wires", c_i32),
+        ("size_of_individual", c_i32),
+        ("population", c_i64),
+        ("mutation_rate", c_dbl),
+        ("mutation_range", c_dbl),
+        ("structural_rate", c_dbl),
+        ("max_generations", c_i64),
+        ("target_fitness", c_dbl),
+        ("seed", c_u64),
+        ("rank", c_i32),
+        ("world", c_i32),
+    ]
+
+
 GEN_RECORD = np.dtype([("gen_best", "f8"), ("gen_mean", "f8"), ("best_fitness", "f8"), ("reserved", "f8")])
 
 c_i32p = ctypes.POINTER(c_i32)
@@ -75,6 +91,20 @@ SIGNATURES: dict[str, tuple] = {
     "isq_qeqea_live_population": (c_i32, [c_vp, c_vp, c_vp]),
     "isq_qeqea_sample": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "isq_qeqea_fitness": (c_i32, [c_vp, c_vp]),
+    "isq_ga_create": (c_i32, [ctypes.POINTER(GaConfigC), c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "isq_ga_destroy": (c_i32, [c_vp]),
+    "isq_ga_set_stream": (c_i32, [c_vp, c_vp]),
+    "isq_ga_step": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "isq_ga_begin_batch": (c_i32, [c_vp]),
+    "isq_ga_eval": (c_i32, [c_vp]),
+    "isq_ga_finish": (c_i32, [c_vp]),
+    "isq_ga_read_batch": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "isq_ga_buffers": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "isq_ga_best": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
+    "isq_ga_get_state": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "isq_ga_set_state": (c_i32, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_i32, c_vp, c_vp]),
+    "isq_ga_fitness": (c_i32, [c_vp, c_vp]),
+    "isq_ga_parents": (c_i32, [c_vp, c_vp]),
     "isq_last_error": (ctypes.c_char_p, []),
     "isq_abi_version": (c_i32, []),
     "isq_fitness_batch": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),

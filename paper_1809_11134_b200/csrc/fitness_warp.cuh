@@ -203,4 +203,35 @@ struct FastEval {
   }
 };
 
+// Grid-stride body shared by the explicit-gate fitness kernels: warp per
+// circuit over circuits [0, count) of (codes, thetas) rows of length L.
+template <int NQ>
+__device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t* __restrict__ codes,
+                                             const double* __restrict__ thetas,
+                                             const double2* __restrict__ Ts, FastChunk* sh,
+                                             double* __restrict__ fitness, int warps_per_block) {
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  FastChunk& cs = sh[wib];
+  const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
+  for (int64_t c = (int64_t)blockIdx.x * warps_per_block + wib; c < count; c += nwarps) {
+    FastEval<NQ> ev;
+    ev.begin(lane);
+    const uint8_t* cc = codes + c * (int64_t)L;
+    const double* ct = thetas + c * (int64_t)L;
+    for (int base = 0; base < L; base += 32) {
+      const int nq = min(32, L - base);
+      int code = 0;
+      double th = 0.0;
+      if (lane < nq) {
+        code = cc[base + lane];
+        th = ct[base + lane];
+      }
+      ev.chunk(code, th, nq, cs, lane);
+    }
+    const double f = ev.finish(Ts, cs, lane);
+    if (lane == 0) fitness[c] = f;
+  }
+}
+
 }  // namespace isq

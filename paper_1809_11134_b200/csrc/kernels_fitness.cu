@@ -25,29 +25,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock)
   if (stop != nullptr && *stop) return;
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  FastChunk& cs = sh[wib];
-  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
-  for (int64_t c = (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < count; c += nwarps) {
-    FastEval<NQ> ev;
-    ev.begin(lane);
-    const uint8_t* cc = codes + c * (int64_t)L;
-    const double* ct = thetas + c * (int64_t)L;
-    for (int base = 0; base < L; base += 32) {
-      const int p = base + lane;
-      const int nq = min(32, L - base);
-      int code = 0;
-      double th = 0.0;
-      if (lane < nq) {
-        code = cc[p];
-        th = ct[p];
-      }
-      ev.chunk(code, th, nq, cs, lane);
-    }
-    const double f = ev.finish(Ts, cs, lane);
-    if (lane == 0) fitness[c] = f;
-  }
+  fitness_rows<NQ>(count, L, codes, thetas, Ts, sh, fitness, kWarpsPerBlock);
 }
 
 // Composition with the exact global phase (compose_gates readout) + fitness.

@@ -1,0 +1,602 @@
+// GPUGA baseline generation loop (GaEngine.step, ga.py:165-194).
+//
+// Genomes live on the device as two (double-buffered by generation parity)
+// SoA banks: codes[P*L] u8 (gate_choices index, ga.py:47-59) and thetas[P*L]
+// f64.  One generation g:
+//   eval    fitness of this rank's genome shard            (fitness_rows)
+//   (multi-GPU: all-gather of the fitness vector)
+//   reduce  max / first argmax (elite) / mean, best-so-far + genome capture
+//   sus     stochastic universal sampling, exact sequential replica of
+//           sus_select (ga.py:95-116) incl. numpy's pairwise np.sum
+//   breed   thread per (child, gene): two-point crossover of the pair
+//           (ga.py:81-92, 177-187) + per-gene mutation (ga.py:119-138); elite
+//           copied unmutated to slot 0
+//   advance generation += 1, stop reason (ga.py:189-193)
+// Draws: per-pair crossover stream (DOM_GA_PAIR, g, pair), per-(child, gene)
+// mutation stream (DOM_GA_MUT, g, child, gene), SUS stream (DOM_GA_SUS, g).
+#include <cstring>
+#include <string>
+
+#include "engine_common.cuh"
+#include "fitness_warp.cuh"
+#include "isq_internal.h"
+
+namespace isq {
+
+struct GaDevState {
+  uint64_t generation;
+  uint64_t rec_base;
+  double best_fitness;
+  int64_t elite;
+  int32_t stop;
+  int32_t improved;
+};
+
+struct GaArgs {
+  int n, L, ncodes;
+  int64_t P;
+  double rate, mrange, structural, target_fitness;
+  uint64_t max_generations, seed;
+  uint8_t* codes[2];
+  double* thetas[2];
+  double* fitness;
+  int32_t* parents;
+  GaDevState* st;
+  GenRecord* records;
+  int rec_cap;
+  uint8_t* best_codes;
+  double* best_thetas;
+  const double2* target;
+  double* part_max;
+  double* part_sum;
+  int64_t* part_arg;
+  int n_parts;
+};
+
+__device__ __forceinline__ int ga_cur(const GaArgs& a) { return (int)(a.st->generation & 1); }
+
+// ------------------------------------------------------------------ eval ---
+template <int NQ>
+__global__ void __launch_bounds__(kThreadsPerBlock) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
+  using G = Geo<NQ>;
+  __shared__ double2 Ts[G::D * G::D];
+  __shared__ FastChunk sh[kWarpsPerBlock];
+  if (a.st->stop) return;
+  const int cur = ga_cur(a);
+  for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = a.target[i];
+  __syncthreads();
+  fitness_rows<NQ>(c1 - c0, a.L, a.codes[cur] + c0 * a.L, a.thetas[cur] + c0 * a.L, Ts, sh,
+                   a.fitness + c0, kWarpsPerBlock);
+}
+
+// ---------------------------------------------------------------- reduce ---
+constexpr int kGaRed = 256;
+
+__global__ void __launch_bounds__(kGaRed) ga_reduce_partials(GaArgs a) {
+  if (a.st->stop) return;
+  __shared__ double smax[kGaRed], ssum[kGaRed];
+  __shared__ int64_t sarg[kGaRed];
+  const int64_t per = (a.P + a.n_parts - 1) / a.n_parts;
+  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t hi = min(a.P, lo + per);
+  double m = -1.0, sum = 0.0;
+  int64_t arg = INT64_MAX;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double f = a.fitness[i];
+    sum += f;
+    if (f > m) {
+      m = f;
+      arg = i;
+    }
+  }
+  smax[threadIdx.x] = m;
+  ssum[threadIdx.x] = sum;
+  sarg[threadIdx.x] = arg;
+  __syncthreads();
+  for (int off = kGaRed / 2; off >= 1; off >>= 1) {
+    if (threadIdx.x < off) {
+      const double m2 = smax[threadIdx.x + off];
+      const int64_t a2 = sarg[threadIdx.x + off];
+      if (m2 > smax[threadIdx.x] || (m2 == smax[threadIdx.x] && a2 < sarg[threadIdx.x])) {
+        smax[threadIdx.x] = m2;
+        sarg[threadIdx.x] = a2;
+      }
+      ssum[threadIdx.x] += ssum[threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.part_max[blockIdx.x] = smax[0];
+    a.part_sum[blockIdx.x] = ssum[0];
+    a.part_arg[blockIdx.x] = sarg[0];
+  }
+}
+
+// numpy's pairwise summation of a contiguous float64 array (np.sum, used by
+// sus_select's total, ga.py:100): blocks of <= 128 with 8 accumulators,
+// recursive halving at multiples of 8 above.
+__device__ double np_pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
+}
+
+// Final reduction + best-so-far update (ga.py:171-174) + SUS (ga.py:95-116).
+// SUS is inherently sequential (cumulative sums compared against pointer +=
+// spacing): thread 0 replays it exactly; warp 0 copies the elite genome.
+__global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
+  __shared__ int s_improved;
+  __shared__ int64_t s_elite;
+  GaDevState* st = a.st;
+  if (st->stop) return;
+  const int cur = ga_cur(a);
+  if (threadIdx.x == 0) {
+    double m = -1.0, sum = 0.0;
+    int64_t arg = INT64_MAX;
+    for (int i = 0; i < a.n_parts; ++i) {
+      const double pm = a.part_max[i];
+      if (pm > m || (pm == m && a.part_arg[i] < arg)) {
+        m = pm;
+        arg = a.part_arg[i];
+      }
+      sum += a.part_sum[i];
+    }
+    const int improved = m > st->best_fitness;
+    if (improved) st->best_fitness = m;
+    st->elite = arg;
+    st->improved = improved;
+    GenRecord r;
+    r.gen_best = m;
+    r.gen_mean = sum / (double)a.P;
+    r.best_fitness = st->best_fitness;
+    r.pad = 0.0;
+    const uint64_t ri = st->generation - st->rec_base;
+    if (ri < (uint64_t)a.rec_cap) a.records[ri] = r;
+    s_improved = improved;
+    s_elite = arg;
+
+    // ---- sus_select(fitnesses, P, stream) ----
+    NpStream rs;
+    rs.init(a.seed, DOM_GA_SUS, st->generation, 0, 0);
+    const double total = np_pairwise_sum(a.fitness, a.P);
+    if (total <= 0.0) {
+      for (int64_t k = 0; k < a.P; ++k) a.parents[k] = (int32_t)rs.integers(a.P);
+    } else {
+      const double spacing = __ddiv_rn(total, (double)a.P);
+      double pointer = rs.uniform(0.0, spacing);
+      double cumulative = 0.0;
+      int64_t index = 0;
+      for (int64_t k = 0; k < a.P; ++k) {
+        while (index < a.P - 1 && __dadd_rn(cumulative, a.fitness[index]) <= pointer) {
+          cumulative = __dadd_rn(cumulative, a.fitness[index]);
+          ++index;
+        }
+        a.parents[k] = (int32_t)index;
+        pointer = __dadd_rn(pointer, spacing);
+      }
+    }
+  }
+  __syncthreads();
+  if (s_improved && threadIdx.x < 32) {
+    for (int j = threadIdx.x; j < a.L; j += 32) {
+      a.best_codes[j] = a.codes[cur][s_elite * a.L + j];
+      a.best_thetas[j] = a.thetas[cur][s_elite * a.L + j];
+    }
+  }
+}
+
+// ----------------------------------------------------------------- breed ---
+// Child i >= 1 is the (i-1)%2-th child of pair k = (i-1)/2 of parents
+// (parents[2k % P], parents[(2k+1) % P]) (ga.py:177-187); slot 0 is the elite.
+__global__ void ga_breed_kernel(GaArgs a) {
+  if (a.st->stop) return;
+  const uint64_t g = a.st->generation;
+  const int cur = ga_cur(a), nxt = cur ^ 1;
+  const int64_t total = a.P * a.L;
+  const int64_t elite = a.st->elite;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / a.L;
+    const int j = (int)(t - i * a.L);
+    if (i == 0) {
+      a.codes[nxt][j] = a.codes[cur][elite * a.L + j];
+      a.thetas[nxt][j] = a.thetas[cur][elite * a.L + j];
+      continue;
+    }
+    const int64_t k = (i - 1) >> 1;
+    const bool first = ((i - 1) & 1) == 0;
+    const int64_t pa = a.parents[(2 * k) % a.P], pb = a.parents[(2 * k + 1) % a.P];
+    // two_point_crossover: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
+    int p = 0, q = 0;
+    if (a.L >= 2) {
+      NpStream cs;
+      cs.init(a.seed, DOM_GA_PAIR, g, (uint64_t)k, 0);
+      const int x = (int)cs.integers(a.L + 1), y = (int)cs.integers(a.L + 1);
+      p = x < y ? x : y;
+      q = x < y ? y : x;
+    }
+    const bool inside = j >= p && j < q;
+    const int64_t src = (first != inside) ? pa : pb;  // child a: a outside, b inside
+    int code = a.codes[cur][src * a.L + j];
+    double theta = a.thetas[cur][src * a.L + j];
+    // ga_mutate for this gene (ga.py:126-137)
+    NpStream ms;
+    ms.init(a.seed, DOM_GA_MUT, g, (uint64_t)i, (uint64_t)j);
+    if (ms.random() < a.rate) {
+      if (ms.random() < a.structural) {
+        code = (int)ms.integers(a.ncodes);
+      } else {
+        const double u = ms.uniform(-a.mrange, a.mrange);
+        theta = py_mod(__dadd_rn(theta, u), kTwoPiD);
+      }
+    }
+    a.codes[nxt][i * a.L + j] = (uint8_t)code;
+    a.thetas[nxt][i * a.L + j] = theta;
+  }
+}
+
+__global__ void ga_advance_kernel(GaArgs a) {
+  GaDevState* st = a.st;
+  if (st->stop) return;
+  st->generation += 1;
+  if (st->best_fitness >= a.target_fitness)
+    st->stop = 1;
+  else if (st->generation >= a.max_generations)
+    st->stop = 2;
+}
+
+// random_genome (ga.py:68-73), one stream per (genome, gene).
+__global__ void ga_init_kernel(GaArgs a) {
+  const int64_t total = a.P * a.L;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / a.L;
+    const int j = (int)(t - i * a.L);
+    NpStream s;
+    s.init(a.seed, DOM_GA_INIT, 0, (uint64_t)i, (uint64_t)j);
+    a.codes[0][t] = (uint8_t)s.integers(a.ncodes);
+    a.thetas[0][t] = s.uniform(0.0, kTwoPiD);
+  }
+}
+
+// --------------------------------------------------------------- handle ---
+struct GaHandle {
+  GaArgs a;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  int64_t shard = 0;
+  int max_batch = 0;
+};
+
+static void ga_free(GaHandle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  GaArgs& a = h->a;
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(a.codes[b]);
+    cudaFree(a.thetas[b]);
+  }
+  cudaFree(a.fitness);
+  cudaFree(a.parents);
+  cudaFree(a.st);
+  cudaFree(a.records);
+  cudaFree(a.best_codes);
+  cudaFree(a.best_thetas);
+  cudaFree((void*)a.target);
+  cudaFree(a.part_max);
+  cudaFree(a.part_sum);
+  cudaFree(a.part_arg);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+static int ga_blocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)(b < 1 ? 1 : b);
+}
+
+template <int NQ>
+static isq_status ga_launch_eval_nq(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
+  const void* k = (const void*)ga_eval_kernel<NQ>;
+  const int grid = persistent_grid(k, 0, c1 - c0);
+  ga_eval_kernel<NQ><<<grid, kThreadsPerBlock, 0, s>>>(a, c0, c1);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
+  if (c1 <= c0) return ISQ_OK;
+  switch (a.n) {
+    case 2: return ga_launch_eval_nq<2>(a, c0, c1, s);
+    case 3: return ga_launch_eval_nq<3>(a, c0, c1, s);
+    case 4: return ga_launch_eval_nq<4>(a, c0, c1, s);
+    case 5: return ga_launch_eval_nq<5>(a, c0, c1, s);
+    default:
+      set_error("numberOfWires outside the compiled range 2..5");
+      return ISQ_ERR_UNSUPPORTED;
+  }
+}
+
+static isq_status ga_launch_finish(const GaArgs& a, cudaStream_t s) {
+  ga_reduce_partials<<<a.n_parts, kGaRed, 0, s>>>(a);
+  ga_reduce_sus_kernel<<<1, kGaRed, 0, s>>>(a);
+  ga_breed_kernel<<<ga_blocks(a.P * a.L), 256, 0, s>>>(a);
+  ga_advance_kernel<<<1, 1, 0, s>>>(a);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+}  // namespace isq
+
+using namespace isq;
+
+#define GA_TRY(expr)                                                 \
+  do {                                                               \
+    cudaError_t _e = (expr);                                         \
+    if (_e != cudaSuccess) {                                         \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+      ga_free(h);                                                    \
+      return ISQ_ERR_CUDA;                                           \
+    }                                                                \
+  } while (0)
+
+extern "C" {
+
+isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t device,
+                         int32_t max_batch, void** out) {
+  *out = nullptr;
+  auto bad = [](const std::string& m, isq_status code = ISQ_ERR_CONFIG) {
+    set_error(m);
+    return code;
+  };
+  if (cfg->number_of_wires < 2) return bad("numberOfWires must be ≥ 2");
+  if (cfg->size_of_individual < 1) return bad("sizeOfIndividual must be ≥ 1");
+  if (cfg->population < 2) return bad("GA population must be ≥ 2");
+  if (!(cfg->mutation_rate >= 0.0 && cfg->mutation_rate <= 1.0))
+    return bad("mutation rate must be in [0, 1]");
+  if (!(cfg->structural_rate >= 0.0 && cfg->structural_rate <= 1.0))
+    return bad("structural rate must be in [0, 1]");
+  if (!(cfg->target_fitness > 0.0 && cfg->target_fitness <= 1.0))
+    return bad("targetFitness must be in (0, 1]");
+  if (cfg->max_generations < 1) return bad("maxGenerations must be ≥ 1");
+  if (cfg->number_of_wires > ISQ_MAX_WIRES)
+    return bad("numberOfWires exceeds the device kernels (compiled for 2..5 wires)",
+               ISQ_ERR_UNSUPPORTED);
+  if (cfg->population >= (1LL << 31)) return bad("population must be < 2^31", ISQ_ERR_UNSUPPORTED);
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return bad("invalid rank/world");
+  GaHandle* h = new GaHandle();
+  h->device = device;
+  h->rank = cfg->rank;
+  h->world = cfg->world;
+  h->max_batch = max_batch < 1 ? 1 : max_batch;
+  GaArgs& a = h->a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = cfg->number_of_wires;
+  a.L = cfg->size_of_individual;
+  a.P = cfg->population;
+  a.ncodes = 3 * a.n + a.n * (a.n - 1) / 2;
+  a.rate = cfg->mutation_rate;
+  a.mrange = cfg->mutation_range;
+  a.structural = cfg->structural_rate;
+  a.target_fitness = cfg->target_fitness;
+  a.max_generations = (uint64_t)cfg->max_generations;
+  a.seed = cfg->seed;
+  a.rec_cap = h->max_batch;
+  h->shard = (a.P + h->world - 1) / h->world;
+  const int64_t D = 1LL << a.n;
+  GA_TRY(cudaSetDevice(device));
+  GA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->own_stream = true;
+  for (int b = 0; b < 2; ++b) {
+    GA_TRY(cudaMalloc((void**)&a.codes[b], a.P * a.L));
+    GA_TRY(cudaMalloc((void**)&a.thetas[b], a.P * a.L * 8));
+  }
+  GA_TRY(cudaMalloc((void**)&a.fitness, h->shard * h->world * 8));
+  GA_TRY(cudaMalloc((void**)&a.parents, a.P * 4));
+  GA_TRY(cudaMalloc((void**)&a.st, sizeof(GaDevState)));
+  GA_TRY(cudaMalloc((void**)&a.records, sizeof(GenRecord) * h->max_batch));
+  GA_TRY(cudaMalloc((void**)&a.best_codes, a.L));
+  GA_TRY(cudaMalloc((void**)&a.best_thetas, a.L * 8));
+  GA_TRY(cudaMalloc((void**)&a.target, D * D * 16));
+  a.n_parts = (int)((a.P + 4095) / 4096);
+  if (a.n_parts > 1024) a.n_parts = 1024;
+  if (a.n_parts < 1) a.n_parts = 1;
+  GA_TRY(cudaMalloc((void**)&a.part_max, a.n_parts * 8));
+  GA_TRY(cudaMalloc((void**)&a.part_sum, a.n_parts * 8));
+  GA_TRY(cudaMalloc((void**)&a.part_arg, a.n_parts * 8));
+  GA_TRY(cudaMemcpy((void*)a.target, target, D * D * 16, cudaMemcpyHostToDevice));
+  GaDevState s0;
+  std::memset(&s0, 0, sizeof(s0));
+  GA_TRY(cudaMemcpy(a.st, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+  GA_TRY(cudaMemset(a.best_codes, 0, a.L));
+  GA_TRY(cudaMemset(a.best_thetas, 0, a.L * 8));
+  GA_TRY(cudaMemset(a.fitness, 0, h->shard * h->world * 8));
+  ga_init_kernel<<<ga_blocks(a.P * a.L), 256, 0, h->stream>>>(a);
+  GA_TRY(cudaGetLastError());
+  GA_TRY(cudaStreamSynchronize(h->stream));
+  *out = h;
+  return ISQ_OK;
+}
+
+isq_status isq_ga_destroy(void* handle) {
+  ga_free(static_cast<GaHandle*>(handle));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_set_stream(void* handle, void* stream) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  h->own_stream = false;
+  h->stream = (cudaStream_t)stream;
+  return ISQ_OK;
+}
+
+isq_status isq_ga_begin_batch(void* handle) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaMemcpyAsync(&h->a.st->rec_base, &h->a.st->generation, 8,
+                               cudaMemcpyDeviceToDevice, h->stream));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_eval(void* handle) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  const int64_t c0 = h->rank * h->shard;
+  const int64_t c1 = c0 + h->shard < h->a.P ? c0 + h->shard : h->a.P;
+  return ga_launch_eval(h->a, c0, c1, h->stream);
+}
+
+isq_status isq_ga_finish(void* handle) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  return ga_launch_finish(h->a, h->stream);
+}
+
+isq_status isq_ga_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
+                             int32_t* stop_reason, uint64_t* generation, double* best_fitness) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  GaDevState s;
+  ISQ_CUDA_TRY(cudaMemcpy(&s, h->a.st, sizeof(s), cudaMemcpyDeviceToHost));
+  int64_t done = (int64_t)(s.generation - s.rec_base);
+  if (done > h->max_batch) done = h->max_batch;
+  if (done > 0 && records)
+    ISQ_CUDA_TRY(cudaMemcpy(records, h->a.records, sizeof(GenRecord) * done, cudaMemcpyDeviceToHost));
+  if (n_done) *n_done = (int32_t)done;
+  if (stop_reason) *stop_reason = s.stop;
+  if (generation) *generation = s.generation;
+  if (best_fitness) *best_fitness = s.best_fitness;
+  return ISQ_OK;
+}
+
+isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, int32_t* n_done,
+                       int32_t* stop_reason) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  if (h->world != 1) {
+    set_error("isq_ga_step drives a single rank; use eval / all-gather / finish for world > 1");
+    return ISQ_ERR_CONFIG;
+  }
+  if (n > h->max_batch) {
+    set_error("n exceeds the handle's record capacity (max_batch)");
+    return ISQ_ERR_CONFIG;
+  }
+  isq_status st = isq_ga_begin_batch(handle);
+  if (st != ISQ_OK) return st;
+  for (int i = 0; i < n; ++i) {
+    st = ga_launch_eval(h->a, 0, h->a.P, h->stream);
+    if (st != ISQ_OK) return st;
+    st = ga_launch_finish(h->a, h->stream);
+    if (st != ISQ_OK) return st;
+  }
+  return isq_ga_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
+}
+
+isq_status isq_ga_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  if (fitness_dev) *fitness_dev = h->a.fitness;
+  if (shard_len) *shard_len = h->shard;
+  if (stream) *stream = h->stream;
+  return ISQ_OK;
+}
+
+isq_status isq_ga_best(void* handle, uint8_t* codes, double* thetas, double* fitness) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  ISQ_CUDA_TRY(cudaMemcpy(codes, h->a.best_codes, h->a.L, cudaMemcpyDeviceToHost));
+  ISQ_CUDA_TRY(cudaMemcpy(thetas, h->a.best_thetas, h->a.L * 8, cudaMemcpyDeviceToHost));
+  GaDevState s;
+  ISQ_CUDA_TRY(cudaMemcpy(&s, h->a.st, sizeof(s), cudaMemcpyDeviceToHost));
+  *fitness = s.best_fitness;
+  return ISQ_OK;
+}
+
+isq_status isq_ga_get_state(void* handle, uint8_t* codes, double* thetas, uint64_t* generation,
+                            double* best_fitness, int32_t* stop) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  const GaArgs& a = h->a;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  GaDevState s;
+  ISQ_CUDA_TRY(cudaMemcpy(&s, a.st, sizeof(s), cudaMemcpyDeviceToHost));
+  const int cur = (int)(s.generation & 1);
+  if (codes) ISQ_CUDA_TRY(cudaMemcpy(codes, a.codes[cur], a.P * a.L, cudaMemcpyDeviceToHost));
+  if (thetas) ISQ_CUDA_TRY(cudaMemcpy(thetas, a.thetas[cur], a.P * a.L * 8, cudaMemcpyDeviceToHost));
+  if (generation) *generation = s.generation;
+  if (best_fitness) *best_fitness = s.best_fitness;
+  if (stop) *stop = s.stop;
+  return ISQ_OK;
+}
+
+isq_status isq_ga_set_state(void* handle, const uint8_t* codes, const double* thetas,
+                            uint64_t generation, double best_fitness, int32_t stop,
+                            const uint8_t* best_codes, const double* best_thetas) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  const GaArgs& a = h->a;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (int64_t i = 0; codes && i < a.P * a.L; ++i)
+    if (codes[i] >= a.ncodes) {
+      set_error("gate code out of range for numberOfWires");
+      return ISQ_ERR_CONFIG;
+    }
+  const int cur = (int)(generation & 1);
+  if (codes) ISQ_CUDA_TRY(cudaMemcpy(a.codes[cur], codes, a.P * a.L, cudaMemcpyHostToDevice));
+  if (thetas) ISQ_CUDA_TRY(cudaMemcpy(a.thetas[cur], thetas, a.P * a.L * 8, cudaMemcpyHostToDevice));
+  if (best_codes) ISQ_CUDA_TRY(cudaMemcpy(a.best_codes, best_codes, a.L, cudaMemcpyHostToDevice));
+  if (best_thetas)
+    ISQ_CUDA_TRY(cudaMemcpy(a.best_thetas, best_thetas, a.L * 8, cudaMemcpyHostToDevice));
+  GaDevState s;
+  std::memset(&s, 0, sizeof(s));
+  s.generation = generation;
+  s.rec_base = generation;
+  s.best_fitness = best_fitness;
+  s.stop = stop;
+  ISQ_CUDA_TRY(cudaMemcpy(a.st, &s, sizeof(s), cudaMemcpyHostToDevice));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_fitness(void* handle, double* out) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  ISQ_CUDA_TRY(cudaMemcpy(out, h->a.fitness, h->a.P * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_parents(void* handle, int32_t* out) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  ISQ_CUDA_TRY(cudaMemcpy(out, h->a.parents, h->a.P * 4, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+}  // extern "C"
