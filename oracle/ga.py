@@ -90,10 +90,17 @@ class OracleGa:
     def done(self) -> bool:
         return self.stop_reason is not None
 
+    def evaluate(self, c0: int, c1: int) -> np.ndarray:
+        """Fitness of genomes [c0, c1) (ga.py:167-170)."""
+        return np.array([circuit_fitness(self.codes[i], self.thetas[i], self.target, self.cfg.n)
+                         for i in range(c0, c1)])
+
     def step(self, trace: bool = False):
+        return self.finish_generation(self.evaluate(0, self.cfg.P), trace=trace)
+
+    def finish_generation(self, fits: np.ndarray, trace: bool = False):
         cfg, gen = self.cfg, self.generation
-        fits = np.array([circuit_fitness(self.codes[i], self.thetas[i], self.target, cfg.n)
-                         for i in range(cfg.P)])
+        fits = np.asarray(fits)
         elite = int(np.argmax(fits))
         if fits[elite] > self.best_fitness:
             self.best_fitness = float(fits[elite])

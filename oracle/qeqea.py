@@ -250,21 +250,26 @@ class OracleQeqea:
     def done(self) -> bool:
         return self.stop_reason is not None
 
-    def step(self, trace: bool = False):
+    # The generation is split into phases so a population-sharded driver can
+    # score a subset of the circuits and finish on the gathered fitness vector.
+    def begin_generation(self):
         lay, g = self.layout, self.generation
         # construct_segments (engine.py:156-171)
-        axes = measure_axes(self.qutrits, lay.n_meas, self.seed, g, np.arange(lay.Qt))
-        bank_thetas = self.thetas.copy()
+        self._axes = measure_axes(self.qutrits, lay.n_meas, self.seed, g, np.arange(lay.Qt))
+        self._bank_thetas = self.thetas.copy()
         # sample_circuit x P (engine.py:322-325)
-        bps = np.stack([sample_blueprint(lay, self.seed, g, c) for c in range(lay.P)])
-        # evaluate_circuit x P (engine.py:187-199, 326-336)
-        fits = np.empty(lay.P)
-        codes_all = np.empty((lay.P, lay.L), dtype=np.int64)
-        for c in range(lay.P):
-            bp = bps[c]
-            codes = [gate_code(lay, f, axes[f] if f < lay.Qt else 0) for f in bp]
-            codes_all[c] = codes
-            fits[c] = circuit_fitness(codes, bank_thetas[bp], self.target, lay.n)
+        self._bps = np.stack([sample_blueprint(lay, self.seed, g, c) for c in range(lay.P)])
+        self._codes = np.array([[gate_code(lay, f, self._axes[f] if f < lay.Qt else 0) for f in bp]
+                                for bp in self._bps], dtype=np.int64)
+
+    def evaluate(self, c0: int, c1: int) -> np.ndarray:
+        """evaluate_circuit for circuits [c0, c1) (engine.py:187-199, 326-336)."""
+        return np.array([circuit_fitness(self._codes[c], self._bank_thetas[self._bps[c]], self.target,
+                                         self.layout.n) for c in range(c0, c1)])
+
+    def finish_generation(self, fits: np.ndarray, trace: bool = False):
+        lay, g = self.layout, self.generation
+        bps, codes_all, bank_thetas = self._bps, self._codes, self._bank_thetas
         # table update + best tracking (engine.py:202-222, 338-343)
         improved = set()
         for c in range(lay.P):
@@ -295,8 +300,13 @@ class OracleQeqea:
         gen_mean = float(np.mean(fits))
         if trace:
             return gen_best, gen_mean, GenerationTrace(
-                bps, axes, fits, np.array(sorted(improved), dtype=np.int64), gen_best, gen_mean)
+                bps, self._axes, np.asarray(fits), np.array(sorted(improved), dtype=np.int64),
+                gen_best, gen_mean)
         return gen_best, gen_mean
+
+    def step(self, trace: bool = False):
+        self.begin_generation()
+        return self.finish_generation(self.evaluate(0, self.layout.P), trace=trace)
 
     def mutate(self, g: int) -> Dict[int, Tuple[float, Optional[np.ndarray]]]:
         lay = self.layout
