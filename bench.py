@@ -203,8 +203,7 @@ def run_ours(args):
         for _ in range(args.warmup):
             generation()
         stream.synchronize()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-               torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(args.steps)]
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks = ClockSampler(local)
         clocks.start()
@@ -214,21 +213,24 @@ def run_ours(args):
         start.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
-            _lib.check(lib.isq_qeqea_eval(eng._h))
+            _lib.check(lib.isq_qeqea_prepare(eng._h))
             ev[i][1].record(stream)
+            _lib.check(lib.isq_qeqea_score(eng._h))
+            ev[i][2].record(stream)
             if world > 1:
                 send.copy_(mine)
                 dist.all_gather_into_tensor(full, send)
             _lib.check(lib.isq_qeqea_finish(eng._h))
-            ev[i][2].record(stream)
+            ev[i][3].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         clk = clocks.stop()
     ms = start.elapsed_time(end)
-    eval_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    fin_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    prep_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    eval_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    fin_ms = [e[2].elapsed_time(e[3]) for e in ev]
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -257,15 +259,17 @@ def run_ours(args):
                    "n": N, "L": L, "P": P, "global_batch": P, "parallelism": f"dp{world} (circuit shards)",
                    "l2": "inputs larger than L2 (36 GB bank vs 126 MB)"},
         "gens_per_s": args.steps / (ms * 1e-3),
-        "phase_ms": {"eval": sum(eval_ms) / len(eval_ms), "finish": sum(fin_ms) / len(fin_ms)},
+        "phase_ms": {"prepare (sample + lazy mutation + measure)": sum(prep_ms) / len(prep_ms),
+                     "score (fitness kernel)": sum(eval_ms) / len(eval_ms),
+                     "finish (reduce + commit + table)": sum(fin_ms) / len(fin_ms)},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
-                     "kernel": "qeqea_eval_kernel<5>",
+                     "kernel": "fitness_fast_kernel<5> (score phase, one launch per generation)",
                      "peak_source": "FP64 CUDA-core FMA peak measured live by isq_fma_peak "
                                     "(MEASURED_PEAKS.json carries no FP64 figure)",
                      "work": "canonical F(n,L) = (6L+8) 4^n flop/eval (SURVEY.md §8d) x circuits per launch"},
         "clocks": clk,
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": 8 * args.steps,
         "best_fitness": float(rec["best_fitness"][-1]),
     }
 

@@ -136,6 +136,11 @@ isq_status isq_qeqea_step(void* handle, int32_t n, isq_generation_record* record
 isq_status isq_qeqea_begin_batch(void* handle);
 isq_status isq_qeqea_eval(void* handle);
 isq_status isq_qeqea_finish(void* handle);
+/* eval == prepare (sample all circuits + gate values of the shard: K1/K2)
+ * followed by score (compose + fitness of the shard: K3); exposed separately
+ * so callers can time the fitness kernel alone. */
+isq_status isq_qeqea_prepare(void* handle);
+isq_status isq_qeqea_score(void* handle);
 isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
                                 int32_t* stop_reason, uint64_t* generation, double* best_fitness);
 isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream);

@@ -83,6 +83,8 @@ SIGNATURES: dict[str, tuple] = {
     "isq_qeqea_begin_batch": (c_i32, [c_vp]),
     "isq_qeqea_eval": (c_i32, [c_vp]),
     "isq_qeqea_finish": (c_i32, [c_vp]),
+    "isq_qeqea_prepare": (c_i32, [c_vp]),
+    "isq_qeqea_score": (c_i32, [c_vp]),
     "isq_qeqea_read_batch": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "isq_qeqea_buffers": (c_i32, [c_vp, c_vp, c_vp, c_vp]),
     "isq_qeqea_best": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

@@ -204,6 +204,27 @@ isq_status isq_qeqea_eval(void* handle) {
   return qeqea_launch_eval(h->a, c0, c1, h->stream);
 }
 
+static void shard_range(const QeqeaHandle* h, int64_t* c0, int64_t* c1) {
+  *c0 = h->rank * h->shard;
+  *c1 = *c0 + h->shard < h->a.P ? *c0 + h->shard : h->a.P;
+}
+
+isq_status isq_qeqea_prepare(void* handle) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  int64_t c0, c1;
+  shard_range(h, &c0, &c1);
+  return qeqea_launch_prepare(h->a, c0, c1, h->stream);
+}
+
+isq_status isq_qeqea_score(void* handle) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  int64_t c0, c1;
+  shard_range(h, &c0, &c1);
+  return qeqea_launch_score(h->a, c0, c1, h->stream);
+}
+
 isq_status isq_qeqea_finish(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
   ISQ_CUDA_TRY(cudaSetDevice(h->device));

@@ -387,15 +387,26 @@ static int blocks_for(int64_t n, int threads) {
 
 
 
-isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
+isq_status qeqea_launch_prepare(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
   const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, a.P);
   qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a);
-  if (c1 <= c0) return ISQ_OK;
-  qeqea_values_kernel<<<blocks_for((c1 - c0) * a.L, kValThreads), kValThreads, 0, s>>>(a, c0 * a.L, c1 * a.L);
+  if (c1 > c0)
+    qeqea_values_kernel<<<blocks_for((c1 - c0) * a.L, kValThreads), kValThreads, 0, s>>>(a, c0 * a.L, c1 * a.L);
   ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+isq_status qeqea_launch_score(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
+  if (c1 <= c0) return ISQ_OK;
   return launch_fitness_batch_stoppable(a.n, a.L, c1 - c0, a.gate_codes, a.gate_thetas,
                                         reinterpret_cast<const double*>(a.target), a.fitness + c0,
                                         &a.st->stop, s);
+}
+
+isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
+  isq_status st = qeqea_launch_prepare(a, c0, c1, s);
+  if (st != ISQ_OK) return st;
+  return qeqea_launch_score(a, c0, c1, s);
 }
 
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {

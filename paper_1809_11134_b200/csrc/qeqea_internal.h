@@ -5,6 +5,8 @@
 
 namespace isq {
 
+isq_status qeqea_launch_prepare(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s);
+isq_status qeqea_launch_score(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s);
 isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s);
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_init(const QeqeaArgs& a, cudaStream_t s);
