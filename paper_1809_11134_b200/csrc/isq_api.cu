@@ -1,4 +1,5 @@
 // C ABI of libisq: argument validation, host<->device staging, error state.
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -64,6 +65,44 @@ isq_status isq_fitness_batch_device(int32_t n, int32_t length, int64_t count,
                               unitary_dev, (cudaStream_t)stream);
 }
 
+// Host-buffer fitness: a per-device staging context (grow-only device buffers,
+// two streams) pipelines the batch in chunks so the host->device copy of chunk
+// i+1 overlaps the fitness kernel of chunk i and the fitness read-back.
+// Pinned host buffers give full-bandwidth DMA; pageable ones still work.
+struct BatchContext {
+  int device = -1;
+  cudaStream_t copy = nullptr, comp = nullptr;
+  uint8_t* codes[2] = {nullptr, nullptr};
+  double* thetas[2] = {nullptr, nullptr};
+  double* fit[2] = {nullptr, nullptr};
+  double* target = nullptr;
+  unsigned char* unit = nullptr;  // compose output (not pipelined)
+  size_t cap_rows = 0, cap_len = 0, cap_unit = 0;
+  cudaEvent_t loaded[2], done[2];
+  std::mutex mu;
+};
+
+static BatchContext* batch_context(int device) {
+  static std::mutex g;
+  static BatchContext* ctx[64] = {nullptr};
+  std::lock_guard<std::mutex> lk(g);
+  if (device < 0 || device >= 64) return nullptr;
+  if (!ctx[device]) {
+    BatchContext* c = new BatchContext();
+    c->device = device;
+    cudaSetDevice(device);
+    cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&c->comp, cudaStreamNonBlocking);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventCreateWithFlags(&c->loaded[b], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&c->done[b], cudaEventDisableTiming);
+    }
+    cudaMalloc((void**)&c->target, 32 * 32 * 16);
+    ctx[device] = c;
+  }
+  return ctx[device];
+}
+
 isq_status isq_fitness_batch(int32_t n, int32_t length, int64_t count, const uint8_t* codes,
                              const double* thetas, const double* target, double* fitness_out,
                              double* unitary_out, int32_t device) {
@@ -74,45 +113,79 @@ isq_status isq_fitness_batch(int32_t n, int32_t length, int64_t count, const uin
   if (st != ISQ_OK) return st;
   if (count == 0) return ISQ_OK;
   ISQ_CUDA_TRY(cudaSetDevice(device));
-  const int64_t D = 1LL << n;
-  uint8_t* d_codes = nullptr;
-  double *d_thetas = nullptr, *d_target = nullptr, *d_fit = nullptr, *d_u = nullptr;
-  cudaStream_t s = nullptr;
-  isq_status rc = ISQ_OK;
-  auto fail = [&](cudaError_t e, const char* what) {
-    set_error(std::string(what) + ": " + cudaGetErrorString(e));
-    rc = ISQ_ERR_CUDA;
-  };
-  cudaError_t e;
-  if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) {
-    fail(e, "cudaStreamCreate");
-    return rc;
+  BatchContext* c = batch_context(device);
+  if (!c) {
+    set_error("invalid device ordinal");
+    return ISQ_ERR_CONFIG;
   }
-  do {
-    if ((e = cudaMallocAsync((void**)&d_codes, total > 0 ? total : 1, s))) { fail(e, "cudaMalloc"); break; }
-    if ((e = cudaMallocAsync((void**)&d_thetas, (total > 0 ? total : 1) * 8, s))) { fail(e, "cudaMalloc"); break; }
-    if ((e = cudaMallocAsync((void**)&d_target, 2 * D * D * 8, s))) { fail(e, "cudaMalloc"); break; }
-    if ((e = cudaMallocAsync((void**)&d_fit, count * 8, s))) { fail(e, "cudaMalloc"); break; }
-    if (unitary_out && (e = cudaMallocAsync((void**)&d_u, count * 2 * D * D * 8, s))) { fail(e, "cudaMalloc"); break; }
-    if (total > 0) {
-      if ((e = cudaMemcpyAsync(d_codes, codes, total, cudaMemcpyHostToDevice, s))) { fail(e, "H2D codes"); break; }
-      if ((e = cudaMemcpyAsync(d_thetas, thetas, total * 8, cudaMemcpyHostToDevice, s))) { fail(e, "H2D thetas"); break; }
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int64_t D = 1LL << n;
+  const int64_t chunk = count < (1 << 17) ? count : (1 << 17);  // circuits per pipeline stage
+  const size_t len = (size_t)(length > 0 ? length : 1);
+  if ((size_t)chunk > c->cap_rows || len > c->cap_len) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(c->codes[b]);
+      cudaFree(c->thetas[b]);
+      cudaFree(c->fit[b]);
     }
-    if ((e = cudaMemcpyAsync(d_target, target, 2 * D * D * 8, cudaMemcpyHostToDevice, s))) { fail(e, "H2D target"); break; }
-    rc = launch_fitness_batch(n, length, count, d_codes, d_thetas, d_target, d_fit, d_u, s);
-    if (rc != ISQ_OK) break;
-    if ((e = cudaMemcpyAsync(fitness_out, d_fit, count * 8, cudaMemcpyDeviceToHost, s))) { fail(e, "D2H fitness"); break; }
-    if (unitary_out && (e = cudaMemcpyAsync(unitary_out, d_u, count * 2 * D * D * 8, cudaMemcpyDeviceToHost, s))) { fail(e, "D2H unitary"); break; }
-    if ((e = cudaStreamSynchronize(s))) { fail(e, "cudaStreamSynchronize"); break; }
-  } while (0);
-  cudaFreeAsync(d_codes, s);
-  cudaFreeAsync(d_thetas, s);
-  cudaFreeAsync(d_target, s);
-  cudaFreeAsync(d_fit, s);
-  if (d_u) cudaFreeAsync(d_u, s);
-  cudaStreamSynchronize(s);
-  cudaStreamDestroy(s);
-  return rc;
+    c->cap_rows = (size_t)chunk;
+    c->cap_len = len;
+    for (int b = 0; b < 2; ++b) {
+      ISQ_CUDA_TRY(cudaMalloc((void**)&c->codes[b], c->cap_rows * c->cap_len));
+      ISQ_CUDA_TRY(cudaMalloc((void**)&c->thetas[b], c->cap_rows * c->cap_len * 8));
+      ISQ_CUDA_TRY(cudaMalloc((void**)&c->fit[b], c->cap_rows * 8));
+    }
+  }
+  ISQ_CUDA_TRY(cudaMemcpyAsync(c->target, target, D * D * 16, cudaMemcpyHostToDevice, c->copy));
+  if (unitary_out) {
+    // composition output (readout path): chunk by chunk, not pipelined
+    const size_t ub = (size_t)chunk * D * D * 16;
+    if (ub > c->cap_unit) {
+      cudaFree(c->unit);
+      c->cap_unit = ub;
+      ISQ_CUDA_TRY(cudaMalloc((void**)&c->unit, ub));
+    }
+    for (int64_t off = 0; off < count; off += chunk) {
+      const int64_t m = (count - off) < chunk ? (count - off) : chunk;
+      if (length > 0) {
+        ISQ_CUDA_TRY(cudaMemcpyAsync(c->codes[0], codes + off * length, m * length,
+                                     cudaMemcpyHostToDevice, c->copy));
+        ISQ_CUDA_TRY(cudaMemcpyAsync(c->thetas[0], thetas + off * length, m * length * 8,
+                                     cudaMemcpyHostToDevice, c->copy));
+      }
+      ISQ_CUDA_TRY(cudaStreamSynchronize(c->copy));
+      st = launch_fitness_batch(n, length, m, c->codes[0], c->thetas[0], c->target, c->fit[0],
+                                reinterpret_cast<double*>(c->unit), c->comp);
+      if (st != ISQ_OK) return st;
+      ISQ_CUDA_TRY(cudaMemcpyAsync(fitness_out + off, c->fit[0], m * 8, cudaMemcpyDeviceToHost, c->comp));
+      ISQ_CUDA_TRY(cudaMemcpyAsync(unitary_out + off * D * D * 2, c->unit, (size_t)m * D * D * 16,
+                                   cudaMemcpyDeviceToHost, c->comp));
+      ISQ_CUDA_TRY(cudaStreamSynchronize(c->comp));
+    }
+    return ISQ_OK;
+  }
+  // pipelined: copy stream loads chunk i into buffer i%2 while comp scores chunk i-1
+  int64_t i = 0;
+  for (int64_t off = 0; off < count; off += chunk, ++i) {
+    const int b = (int)(i & 1);
+    const int64_t m = (count - off) < chunk ? (count - off) : chunk;
+    ISQ_CUDA_TRY(cudaStreamWaitEvent(c->copy, c->done[b], 0));  // buffer b free again
+    if (length > 0) {
+      ISQ_CUDA_TRY(cudaMemcpyAsync(c->codes[b], codes + off * length, m * length,
+                                   cudaMemcpyHostToDevice, c->copy));
+      ISQ_CUDA_TRY(cudaMemcpyAsync(c->thetas[b], thetas + off * length, m * length * 8,
+                                   cudaMemcpyHostToDevice, c->copy));
+    }
+    ISQ_CUDA_TRY(cudaEventRecord(c->loaded[b], c->copy));
+    ISQ_CUDA_TRY(cudaStreamWaitEvent(c->comp, c->loaded[b], 0));
+    st = launch_fitness_batch(n, length, m, c->codes[b], c->thetas[b], c->target, c->fit[b],
+                              nullptr, c->comp);
+    if (st != ISQ_OK) return st;
+    ISQ_CUDA_TRY(cudaMemcpyAsync(fitness_out + off, c->fit[b], m * 8, cudaMemcpyDeviceToHost, c->comp));
+    ISQ_CUDA_TRY(cudaEventRecord(c->done[b], c->comp));
+  }
+  ISQ_CUDA_TRY(cudaStreamSynchronize(c->comp));
+  return ISQ_OK;
 }
 
 isq_status isq_fitness_of_unitaries(int64_t dim, int64_t count, const double* unitaries,

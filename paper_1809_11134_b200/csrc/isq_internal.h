@@ -23,9 +23,14 @@ void set_error(const std::string& msg);
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreadsPerBlock = 32 * kWarpsPerBlock;
+// Fitness kernels: 2 warps per block keeps the per-warp chunk scratch
+// (FastChunk, ~9.6 KB) plus the target inside the 48 KB static shared limit.
+constexpr int kFitWarps = 2;
+constexpr int kFitThreads = 32 * kFitWarps;
 
-// Number of resident blocks for a persistent grid of `kernel` (blocks of 128 threads).
-int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps);
+// Number of resident blocks for a persistent grid of `kernel`.
+int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps,
+                    int warps_per_block = kWarpsPerBlock);
 
 // fitness / compose over explicit gate lists (device pointers).
 isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* codes,

@@ -15,17 +15,17 @@ struct ChunkShared {
 
 // Fitness only (the hot path): diagonal-phase accumulation + Pauli frame.
 template <int NQ>
-__global__ void __launch_bounds__(kThreadsPerBlock)
+__global__ void __launch_bounds__(kFitThreads)
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
                         double* __restrict__ fitness, const int32_t* __restrict__ stop) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kWarpsPerBlock];
+  __shared__ FastChunk sh[kFitWarps];
   if (stop != nullptr && *stop) return;
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
   __syncthreads();
-  fitness_rows<NQ>(count, L, codes, thetas, Ts, sh, fitness, kWarpsPerBlock);
+  fitness_rows<NQ>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps);
 }
 
 // Composition with the exact global phase (compose_gates readout) + fitness.
@@ -136,7 +136,7 @@ isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, con
   return ISQ_OK;
 }
 
-int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps) {
+int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps, int warps_per_block) {
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;
@@ -145,9 +145,9 @@ int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps) {
     if (num_sms <= 0) num_sms = 148;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreadsPerBlock, dyn_smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 32 * warps_per_block, dyn_smem);
   if (per_sm <= 0) per_sm = 1;
-  const int64_t need = (work_warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int64_t need = (work_warps + warps_per_block - 1) / warps_per_block;
   const int64_t full = (int64_t)num_sms * per_sm;
   int64_t g = need < full ? need : full;
   return (int)(g < 1 ? 1 : g);
@@ -159,8 +159,8 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
                             cudaStream_t stream) {
   if (unitary == nullptr) {
     const void* k = (const void*)fitness_fast_kernel<NQ>;
-    const int grid = persistent_grid(k, 0, count);
-    fitness_fast_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
+    const int grid = persistent_grid(k, 0, count, kFitWarps);
+    fitness_fast_kernel<NQ><<<grid, kFitThreads, 0, stream>>>(
         count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, nullptr);
     ISQ_CUDA_TRY(cudaGetLastError());
     return ISQ_OK;
@@ -179,8 +179,8 @@ static isq_status launch_fast_stoppable(int L, int64_t count, const uint8_t* cod
                                         const double* thetas, const double* target, double* fitness,
                                         const int32_t* stop, cudaStream_t stream) {
   const void* k = (const void*)fitness_fast_kernel<NQ>;
-  const int grid = persistent_grid(k, 0, count);
-  fitness_fast_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
+  const int grid = persistent_grid(k, 0, count, kFitWarps);
+  fitness_fast_kernel<NQ><<<grid, kFitThreads, 0, stream>>>(
       count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;

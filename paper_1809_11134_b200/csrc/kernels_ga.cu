@@ -57,16 +57,16 @@ __device__ __forceinline__ int ga_cur(const GaArgs& a) { return (int)(a.st->gene
 
 // ------------------------------------------------------------------ eval ---
 template <int NQ>
-__global__ void __launch_bounds__(kThreadsPerBlock) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
+__global__ void __launch_bounds__(kFitThreads) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kWarpsPerBlock];
+  __shared__ FastChunk sh[kFitWarps];
   if (a.st->stop) return;
   const int cur = ga_cur(a);
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = a.target[i];
   __syncthreads();
   fitness_rows<NQ>(c1 - c0, a.L, a.codes[cur] + c0 * a.L, a.thetas[cur] + c0 * a.L, Ts, sh,
-                   a.fitness + c0, kWarpsPerBlock);
+                   a.fitness + c0, kFitWarps);
 }
 
 // ---------------------------------------------------------------- reduce ---
@@ -321,8 +321,8 @@ static int ga_blocks(int64_t n) {
 template <int NQ>
 static isq_status ga_launch_eval_nq(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
   const void* k = (const void*)ga_eval_kernel<NQ>;
-  const int grid = persistent_grid(k, 0, c1 - c0);
-  ga_eval_kernel<NQ><<<grid, kThreadsPerBlock, 0, s>>>(a, c0, c1);
+  const int grid = persistent_grid(k, 0, c1 - c0, kFitWarps);
+  ga_eval_kernel<NQ><<<grid, kFitThreads, 0, s>>>(a, c0, c1);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
