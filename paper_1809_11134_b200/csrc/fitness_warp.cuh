@@ -8,11 +8,12 @@
 //     S_true  ~  diag(e^{i phi}) . S_phys          (up to a global phase / sign)
 //
 //   S_phys : register state (WarpUnitary layout, unitary_warp.cuh)
-//   phi    : pending per-row phases; lane r holds phi_r (r < D)
+//   phi    : pending per-row phases, carried as the unit complex factor
+//            e^{i phi_r} on lane r (r < D), so flushes need no sincos
 //
 // * Rz and ZZ are diagonal: e^{-i th/2} diag(1 | e^{i th}) over the rows whose
 //   wire bit (Rz) or bit parity (ZZ) is 1.  They commute with phi, so each
-//   costs one predicated DADD per lane (phi_r += th * g(r)) and no per-gate
+//   costs one predicated complex multiply per lane (w_r *= e^{i th g(r)}), no per-gate
 //   code path.
 // * An Rx/Ry rotation on row bit b only fails to commute with the part of phi
 //   that differs between rows r and r ^ 2^b.  Those deltas are flushed into
@@ -46,11 +47,12 @@ template <int NQ>
 struct FastEval {
   using G = Geo<NQ>;
   WarpUnitary<NQ> st;
-  double phi;  // pending phase of physical row `lane` (lane < D)
+  double wr, wi;  // pending phase factor e^{i phi} of physical row `lane` (lane < D)
 
   __device__ __forceinline__ void begin(int lane) {
     st.set_identity(lane);
-    phi = 0.0;
+    wr = 1.0;
+    wi = 0.0;
   }
 
   // Lane-parallel gate preparation for one position.
@@ -62,7 +64,7 @@ struct FastEval {
       const int b = NQ - 1 - w0;  // row bit of the wire (wire 1 = MSB)
       if (axis == 2) {
         info = GT_DIAG | ((1 << b) << 8);
-        c0 = theta;
+        sincos(theta, &c1, &c0);  // e^{i theta} = (c0, c1)
         return;
       }
       // plane angle, reduced to [-pi/2, pi/2] up to a global sign
@@ -85,7 +87,7 @@ struct FastEval {
     }
     const int j = i + 1 + tt;
     info = GT_DIAG | (((1 << (NQ - i)) | (1 << (NQ - j))) << 8);
-    c0 = theta;
+    sincos(theta, &c1, &c0);
   }
 
   // Multiply the register rows with bit B set by fac[row] (flush of pending deltas).
@@ -150,21 +152,34 @@ struct FastEval {
       const int inf = sm.info[q];
       const int type = inf & 3;
       if (type == GT_DIAG) {
-        if (__popc(row & (inf >> 8)) & 1) phi += sm.c0[q];
+        if (__popc(row & (inf >> 8)) & 1) {
+          const double c = sm.c0[q], s = sm.c1[q];
+          const double t = wr * s;
+          wr = fma(wr, c, -wi * s);
+          wi = fma(wi, c, t);
+        }
         continue;
       }
       const int b = inf >> 8;
       const int m = 1 << b;
-      const double other = __shfl_xor_sync(0xffffffffu, phi, m);
-      const double delta = (has_row && (row & m)) ? phi - other : 0.0;
-      if (__any_sync(0xffffffffu, delta != 0.0)) {
-        double ds = 0.0, dc = 1.0;
-        if (delta != 0.0) sincos(delta, &ds, &dc);
-        sm.fac[lane] = make_double2(dc, ds);
+      const double orr = __shfl_xor_sync(0xffffffffu, wr, m);
+      const double ori = __shfl_xor_sync(0xffffffffu, wi, m);
+      const bool differs = has_row && (row & m) && (wr != orr || wi != ori);
+      if (__any_sync(0xffffffffu, differs)) {
+        // flush factor of the rows with bit b set: w_r * conj(w_{r^m})
+        double fr = 1.0, fi = 0.0;
+        if (differs) {
+          fr = fma(wr, orr, wi * ori);
+          fi = fma(wi, orr, -wr * ori);
+        }
+        sm.fac[lane] = make_double2(fr, fi);
         __syncwarp();
         flush(b, sm.fac, lane);
         __syncwarp();
-        if (row & m) phi = other;
+        if (row & m) {
+          wr = orr;
+          wi = ori;
+        }
       }
       rotate(type, b, sm.c0[q], sm.c1[q], sm.c2[q], lane);
     }
@@ -173,11 +188,7 @@ struct FastEval {
 
   // Fitness from the final state (fitness.py:36-49).
   __device__ __forceinline__ double finish(const double2* __restrict__ T, FastChunk& sm, int lane) {
-    if (lane < G::D) {
-      double s, c;
-      sincos(phi, &s, &c);
-      sm.fac[lane] = make_double2(c, -s);
-    }
+    if (lane < G::D) sm.fac[lane] = make_double2(wr, -wi);  // e^{-i phi}
     __syncwarp();
     const int j = lane & (G::D - 1);
     const int h = (lane >> NQ) & (G::LPC - 1);

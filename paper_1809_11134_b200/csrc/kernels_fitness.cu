@@ -14,8 +14,10 @@ struct ChunkShared {
 };
 
 // Fitness only (the hot path): diagonal-phase accumulation + Pauli frame.
+// 6 resident 2-warp blocks per SM (<= 170 registers) gives 3 warps per
+// scheduler for the n = 5 register-resident state.
 template <int NQ>
-__global__ void __launch_bounds__(kFitThreads)
+__global__ void __launch_bounds__(kFitThreads, 6)
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
                         double* __restrict__ fitness, const int32_t* __restrict__ stop) {

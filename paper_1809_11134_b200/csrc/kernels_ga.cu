@@ -57,7 +57,7 @@ __device__ __forceinline__ int ga_cur(const GaArgs& a) { return (int)(a.st->gene
 
 // ------------------------------------------------------------------ eval ---
 template <int NQ>
-__global__ void __launch_bounds__(kFitThreads) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
+__global__ void __launch_bounds__(kFitThreads, 6) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
   __shared__ FastChunk sh[kFitWarps];
