@@ -78,5 +78,10 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build_library(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    try:
+        build_library(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    except RuntimeError as exc:
+        print("BUILD FAILED\n" + str(exc)[-3000:], file=sys.stderr)
+        print("BUILD FAILED")
+        sys.exit(1)
+    print("built", LIB)

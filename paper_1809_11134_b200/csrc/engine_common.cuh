@@ -74,7 +74,7 @@ struct QeqeaArgs {
   uint8_t* gate_codes;   // shard * L gate codes of the generation (params -> fitness)
   double* gate_thetas;   // shard * L live angles
   double* touch_fbefore;  // shard * L slot_max each touch started the generation from
-  uint8_t* touch_mutated; // shard * L pending-mutation flag of each touch
+  uint8_t* touch_mutated; // shard * L: bit 0 pending mutation, bit 1 it is a qutrit mutation
   int fused_commit;       // 1: single rank, commit+table fused over the touch records
   QeqeaDevState* st;
   GenRecord* records;
@@ -180,13 +180,14 @@ __device__ __forceinline__ void su3_one_param(int which, double v, double2 q[3])
 // Draw layout of the first block: w0 mask, w1 coin, w2 integers(8) (low
 // u32) or the angle sign, w3 the SU(3) parameter value.
 __device__ __forceinline__ bool mutate_slot(const QeqeaArgs& a, int64_t s, uint64_t mg, double f,
-                                            LiveSlot& v) {
+                                            LiveSlot& v, bool* qutrit_path = nullptr) {
   uint64_t w[4];
   stream_block(a.seed, DOM_MUTATE, mg, (uint64_t)s, 0, 1, w);
   if (!(u64_to_double(w[0]) < a.p_mut)) return false;
   if (!(f < 1.0)) return false;
   const bool coin = u64_to_double(w[1]) < 0.5;
   const double omf = __dsub_rn(1.0, f);
+  if (qutrit_path) *qutrit_path = coin && s < a.Qt;
   if (coin && s < a.Qt) {
     const int which = (int)((uint32_t)(w[2] & 0xffffffffULL) >> 29);  // Lemire, bound 8
     const double range = which < 3 ? kHalfPiD : kTwoPiD;             // encoding.py:23

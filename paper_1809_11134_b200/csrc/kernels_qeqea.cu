@@ -43,38 +43,44 @@ __global__ void __launch_bounds__(kThreadsPerBlock) qeqea_sample_flats_kernel(Qe
 // whether the slot carries a pending mutation (the fused single-rank commit
 // consumes both).
 constexpr int kValThreads = 256;
+constexpr int kValPerThread = 3;  // touches per thread per tile: ~1 measurement task per thread
 
-struct MeasureTask {
-  double2 q[3];
+struct MeasureTask {  // 56 B: 768 tasks fit the 48 KB static shared limit
+  double re[3], im[3];
   uint32_t s;
   uint32_t out;
 };
 
 __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t0, int64_t t1) {
-  __shared__ MeasureTask tasks[kValThreads];
+  __shared__ MeasureTask tasks[kValThreads * kValPerThread];
   __shared__ int ntask;
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
-  for (int64_t base = t0 + (int64_t)blockIdx.x * kValThreads; base < t1;
-       base += (int64_t)gridDim.x * kValThreads) {
+  constexpr int kTile = kValThreads * kValPerThread;
+  for (int64_t base = t0 + (int64_t)blockIdx.x * kTile; base < t1; base += (int64_t)gridDim.x * kTile) {
     if (threadIdx.x == 0) ntask = 0;
     __syncthreads();
-    const int64_t i = base + threadIdx.x;
-    if (i < t1) {
+#pragma unroll
+    for (int u = 0; u < kValPerThread; ++u) {
+      const int64_t i = base + u * kValThreads + threadIdx.x;
+      if (i >= t1) break;
       const uint32_t s = a.flats[i];
       LiveSlot v;
       const double f = load_committed(a, s, v);
-      const bool mutated = g > 0 && mutate_slot(a, s, g - 1, f, v);
+      bool qpath = false;
+      const bool mutated = g > 0 && mutate_slot(a, s, g - 1, f, v, &qpath);
       const int64_t o = i - t0;
       a.gate_thetas[o] = v.theta;
       a.touch_fbefore[o] = f;
-      a.touch_mutated[o] = mutated;
+      a.touch_mutated[o] = (uint8_t)((mutated ? 1 : 0) | (mutated && qpath ? 2 : 0));
       const int64_t kind = (int64_t)s / (a.L * a.P);
       if (kind < a.n) {
         const int k = atomicAdd(&ntask, 1);
-        tasks[k].q[0] = v.q[0];
-        tasks[k].q[1] = v.q[1];
-        tasks[k].q[2] = v.q[2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          tasks[k].re[c] = v.q[c].x;
+          tasks[k].im[c] = v.q[c].y;
+        }
         tasks[k].s = s;
         tasks[k].out = (uint32_t)o;
       } else {
@@ -86,8 +92,8 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       const MeasureTask& t = tasks[k];
       NpStream st;
       st.init(a.seed, DOM_MEASURE, g, (uint64_t)t.s, 0);
-      double re[3] = {t.q[0].x, t.q[1].x, t.q[2].x};
-      double im[3] = {t.q[0].y, t.q[1].y, t.q[2].y};
+      double re[3] = {t.re[0], t.re[1], t.re[2]};
+      double im[3] = {t.im[0], t.im[1], t.im[2]};
       bool ok = true;
       const int axis = measure_axis(re, im, a.n_meas, st, &ok);
       const int64_t kind = (int64_t)t.s / (a.L * a.P);
@@ -231,11 +237,22 @@ __global__ void __launch_bounds__(256) qeqea_commit_table_kernel(QeqeaArgs a) {
     const double fb = a.touch_fbefore[i];
     if (!(fit > fb)) continue;
     const uint32_t s = a.flats[i];
-    if (a.touch_mutated[i] && atomicMax(&a.claim[s], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
-      LiveSlot v;
-      load_committed(a, s, v);  // commit writes only theta / qutrit, never slot_max
-      mutate_slot(a, s, g - 1, fb, v);
-      store_committed(a, s, v);
+    const uint8_t mf = a.touch_mutated[i];
+    if (mf & 2) {
+      // qutrit mutation: one improving touch per slot recomputes and writes it
+      if (atomicMax(&a.claim[s], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
+        LiveSlot v;
+        load_committed(a, s, v);  // commit writes only theta / qutrit, never slot_max
+        mutate_slot(a, s, g - 1, fb, v);
+        store_committed(a, s, v);
+      }
+    } else if (mf & 1) {
+      // angle mutation: every improving touch holds the same live angle
+      // (values kernel), so the idempotent store needs no arbitration
+      if (s < a.Qt)
+        a.rot[s].theta = a.gate_thetas[i];
+      else
+        a.inter[s - a.Qt].theta = a.gate_thetas[i];
     }
     atomicMax(reinterpret_cast<unsigned long long*>(smax_ptr(a, s)),
               (unsigned long long)__double_as_longlong(fit));
