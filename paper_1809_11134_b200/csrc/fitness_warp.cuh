@@ -13,16 +13,19 @@
 //
 // * Rz and ZZ are diagonal: e^{-i th/2} diag(1 | e^{i th}) over the rows whose
 //   wire bit (Rz) or bit parity (ZZ) is 1.  They commute with phi, so each
-//   costs one predicated complex multiply per lane (w_r *= e^{i th g(r)}), no per-gate
-//   code path.
-// * An Rx/Ry rotation on row bit b only fails to commute with the part of phi
-//   that differs between rows r and r ^ 2^b.  Those deltas are flushed into
-//   the rows with bit b set (skipped when all are 0), then the rotation is
-//   applied as a rotation by a = -th/2 (Rx) or +th/2 (Ry) of two real planes
-//   per row pair, reduced to |a| <= pi/2 (R(a) = -R(a -+ pi), a global sign),
-//   with the in-place 3-shear lifting x += p y; y += q x; x += p y.  In-place
-//   updates keep every switch case free of register moves, so the hot code is
-//   2n rotation cases + n flush cases and fits the instruction cache.
+//   costs one predicated complex multiply per lane (w_r *= e^{i th g(r)}).
+//   The rotation positions of a 32-gate chunk come from one ballot; the
+//   diagonal runs between them are branch-free loops over the pending phase.
+// * Ry = S Rx S^dagger with S = diag(1, i) on the wire, and both S factors are
+//   diagonal, so they go into phi and every rotation is an Rx.
+// * An Rx on row bit b only fails to commute with the part of phi that
+//   differs between rows r and r ^ 2^b.  Those deltas are flushed into the
+//   rows with bit b set (skipped when all are 0), then the rotation is
+//   applied as a rotation by a = -th/2 of the planes (re_r, im_r'), (re_r', im_r)
+//   of every row pair, reduced to |a| <= pi/2 (R(a) = -R(a -+ pi), a global
+//   sign), with the in-place 3-shear lifting x += p y; y += q x; x += p y.
+//   In-place updates keep every switch case free of register moves, so the
+//   hot code is n rotation cases + n flush cases and fits the instruction cache.
 // * At the end |tr(S_true^dagger T)| = |sum_kj conj(S_phys[k][j]) e^{-i phi_k} T[k][j]|.
 #pragma once
 #include "unitary_warp.cuh"
@@ -31,10 +34,9 @@ namespace isq {
 
 // Per-warp shared scratch for one 32-gate chunk.
 struct FastChunk {
-  int info[32];      // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit or row mask
-  double c0[32];     // diag: theta ; rotation: p = -tan(a/2)
-  double c1[32];     // rotation: q = sin a
+  double2 cs[32];    // diag: (cos th, sin th) ; rotation: (p = -tan(a/2), q = sin a)
   double c2[32];     // rotation: C = cos a (lane-bit form)
+  int info[32];      // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit or row mask
   double2 fac[32];   // flush factors / final row weights, indexed by physical row
 };
 
@@ -68,7 +70,7 @@ struct FastEval {
         return;
       }
       // plane angle, reduced to [-pi/2, pi/2] up to a global sign
-      double a = remainder(theta, kTwoPi) * (axis == 0 ? -0.5 : 0.5);
+      double a = -0.5 * remainder(theta, kTwoPi);
       if (a > 0.5 * kPi) a -= kPi;
       if (a < -0.5 * kPi) a += kPi;
       double sh, ch;
@@ -113,55 +115,64 @@ struct FastEval {
     }
   }
 
-  __device__ __forceinline__ void rotate(int type, int b, double p, double q, double C, int lane) {
-    if (type == GT_RX) {
-      switch (b) {
-        case 0: st.template lift<0, 0>(p, q, C, lane); break;
-        case 1: if constexpr (NQ > 1) st.template lift<1, 0>(p, q, C, lane); break;
-        case 2: if constexpr (NQ > 2) st.template lift<2, 0>(p, q, C, lane); break;
-        case 3: if constexpr (NQ > 3) st.template lift<3, 0>(p, q, C, lane); break;
-        case 4: if constexpr (NQ > 4) st.template lift<4, 0>(p, q, C, lane); break;
-        default: break;
-      }
-    } else {
-      switch (b) {
-        case 0: st.template lift<0, 1>(p, q, C, lane); break;
-        case 1: if constexpr (NQ > 1) st.template lift<1, 1>(p, q, C, lane); break;
-        case 2: if constexpr (NQ > 2) st.template lift<2, 1>(p, q, C, lane); break;
-        case 3: if constexpr (NQ > 3) st.template lift<3, 1>(p, q, C, lane); break;
-        case 4: if constexpr (NQ > 4) st.template lift<4, 1>(p, q, C, lane); break;
-        default: break;
-      }
+  __device__ __forceinline__ void rotate(int b, double p, double q, double C, int lane) {
+    switch (b) {
+      case 0: st.template lift<0, 0>(p, q, C, lane); break;
+      case 1: if constexpr (NQ > 1) st.template lift<1, 0>(p, q, C, lane); break;
+      case 2: if constexpr (NQ > 2) st.template lift<2, 0>(p, q, C, lane); break;
+      case 3: if constexpr (NQ > 3) st.template lift<3, 0>(p, q, C, lane); break;
+      case 4: if constexpr (NQ > 4) st.template lift<4, 0>(p, q, C, lane); break;
+      default: break;
+    }
+  }
+
+  // Pending phase of this lane's row times the diagonal gates [q, qe) of the
+  // chunk (all of them diagonal): branch-free, one predicated complex
+  // multiply per gate.
+  __device__ __forceinline__ void diag_run(int q, int qe, const FastChunk& sm, int row) {
+#pragma unroll 2
+    for (; q < qe; ++q) {
+      const int mask = sm.info[q] >> 8;
+      const double2 e = sm.cs[q];
+      const bool odd = __popc(row & mask) & 1;
+      const double c = odd ? e.x : 1.0, s = odd ? e.y : 0.0;
+      const double t = wr * s;
+      wr = fma(wr, c, -wi * s);
+      wi = fma(wi, c, t);
     }
   }
 
   // One chunk: lane q < nq supplies (code_q, theta_q) for position base+q.
+  // The rotation positions are found with one ballot; the diagonal runs
+  // between them touch only the pending phase (diag_run), the rotations
+  // flush the non-commuting part of it and rotate the register state.
   __device__ __forceinline__ void chunk(int code, double theta, int nq, FastChunk& sm, int lane) {
     int info = GT_DIAG;  // lanes past the end: neutral diagonal with an empty mask
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
     if (lane < nq) prepare(code, theta, info, c0, c1, c2);
     sm.info[lane] = info;
-    sm.c0[lane] = c0;
-    sm.c1[lane] = c1;
+    sm.cs[lane] = make_double2(c0, c1);
     sm.c2[lane] = c2;
+    unsigned rot = __ballot_sync(0xffffffffu, (info & 3) != GT_DIAG);
     __syncwarp();
     const int row = lane;  // physical row whose phase this lane carries
     const bool has_row = lane < G::D;
-#pragma unroll 1
-    for (int q = 0; q < nq; ++q) {
-      const int inf = sm.info[q];
-      const int type = inf & 3;
-      if (type == GT_DIAG) {
-        if (__popc(row & (inf >> 8)) & 1) {
-          const double c = sm.c0[q], s = sm.c1[q];
-          const double t = wr * s;
-          wr = fma(wr, c, -wi * s);
-          wi = fma(wi, c, t);
-        }
-        continue;
-      }
+    int q = 0;
+    for (;;) {
+      const int qr = rot ? __ffs(rot) - 1 : nq;
+      diag_run(q, qr, sm, row);
+      if (qr >= nq) break;
+      rot &= rot - 1;
+      q = qr + 1;
+      const int inf = sm.info[qr];
       const int b = inf >> 8;
       const int m = 1 << b;
+      const bool ry = (inf & 3) == GT_RY;
+      if (ry && (row & m)) {  // S^dagger: rows with the wire bit set pick up -i
+        const double t = wr;
+        wr = wi;
+        wi = -t;
+      }
       const double orr = __shfl_xor_sync(0xffffffffu, wr, m);
       const double ori = __shfl_xor_sync(0xffffffffu, wi, m);
       const bool differs = has_row && (row & m) && (wr != orr || wi != ori);
@@ -181,7 +192,13 @@ struct FastEval {
           wi = ori;
         }
       }
-      rotate(type, b, sm.c0[q], sm.c1[q], sm.c2[q], lane);
+      const double2 pq = sm.cs[qr];
+      rotate(b, pq.x, pq.y, sm.c2[qr], lane);
+      if (ry && (row & m)) {  // S: rows with the wire bit set pick up +i
+        const double t = wr;
+        wr = -wi;
+        wi = t;
+      }
     }
     __syncwarp();
   }
