@@ -14,8 +14,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = ROOT / "build" / "isq"
-LIB = PKG / "libisq.so"
+BUILD = Path(os.environ.get("ISQ_BUILD_DIR") or ROOT / "build" / "isq")
+LIB = Path(os.environ.get("ISQ_LIBRARY") or PKG / "libisq.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
@@ -56,7 +56,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path) -> tuple[Path, str]:
         obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        extra = os.environ.get("ISQ_NVCC_EXTRA", "").split()
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         proc = subprocess.run(cmd, capture_output=True, text=True)
         if proc.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{proc.stdout}\n{proc.stderr}")

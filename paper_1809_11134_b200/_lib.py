@@ -6,6 +6,7 @@ usable, calls raise instead of computing anything on the host.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -13,7 +14,8 @@ import numpy as np
 
 from .errors import ConfigurationError, InvariantViolation
 
-LIB_PATH = Path(__file__).resolve().parent / "libisq.so"
+# ISQ_LIBRARY: an alternative in-tree build of the same library (kernel-variant experiments)
+LIB_PATH = Path(os.environ.get("ISQ_LIBRARY") or Path(__file__).resolve().parent / "libisq.so")
 
 ISQ_OK = 0
 ISQ_ERR_CONFIG = 1

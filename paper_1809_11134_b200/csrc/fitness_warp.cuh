@@ -34,10 +34,10 @@ namespace isq {
 
 // Per-warp shared scratch for one 32-gate chunk.
 struct FastChunk {
-  double2 cs[32];    // diag: (cos th, sin th) ; rotation: (p = -tan(a/2), q = sin a)
-  double c2[32];     // rotation: C = cos a (lane-bit form)
-  int info[32];      // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit or row mask
-  double2 fac[32];   // flush factors / final row weights, indexed by physical row
+  double2 cs2[32][2];  // diag: {(1, 0), (cos th, sin th)}; rotation: {(C = cos a, 0), (p, q)}
+  int dmask[32];       // diag: row mask whose parity picks up e^{i th}; 0 for rotations
+  int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit
+  double2 fac[32];     // flush factors / final row weights, indexed by physical row
 };
 
 enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
@@ -57,39 +57,49 @@ struct FastEval {
     wi = 0.0;
   }
 
-  // Lane-parallel gate preparation for one position.
-  __device__ __forceinline__ static void prepare(int code, double theta, int& info, double& c0,
-                                                 double& c1, double& c2) {
-    c1 = c2 = 0.0;
+  // Lane-parallel gate preparation for one position (one sincos call site
+  // for every gate type, so a chunk pays for it once).
+  __device__ __forceinline__ static void prepare(int code, double theta, int& info, int& dmask,
+                                                 double2& e0, double2& e1) {
+    int b = -1, type = GT_DIAG, mask;
     if (code < 3 * NQ) {
       const int w0 = code / 3, axis = code - 3 * w0;
-      const int b = NQ - 1 - w0;  // row bit of the wire (wire 1 = MSB)
-      if (axis == 2) {
-        info = GT_DIAG | ((1 << b) << 8);
-        sincos(theta, &c1, &c0);  // e^{i theta} = (c0, c1)
-        return;
+      const int rb = NQ - 1 - w0;  // row bit of the wire (wire 1 = MSB)
+      mask = 1 << rb;
+      if (axis != 2) {
+        b = rb;
+        type = axis == 0 ? GT_RX : GT_RY;
       }
+    } else {
+      int i = 1, tt = code - 3 * NQ;
+      while (tt >= NQ - i) {
+        tt -= NQ - i;
+        ++i;
+      }
+      const int j = i + 1 + tt;
+      mask = (1 << (NQ - i)) | (1 << (NQ - j));
+    }
+    double x = theta;
+    if (b >= 0) {
       // plane angle, reduced to [-pi/2, pi/2] up to a global sign
       double a = -0.5 * remainder(theta, kTwoPi);
       if (a > 0.5 * kPi) a -= kPi;
       if (a < -0.5 * kPi) a += kPi;
-      double sh, ch;
-      sincos(0.5 * a, &sh, &ch);
-      info = (axis == 0 ? GT_RX : GT_RY) | (b << 8);
-      c0 = -sh / ch;
-      c1 = 2.0 * sh * ch;
-      c2 = fma(ch, ch, -sh * sh);
-      return;
+      x = 0.5 * a;
     }
-    const int t = code - 3 * NQ;
-    int i = 1, tt = t;
-    while (tt >= NQ - i) {
-      tt -= NQ - i;
-      ++i;
+    double sn, cs;
+    sincos(x, &sn, &cs);
+    if (b >= 0) {
+      info = type | (b << 8);
+      dmask = 0;
+      e0 = make_double2(fma(cs, cs, -sn * sn), 0.0);
+      e1 = make_double2(-sn / cs, 2.0 * sn * cs);
+    } else {
+      info = GT_DIAG;
+      dmask = mask;
+      e0 = make_double2(1.0, 0.0);
+      e1 = make_double2(cs, sn);
     }
-    const int j = i + 1 + tt;
-    info = GT_DIAG | (((1 << (NQ - i)) | (1 << (NQ - j))) << 8);
-    sincos(theta, &c1, &c0);
   }
 
   // Multiply the register rows with bit B set by fac[row] (flush of pending deltas).
@@ -132,13 +142,10 @@ struct FastEval {
   __device__ __forceinline__ void diag_run(int q, int qe, const FastChunk& sm, int row) {
 #pragma unroll 2
     for (; q < qe; ++q) {
-      const int mask = sm.info[q] >> 8;
-      const double2 e = sm.cs[q];
-      const bool odd = __popc(row & mask) & 1;
-      const double c = odd ? e.x : 1.0, s = odd ? e.y : 0.0;
-      const double t = wr * s;
-      wr = fma(wr, c, -wi * s);
-      wi = fma(wi, c, t);
+      const double2 e = sm.cs2[q][__popc(row & sm.dmask[q]) & 1];
+      const double t = wr * e.y;
+      wr = fma(wr, e.x, -wi * e.y);
+      wi = fma(wi, e.x, t);
     }
   }
 
@@ -147,13 +154,14 @@ struct FastEval {
   // between them touch only the pending phase (diag_run), the rotations
   // flush the non-commuting part of it and rotate the register state.
   __device__ __forceinline__ void chunk(int code, double theta, int nq, FastChunk& sm, int lane) {
-    int info = GT_DIAG;  // lanes past the end: neutral diagonal with an empty mask
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    if (lane < nq) prepare(code, theta, info, c0, c1, c2);
+    int info = GT_DIAG, dmask = 0;  // lanes past the end: neutral diagonal, empty mask
+    double2 e0 = make_double2(1.0, 0.0), e1 = e0;
+    if (lane < nq) prepare(code, theta, info, dmask, e0, e1);
     sm.info[lane] = info;
-    sm.cs[lane] = make_double2(c0, c1);
-    sm.c2[lane] = c2;
-    unsigned rot = __ballot_sync(0xffffffffu, (info & 3) != GT_DIAG);
+    sm.dmask[lane] = dmask;
+    sm.cs2[lane][0] = e0;
+    sm.cs2[lane][1] = e1;
+    unsigned rot = __ballot_sync(0xffffffffu, info != GT_DIAG);
     __syncwarp();
     const int row = lane;  // physical row whose phase this lane carries
     const bool has_row = lane < G::D;
@@ -192,8 +200,8 @@ struct FastEval {
           wi = ori;
         }
       }
-      const double2 pq = sm.cs[qr];
-      rotate(b, pq.x, pq.y, sm.c2[qr], lane);
+      const double2 pq = sm.cs2[qr][1];
+      rotate(b, pq.x, pq.y, sm.cs2[qr][0].x, lane);
       if (ry && (row & m)) {  // S: rows with the wire bit set pick up +i
         const double t = wr;
         wr = -wi;
@@ -242,20 +250,34 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
   const int wib = threadIdx.x >> 5;
   FastChunk& cs = sh[wib];
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
-  for (int64_t c = (int64_t)blockIdx.x * warps_per_block + wib; c < count; c += nwarps) {
+  int64_t c = (int64_t)blockIdx.x * warps_per_block + wib;
+  // (code, theta) of the next chunk are loaded one chunk ahead
+  int code = 0;
+  double th = 0.0;
+  if (c < count && lane < L) {
+    code = codes[c * (int64_t)L + lane];
+    th = thetas[c * (int64_t)L + lane];
+  }
+  for (; c < count; c += nwarps) {
     FastEval<NQ> ev;
     ev.begin(lane);
-    const uint8_t* cc = codes + c * (int64_t)L;
-    const double* ct = thetas + c * (int64_t)L;
     for (int base = 0; base < L; base += 32) {
       const int nq = min(32, L - base);
-      int code = 0;
-      double th = 0.0;
-      if (lane < nq) {
-        code = cc[base + lane];
-        th = ct[base + lane];
+      int64_t nc = c;
+      int nb = base + 32;
+      if (nb >= L) {
+        nc = c + nwarps;
+        nb = 0;
+      }
+      int ncode = 0;
+      double nth = 0.0;
+      if (nc < count && nb + lane < L) {
+        ncode = codes[nc * (int64_t)L + nb + lane];
+        nth = thetas[nc * (int64_t)L + nb + lane];
       }
       ev.chunk(code, th, nq, cs, lane);
+      code = ncode;
+      th = nth;
     }
     const double f = ev.finish(Ts, cs, lane);
     if (lane == 0) fitness[c] = f;

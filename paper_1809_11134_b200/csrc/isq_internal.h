@@ -28,6 +28,7 @@ constexpr int kThreadsPerBlock = 32 * kWarpsPerBlock;
 constexpr int kFitWarps = 2;
 constexpr int kFitThreads = 32 * kFitWarps;
 
+int num_sms();
 // Number of resident blocks for a persistent grid of `kernel`.
 int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps,
                     int warps_per_block = kWarpsPerBlock);
@@ -41,7 +42,7 @@ isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* code
 isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
                                           const double* thetas, const double* target_dev,
                                           double* fitness_dev, const int32_t* stop,
-                                          cudaStream_t stream);
+                                          cudaStream_t stream, int blocks_per_sm = 0);
 
 isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, const double* T,
                                   double* out, cudaStream_t stream);

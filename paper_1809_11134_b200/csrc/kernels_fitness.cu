@@ -13,11 +13,12 @@ struct ChunkShared {
   double b[32];
 };
 
-// Fitness only (the hot path): diagonal-phase accumulation + Pauli frame.
-// 6 resident 2-warp blocks per SM (<= 170 registers) gives 3 warps per
-// scheduler for the n = 5 register-resident state.
-template <int NQ>
-__global__ void __launch_bounds__(kFitThreads, 6)
+// Fitness only (the hot path).  MINB = 6 resident 2-warp blocks per SM
+// (<= 168 registers) gives 3 warps per scheduler for the n = 5
+// register-resident state (measured: 2 warps per scheduler at 244 registers
+// is 11 % slower).
+template <int NQ, int MINB>
+__global__ void __launch_bounds__(kFitThreads, MINB)
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
                         double* __restrict__ fitness, const int32_t* __restrict__ stop) {
@@ -138,14 +139,19 @@ isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, con
   return ISQ_OK;
 }
 
-int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps, int warps_per_block) {
-  static int num_sms = 0;
-  if (num_sms == 0) {
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (num_sms <= 0) num_sms = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
+  return n;
+}
+
+int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps, int warps_per_block) {
+  const int num_sms = isq::num_sms();
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 32 * warps_per_block, dyn_smem);
   if (per_sm <= 0) per_sm = 1;
@@ -160,9 +166,9 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
                             const double* target, double* fitness, double* unitary,
                             cudaStream_t stream) {
   if (unitary == nullptr) {
-    const void* k = (const void*)fitness_fast_kernel<NQ>;
+    const void* k = (const void*)fitness_fast_kernel<NQ, 6>;
     const int grid = persistent_grid(k, 0, count, kFitWarps);
-    fitness_fast_kernel<NQ><<<grid, kFitThreads, 0, stream>>>(
+    fitness_fast_kernel<NQ, 6><<<grid, kFitThreads, 0, stream>>>(
         count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, nullptr);
     ISQ_CUDA_TRY(cudaGetLastError());
     return ISQ_OK;
@@ -176,13 +182,14 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
   return ISQ_OK;
 }
 
-template <int NQ>
+template <int NQ, int MINB>
 static isq_status launch_fast_stoppable(int L, int64_t count, const uint8_t* codes,
                                         const double* thetas, const double* target, double* fitness,
-                                        const int32_t* stop, cudaStream_t stream) {
-  const void* k = (const void*)fitness_fast_kernel<NQ>;
-  const int grid = persistent_grid(k, 0, count, kFitWarps);
-  fitness_fast_kernel<NQ><<<grid, kFitThreads, 0, stream>>>(
+                                        const int32_t* stop, int blocks_per_sm, cudaStream_t stream) {
+  const void* k = (const void*)fitness_fast_kernel<NQ, MINB>;
+  int grid = persistent_grid(k, 0, count, kFitWarps);
+  if (blocks_per_sm > 0 && grid > num_sms() * blocks_per_sm) grid = num_sms() * blocks_per_sm;
+  fitness_fast_kernel<NQ, MINB><<<grid, kFitThreads, 0, stream>>>(
       count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
@@ -191,13 +198,14 @@ static isq_status launch_fast_stoppable(int L, int64_t count, const uint8_t* cod
 isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
                                           const double* thetas, const double* target,
                                           double* fitness, const int32_t* stop,
-                                          cudaStream_t stream) {
+                                          cudaStream_t stream, int blocks_per_sm) {
   if (count <= 0) return ISQ_OK;
+  const int b = blocks_per_sm;
   switch (n) {
-    case 2: return launch_fast_stoppable<2>(L, count, codes, thetas, target, fitness, stop, stream);
-    case 3: return launch_fast_stoppable<3>(L, count, codes, thetas, target, fitness, stop, stream);
-    case 4: return launch_fast_stoppable<4>(L, count, codes, thetas, target, fitness, stop, stream);
-    case 5: return launch_fast_stoppable<5>(L, count, codes, thetas, target, fitness, stop, stream);
+    case 2: return launch_fast_stoppable<2, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
+    case 3: return launch_fast_stoppable<3, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
+    case 4: return launch_fast_stoppable<4, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
+    case 5: return launch_fast_stoppable<5, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
     default:
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;

@@ -24,14 +24,15 @@ namespace isq {
 // keep each one's hot code inside the instruction cache and give the random
 // bank gathers thread-level memory parallelism.
 
-__global__ void __launch_bounds__(kThreadsPerBlock) qeqea_sample_flats_kernel(QeqeaArgs a) {
+__global__ void __launch_bounds__(kThreadsPerBlock)
+    qeqea_sample_flats_kernel(QeqeaArgs a, int64_t c0, int64_t c1) {
   __shared__ uint64_t blk[kWarpsPerBlock][36];
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
-  for (int64_t c = (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < a.P; c += nwarps)
+  for (int64_t c = c0 + (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < c1; c += nwarps)
     sample_circuit_warp(a, g, c, a.flats + c * a.L, blk[wib], lane);
 }
 
@@ -191,11 +192,19 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
   const int lane = threadIdx.x;
   const uint64_t g = st->generation;
   for (int p = lane; p < a.L; p += 32) {
-    const int64_t s = a.flats[s_best * a.L + p];
-    LiveSlot v;
-    live_slot(a, s, g, v);
-    a.best_codes[p] = (uint8_t)slot_gate_code(a, s, g, v);
-    a.best_thetas[p] = v.theta;
+    if (a.fused_commit) {
+      // single rank: the generation's gate codes / live angles of every
+      // circuit are still in place (and the commit may already be rewriting
+      // the bank, so do not recompute them from it)
+      a.best_codes[p] = a.gate_codes[s_best * a.L + p];
+      a.best_thetas[p] = a.gate_thetas[s_best * a.L + p];
+    } else {
+      const int64_t s = a.flats[s_best * a.L + p];
+      LiveSlot v;
+      live_slot(a, s, g, v);
+      a.best_codes[p] = (uint8_t)slot_gate_code(a, s, g, v);
+      a.best_thetas[p] = v.theta;
+    }
   }
 }
 
@@ -224,14 +233,16 @@ __global__ void __launch_bounds__(256) qeqea_commit_kernel(QeqeaArgs a) {
   }
 }
 
+constexpr int kCommitThreads = 256;
+
 // Single-rank fused commit + table (every touch of the generation went through
 // qeqea_values_kernel, which recorded the slot_max it started from and the
 // pending-mutation flag): only improving touches do random bank traffic.
-__global__ void __launch_bounds__(256) qeqea_commit_table_kernel(QeqeaArgs a) {
+__global__ void __launch_bounds__(kCommitThreads)
+    qeqea_commit_table_kernel(QeqeaArgs a, int64_t t0, int64_t t1) {
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
-  const int64_t total = a.P * a.L;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+  for (int64_t i = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t1;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double fit = a.fitness[i / a.L];
     const double fb = a.touch_fbefore[i];
@@ -406,7 +417,7 @@ static int blocks_for(int64_t n, int threads) {
 
 isq_status qeqea_launch_prepare(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
   const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, a.P);
-  qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a);
+  qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a, 0, a.P);
   if (c1 > c0)
     qeqea_values_kernel<<<blocks_for((c1 - c0) * a.L, kValThreads), kValThreads, 0, s>>>(a, c0 * a.L, c1 * a.L);
   ISQ_CUDA_TRY(cudaGetLastError());
@@ -426,11 +437,15 @@ isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStr
   return qeqea_launch_score(a, c0, c1, s);
 }
 
-isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
+static void launch_reduce(const QeqeaArgs& a, cudaStream_t s) {
   qeqea_reduce_partials<<<a.n_parts, kRedThreads, 0, s>>>(a);
   qeqea_reduce_final<<<1, kRedThreads, 0, s>>>(a);
+}
+
+isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
+  launch_reduce(a, s);
   if (a.fused_commit) {
-    qeqea_commit_table_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
+    qeqea_commit_table_kernel<<<blocks_for(a.P * a.L, kCommitThreads), kCommitThreads, 0, s>>>(a, 0, a.P * a.L);
   } else {
     qeqea_commit_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
     qeqea_table_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
