@@ -114,24 +114,42 @@ struct FastEval {
     }
   }
 
-  __device__ __forceinline__ void flush(int b, const double2* fac, int lane) {
-    switch (b) {
-      case 0: flush_bit<0>(fac, lane); break;
-      case 1: if constexpr (NQ > 1) flush_bit<1>(fac, lane); break;
-      case 2: if constexpr (NQ > 2) flush_bit<2>(fac, lane); break;
-      case 3: if constexpr (NQ > 3) flush_bit<3>(fac, lane); break;
-      case 4: if constexpr (NQ > 4) flush_bit<4>(fac, lane); break;
-      default: break;
+  // Flush of row bit B fused with the Rx lifting on it: per row pair
+  // (r, r1 = r | 2^B) the pending delta of r1 is multiplied in, then the pair
+  // is rotated, so the compiler can overlap one pair's flush with another's
+  // lifting.  Lane bits (n < 5) flush all rows of the upper lanes, then rotate.
+  template <int B>
+  __device__ __forceinline__ void flush_lift(const double2* fac, double p, double q, double C, int lane) {
+    if constexpr (B < G::EB) {
+      constexpr int m = 1 << B;
+      const int h = (lane >> NQ) & (G::LPC - 1);
+#pragma unroll
+      for (int r = 0; r < G::E; ++r) {
+        if (r & m) continue;
+        const int r1 = r | m;
+        const double2 f = fac[h * G::E + r1];
+        st.cmul(r1, f.x, f.y);
+        st.re[r] = fma(p, st.im[r1], st.re[r]);
+        st.im[r1] = fma(q, st.re[r], st.im[r1]);
+        st.re[r] = fma(p, st.im[r1], st.re[r]);
+        st.re[r1] = fma(p, st.im[r], st.re[r1]);
+        st.im[r] = fma(q, st.re[r1], st.im[r]);
+        st.re[r1] = fma(p, st.im[r], st.re[r1]);
+      }
+    } else {
+      flush_bit<B>(fac, lane);
+      st.template lift<B, 0>(p, q, C, lane);
     }
   }
 
-  __device__ __forceinline__ void rotate(int b, double p, double q, double C, int lane) {
+  __device__ __forceinline__ void flush_rotate(int b, const double2* fac, double p, double q, double C,
+                                               int lane) {
     switch (b) {
-      case 0: st.template lift<0, 0>(p, q, C, lane); break;
-      case 1: if constexpr (NQ > 1) st.template lift<1, 0>(p, q, C, lane); break;
-      case 2: if constexpr (NQ > 2) st.template lift<2, 0>(p, q, C, lane); break;
-      case 3: if constexpr (NQ > 3) st.template lift<3, 0>(p, q, C, lane); break;
-      case 4: if constexpr (NQ > 4) st.template lift<4, 0>(p, q, C, lane); break;
+      case 0: flush_lift<0>(fac, p, q, C, lane); break;
+      case 1: if constexpr (NQ > 1) flush_lift<1>(fac, p, q, C, lane); break;
+      case 2: if constexpr (NQ > 2) flush_lift<2>(fac, p, q, C, lane); break;
+      case 3: if constexpr (NQ > 3) flush_lift<3>(fac, p, q, C, lane); break;
+      case 4: if constexpr (NQ > 4) flush_lift<4>(fac, p, q, C, lane); break;
       default: break;
     }
   }
@@ -164,7 +182,6 @@ struct FastEval {
     unsigned rot = __ballot_sync(0xffffffffu, info != GT_DIAG);
     __syncwarp();
     const int row = lane;  // physical row whose phase this lane carries
-    const bool has_row = lane < G::D;
     int q = 0;
     for (;;) {
       const int qr = rot ? __ffs(rot) - 1 : nq;
@@ -181,27 +198,23 @@ struct FastEval {
         wr = wi;
         wi = -t;
       }
+      // flush factor of the rows with bit b set: w_r * conj(w_{r^m}) (1 elsewhere);
+      // those rows then carry the phase of their partner, so it commutes with Rx
       const double orr = __shfl_xor_sync(0xffffffffu, wr, m);
       const double ori = __shfl_xor_sync(0xffffffffu, wi, m);
-      const bool differs = has_row && (row & m) && (wr != orr || wi != ori);
-      if (__any_sync(0xffffffffu, differs)) {
-        // flush factor of the rows with bit b set: w_r * conj(w_{r^m})
-        double fr = 1.0, fi = 0.0;
-        if (differs) {
-          fr = fma(wr, orr, wi * ori);
-          fi = fma(wi, orr, -wr * ori);
-        }
-        sm.fac[lane] = make_double2(fr, fi);
-        __syncwarp();
-        flush(b, sm.fac, lane);
-        __syncwarp();
-        if (row & m) {
-          wr = orr;
-          wi = ori;
-        }
+      double fr = 1.0, fi = 0.0;
+      if (row & m) {
+        fr = fma(wr, orr, wi * ori);
+        fi = fma(wi, orr, -wr * ori);
+        wr = orr;
+        wi = ori;
       }
+      sm.fac[lane] = make_double2(fr, fi);
       const double2 pq = sm.cs2[qr][1];
-      rotate(b, pq.x, pq.y, sm.cs2[qr][0].x, lane);
+      const double C = sm.cs2[qr][0].x;
+      __syncwarp();
+      flush_rotate(b, sm.fac, pq.x, pq.y, C, lane);
+      __syncwarp();
       if (ry && (row & m)) {  // S: rows with the wire bit set pick up +i
         const double t = wr;
         wr = -wi;
