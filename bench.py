@@ -6,8 +6,10 @@ one step = one full QEQEA generation (sample + measure + lazy mutation +
 compose + score 2^20 circuits of 64 gates on 5 qubits, reductions, commit,
 table update) over a device-resident bank of 1.0e9 slots (36 GB, far above the
 126 MB L2), Haar-random target.  At N > 1 (torchrun) the 2^20 circuits are
-sharded over the ranks and the per-generation fitness vector is all-gathered
-over NCCL; every rank replays the O(P*L) commit.
+sharded over the ranks and the bank by slot position: per
+generation two NCCL all-to-alls (touches to their owners, gate codes / live
+angles back) and two all-gathers (fitness, shard elites); no O(P*L) pass is
+replicated.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -150,14 +152,6 @@ def run_reference(args):
     })
 
 
-class _CAI:
-    """__cuda_array_interface__ wrapper over a libisq-owned device buffer."""
-
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
-                                         "version": 3, "strides": None}
-
-
 def run_ours(args):
     import numpy as np
     import torch
@@ -183,25 +177,16 @@ def run_ours(args):
                            max_generations=10_000_000, target_fitness=1.0)
     eng = QeqeaEngine(cfg, TargetSpec("haar32", N, T), seed=2024, device=local, rank=rank, world=world,
                       max_batch=max(args.steps + args.warmup, 1) + 1)
+    from paper_1809_11134_b200.distributed import Comm, DeviceQeqeaOps
+
     stream = torch.cuda.Stream(device=local)
-    _lib.check(lib.isq_qeqea_set_stream(eng._h, ctypes.c_void_p(stream.cuda_stream)))
-    fptr, shard = ctypes.c_void_p(), ctypes.c_int64()
-    _lib.check(lib.isq_qeqea_buffers(eng._h, ctypes.byref(fptr), ctypes.byref(shard), None))
-    full = torch.as_tensor(_CAI(fptr.value, shard.value * world), device=f"cuda:{local}")
-    mine = full[rank * shard.value:(rank + 1) * shard.value]
-    send = torch.empty_like(mine)
-
-    def generation():
-        _lib.check(lib.isq_qeqea_eval(eng._h))
-        if world > 1:
-            send.copy_(mine)
-            dist.all_gather_into_tensor(full, send)
-        _lib.check(lib.isq_qeqea_finish(eng._h))
-
     with torch.cuda.stream(stream):
-        _lib.check(lib.isq_qeqea_begin_batch(eng._h))
+        ops = DeviceQeqeaOps(eng)  # binds the handle to `stream`
+        comm = Comm() if world > 1 else None
+        shard = ops.S
+        ops.begin_batch()
         for _ in range(args.warmup):
-            generation()
+            ops.generation(comm)
         stream.synchronize()
         ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(args.steps)]
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -212,16 +197,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         start.record(stream)
         for i in range(args.steps):
-            ev[i][0].record(stream)
-            _lib.check(lib.isq_qeqea_prepare(eng._h))
-            ev[i][1].record(stream)
-            _lib.check(lib.isq_qeqea_score(eng._h))
-            ev[i][2].record(stream)
-            if world > 1:
-                send.copy_(mine)
-                dist.all_gather_into_tensor(full, send)
-            _lib.check(lib.isq_qeqea_finish(eng._h))
-            ev[i][3].record(stream)
+            ops.generation(comm, marks=ev[i])
         end.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -235,14 +211,12 @@ def run_ours(args):
         t = torch.tensor([ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    rec = np.zeros(args.steps + args.warmup, dtype=_lib.GEN_RECORD)
-    nd = ctypes.c_int32()
-    _lib.check(lib.isq_qeqea_read_batch(eng._h, _lib.ptr(rec), ctypes.byref(nd), None, None, None))
-    assert nd.value == args.steps + args.warmup, nd.value
+    rec, _ = ops.read_batch()
+    assert rec.size == args.steps + args.warmup, rec.size
 
     evals_per_s = P * args.steps / (ms * 1e-3)
     avg_eval_s = sum(eval_ms) / len(eval_ms) * 1e-3
-    shard_circuits = min(shard.value, P - rank * shard.value)
+    shard_circuits = min(shard, P - rank * shard)
     achieved = canonical_flops(N, L) * shard_circuits / avg_eval_s / 1e12
     traffic = None
     tf = ROOT / "profiles" / "traffic_eval_c5.json"
@@ -256,58 +230,82 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": "C5: QEQEA generation, n=5 qubits, depth L=64, population 2^20, "
                                "Haar-random 32x32 target; bank 1.0e9 slots (36 GB) resident in HBM",
-                   "n": N, "L": L, "P": P, "global_batch": P, "parallelism": f"dp{world} (circuit shards)",
+                   "n": N, "L": L, "P": P, "global_batch": P, "parallelism": f"dp{world} (circuit shards x position-owned bank shards)",
                    "l2": "inputs larger than L2 (36 GB bank vs 126 MB)"},
         "gens_per_s": args.steps / (ms * 1e-3),
-        "phase_ms": {"prepare (sample + lazy mutation + measure)": sum(prep_ms) / len(prep_ms),
+        "phase_ms": {"prepare (sample + route + lazy mutation + measure; world > 1: + 2 all-to-alls)":
+                         sum(prep_ms) / len(prep_ms),
                      "score (fitness kernel)": sum(eval_ms) / len(eval_ms),
-                     "finish (reduce + commit + table)": sum(fin_ms) / len(fin_ms)},
+                     "finish (world > 1: all-gathers; reduce + commit + table)": sum(fin_ms) / len(fin_ms)},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "kernel": "fitness_fast_kernel<5> (score phase, one launch per generation)",
                      "peak_source": "FP64 CUDA-core FMA peak measured live by isq_fma_peak "
                                     "(MEASURED_PEAKS.json carries no FP64 figure)",
-                     "work": "canonical F(n,L) = (6L+8) 4^n flop/eval (SURVEY.md §8d) x circuits per launch"},
+                     "work": "canonical F(n,L) = (6L+8) 4^n flop/eval (SURVEY.md §8d) x circuits per launch",
+                     "note": ("frac > 1 is possible: diagonal gates (Rz, ZZ; 78% of QEQEA gates) cost O(2^n) "
+                              "phase updates here, not the canonical 6*4^n; the executed FP64 pipe "
+                              "utilisation (ncu sm__pipe_fp64_cycles_active) is in profiles/ and DESIGN.md §6")},
         "clocks": clk,
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": (7 if world == 1 else 10) * args.steps,
         "best_fitness": float(rec["best_fitness"][-1]),
     }
 
     # e2e: the same metric through the C-ABI with host buffers (isq_fitness_batch:
-    # pinned host codes/angles -> device, fitness -> host inside the timed region)
-    if rank == 0 and not args.skip_e2e:
-        flats, codes, thetas = eng.sample(0, P)
-        hc = torch.empty((P, L), dtype=torch.uint8, pin_memory=True).numpy()
-        ht = torch.empty((P, L), dtype=torch.float64, pin_memory=True).numpy()
-        hf = torch.empty(P, dtype=torch.float64, pin_memory=True).numpy()
+    # pinned host codes/angles -> device, fitness -> host inside the timed
+    # region), every rank on its shard of the circuits, max over ranks
+    if not args.skip_e2e:
+        n_mine = shard_circuits
+        if world == 1:
+            _, codes, thetas = eng.sample(0, P)  # this generation's C5 circuits
+            src = "this generation's C5 circuits"
+        else:
+            from oracle.cpu_baseline import qeqea_like_circuits
+
+            codes, thetas = qeqea_like_circuits(N, L, n_mine, seed=77 + rank)
+            src = "QEQEA-mix C5-shaped circuits, P/N per rank"
+        hc = torch.empty((n_mine, L), dtype=torch.uint8, pin_memory=True).numpy()
+        ht = torch.empty((n_mine, L), dtype=torch.float64, pin_memory=True).numpy()
+        hf = torch.empty(n_mine, dtype=torch.float64, pin_memory=True).numpy()
         hc[:] = codes
         ht[:] = thetas
         Tc = np.ascontiguousarray(T, dtype=np.complex128)
+
+        def batch():
+            _lib.check(lib.isq_fitness_batch(N, L, n_mine, _lib.ptr(hc), _lib.ptr(ht), _lib.ptr(Tc),
+                                             _lib.ptr(hf), None, local))
+
         for _ in range(max(1, args.warmup)):
-            _lib.check(lib.isq_fitness_batch(N, L, P, _lib.ptr(hc), _lib.ptr(ht), _lib.ptr(Tc), _lib.ptr(hf), None, local))
+            batch()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            _lib.check(lib.isq_fitness_batch(N, L, P, _lib.ptr(hc), _lib.ptr(ht), _lib.ptr(Tc), _lib.ptr(hf), None, local))
+            batch()
         dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
         out["e2e"] = {"value": P * args.steps / dt, "unit": "evals/s",
-                      "h2d_bytes_per_step": int(hc.nbytes + ht.nbytes + Tc.nbytes),
-                      "d2h_bytes_per_step": int(hf.nbytes),
-                      "path": "isq_fitness_batch (C ABI, pinned host buffers) on this generation's C5 circuits"}
-        # cross-check: fitness of the same circuits inside the engine generation
-        # (generation `warmup+steps` has not been evaluated yet, so compare the
-        # fitness_batch result against the oracle on a few circuits instead)
-        if not args.skip_cpu:
+                      "h2d_bytes_per_step": int(world * (hc.nbytes + ht.nbytes + Tc.nbytes)),
+                      "d2h_bytes_per_step": int(world * hf.nbytes),
+                      "path": f"isq_fitness_batch (C ABI, pinned host buffers) on {src}"}
+        # CPU baseline on the first circuits of rank 0's batch, which is also a
+        # parity spot-check of the GPU result
+        if rank == 0 and not args.skip_cpu:
             from oracle.cpu_baseline import CpuPool
 
             pool = CpuPool()
-            m = args.cpu_per_worker * pool.workers
+            m = min(n_mine, args.cpu_per_worker * pool.workers)
             cpu_fit, wall = pool.evaluate(N, codes[:m], thetas[:m], T)
             pool.close()
             rel = np.abs(cpu_fit - hf[:m]) / np.maximum(np.abs(cpu_fit), 1e-300)
             out["cpu_baseline"] = {
                 "value": m / wall, "unit": "evals/s", "cores": pool.workers, "kind": "port",
-                "sample": (f"first {m} circuits of the C5 generation, oracle restatement of evaluate_circuit "
-                           f"(dense kron matmul per gate), ProcessPool x{pool.workers}, OPENBLAS_NUM_THREADS=1"),
+                "sample": (f"first {m} circuits of the e2e batch ({src}), oracle restatement of "
+                           f"evaluate_circuit (dense kron matmul per gate), ProcessPool x{pool.workers}, "
+                           f"OPENBLAS_NUM_THREADS=1"),
                 "parity_max_rel_err_vs_gpu": float(rel.max()),
             }
     if rank == 0:

@@ -128,26 +128,66 @@ isq_status isq_qeqea_set_stream(void* handle, void* stream);
  * is 0 (running), 1 (target-reached) or 2 (generation-limit). */
 isq_status isq_qeqea_step(void* handle, int32_t n, isq_generation_record* records,
                           int32_t* n_done, int32_t* stop_reason);
-/* Split-phase generation for world > 1: begin_batch marks the record window,
- * eval scores this rank's circuit shard into the fitness buffer
- * (isq_qeqea_buffers: rank r owns [r*shard, (r+1)*shard)), the caller
- * all-gathers that buffer in place on the handle's stream, finish replays the
- * reductions, commit and table update identically on every rank. */
+/*
+ * Split-phase generation (population sharding over `world` ranks, one GPU
+ * each).  Rank r scores circuits [r*S, (r+1)*S) (S = shard,
+ * padded) and owns the bank slots of positions [b[r], b[r+1]) of every slot
+ * kind and individual (b = isq_qeqea_exchange_buffers.position_bounds); the
+ * touches of position p always go to its owner.  Per generation, on the
+ * handle's stream (isq_qeqea_buffers / exchange.stream):
+ *   isq_qeqea_prepare   sample this rank's circuits; world > 1: group their
+ *                       touches by owner into send_flats
+ *   [caller]            all-to-all send_flats -> recv_flats: S*(b[o+1]-b[o])
+ *                       uint32 to / from each rank o, in rank order
+ *   isq_qeqea_values    owned touches: live slot + measured gate code (world 1: no-op,
+ *                       prepare already did it)
+ *   [caller]            all-to-all send_codes -> recv_codes (uint8) and send_thetas
+ *                       -> recv_thetas (double): S*(b[r+1]-b[r]) to each rank,
+ *                       S*(b[o+1]-b[o]) from rank o
+ *   isq_qeqea_score     compose + score this rank's circuits into fitness[r*S ..];
+ *                       world > 1: also this shard's best circuit into elite[r]
+ *   [caller]            all-gather fitness (world*S doubles, S per rank) and
+ *                       elite (world*elite_len doubles) in place
+ *   isq_qeqea_finish    reductions, best-so-far (+ gates from the elite of the
+ *                       rank holding it), commit + table update of the owned
+ *                       touches, advance / stop
+ * World 1: isq_qeqea_eval == prepare + score and no collective is needed.
+ * begin_batch marks the start of a record window (read_batch).
+ */
 isq_status isq_qeqea_begin_batch(void* handle);
 isq_status isq_qeqea_eval(void* handle);
-isq_status isq_qeqea_finish(void* handle);
-/* eval == prepare (sample all circuits + gate values of the shard: K1/K2)
- * followed by score (compose + fitness of the shard: K3); exposed separately
- * so callers can time the fitness kernel alone. */
 isq_status isq_qeqea_prepare(void* handle);
+isq_status isq_qeqea_values(void* handle);
 isq_status isq_qeqea_score(void* handle);
+isq_status isq_qeqea_finish(void* handle);
+
+#define ISQ_MAX_WORLD 64
+typedef struct isq_qeqea_exchange_buffers {
+  int32_t world, rank;
+  int64_t shard;                               /* S                                   */
+  int32_t elite_len;                           /* doubles per rank in `elite`         */
+  int32_t position_bounds[ISQ_MAX_WORLD + 1];  /* rank o owns [b[o], b[o+1])          */
+  void* send_flats;   /* uint32 S*L, grouped by owner (world > 1, else NULL)          */
+  void* recv_flats;   /* uint32 world*S*Lr, rows = global circuits                    */
+  void* send_codes;   /* uint8  world*S*Lr  */
+  void* recv_codes;   /* uint8  S*L, grouped by owner */
+  void* send_thetas;  /* double world*S*Lr  */
+  void* recv_thetas;  /* double S*L, grouped by owner */
+  void* fitness;      /* double world*S (all-gather in place)                         */
+  void* elite;        /* double world*elite_len (all-gather in place)                 */
+  void* stream;       /* cudaStream_t of the handle                                    */
+} isq_qeqea_exchange_buffers;
+isq_status isq_qeqea_exchange(void* handle, isq_qeqea_exchange_buffers* out);
 isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
                                 int32_t* stop_reason, uint64_t* generation, double* best_fitness);
 isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream);
 /* engine.best_gates / best_fitness (gate codes + angles of length L). */
 isq_status isq_qeqea_best(void* handle, uint8_t* codes, double* thetas, double* fitness);
 /* Committed bank + table + counters (pickling, engine.py:301-304); set_state
- * also serves init from host arrays (init_population injection). */
+ * also serves init from host arrays (init_population injection).  Arrays
+ * cover this rank's owned slots in local order (kind, individual, owned
+ * position); world 1: the reference's flat order, theta[Q], qamp[3][Qt],
+ * slot_max[Q]. */
 isq_status isq_qeqea_get_state(void* handle, double* theta, double* qamp, double* slot_max,
                                uint64_t* generation, double* best_fitness, int32_t* stop);
 isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* qamp,
@@ -157,7 +197,8 @@ isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* 
  * the last generation applied); qutrits as Qt x 3 complex (numpy layout). */
 isq_status isq_qeqea_live_population(void* handle, double* theta, double* qutrits);
 /* Blueprints (flat slots), measured gate codes and live angles of circuits
- * [c0, c1) at the current generation (sample_circuit + construct_segments). */
+ * [c0, c1) at the current generation (sample_circuit + construct_segments).
+ * World 1 only. */
 isq_status isq_qeqea_sample(void* handle, int64_t c0, int64_t c1, int64_t* flats, uint8_t* codes,
                             double* thetas);
 /* Fitness vector of the last evaluated generation (P doubles). */

@@ -73,6 +73,30 @@ class GaConfigC(ctypes.Structure):
     ]
 
 
+MAX_WORLD = 64
+
+
+class QeqeaExchange(ctypes.Structure):
+    """isq_qeqea_exchange_buffers (include/isq.h)."""
+
+    _fields_ = [
+        ("world", c_i32),
+        ("rank", c_i32),
+        ("shard", c_i64),
+        ("elite_len", c_i32),
+        ("position_bounds", c_i32 * (MAX_WORLD + 1)),
+        ("send_flats", c_vp),
+        ("recv_flats", c_vp),
+        ("send_codes", c_vp),
+        ("recv_codes", c_vp),
+        ("send_thetas", c_vp),
+        ("recv_thetas", c_vp),
+        ("fitness", c_vp),
+        ("elite", c_vp),
+        ("stream", c_vp),
+    ]
+
+
 GEN_RECORD = np.dtype([("gen_best", "f8"), ("gen_mean", "f8"), ("best_fitness", "f8"), ("reserved", "f8")])
 
 c_i32p = ctypes.POINTER(c_i32)
@@ -86,6 +110,8 @@ SIGNATURES: dict[str, tuple] = {
     "isq_qeqea_eval": (c_i32, [c_vp]),
     "isq_qeqea_finish": (c_i32, [c_vp]),
     "isq_qeqea_prepare": (c_i32, [c_vp]),
+    "isq_qeqea_values": (c_i32, [c_vp]),
+    "isq_qeqea_exchange": (c_i32, [c_vp, c_vp]),
     "isq_qeqea_score": (c_i32, [c_vp]),
     "isq_qeqea_read_batch": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "isq_qeqea_buffers": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

@@ -23,23 +23,17 @@ static void free_handle(QeqeaHandle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   QeqeaArgs& a = h->a;
-  cudaFree(a.rot);
-  cudaFree(a.inter);
-  cudaFree(a.claim);
-  cudaFree(a.fitness);
-  cudaFree(a.flats);
-  cudaFree(a.gate_codes);
-  cudaFree(a.gate_thetas);
-  cudaFree(a.touch_fbefore);
-  cudaFree(a.touch_mutated);
-  cudaFree(a.st);
-  cudaFree(a.records);
-  cudaFree(a.best_codes);
-  cudaFree(a.best_thetas);
-  cudaFree((void*)a.target);
-  cudaFree(a.part_max);
-  cudaFree(a.part_sum);
-  cudaFree(a.part_arg);
+  const bool sharded = a.world > 1;
+  void* bufs[] = {a.rot, a.inter, a.claim, a.fitness, a.flats, a.gate_codes, a.gate_thetas,
+                  a.touch_fbefore, a.touch_mutated, a.st, a.records, a.best_codes, a.best_thetas,
+                  (void*)a.target, a.part_max, a.part_sum, a.part_arg, a.send_flats, a.recv_codes,
+                  a.recv_thetas, a.elite};
+  for (void* b : bufs) cudaFree(b);
+  if (sharded) {  // world 1: the owner-side arrays alias the circuit-side ones
+    cudaFree(a.owner_flats);
+    cudaFree(a.owner_codes);
+    cudaFree(a.owner_thetas);
+  }
   if (h->h_records) cudaFreeHost(h->h_records);
   if (h->h_state) cudaFreeHost(h->h_state);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -82,6 +76,9 @@ static isq_status validate(const isq_qeqea_config* c) {
     return ISQ_ERR_UNSUPPORTED;
   }
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad("invalid rank/world");
+  if (c->world > kMaxWorld) return bad("world exceeds " + std::to_string(kMaxWorld) + " ranks");
+  if (c->world > c->size_of_individual)
+    return bad("population sharding needs sizeOfIndividual >= world (each rank owns positions)");
   return ISQ_OK;
 }
 
@@ -127,20 +124,45 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   a.seed = cfg->seed;
   a.rec_cap = h->max_batch;
   h->shard = (a.P + h->world - 1) / h->world;
+  // sharding (engine_common.cuh QeqeaArgs): circuits [c0, c0 + S), positions [p_lo, p_lo + Lr)
+  a.world = h->world;
+  a.rank = h->rank;
+  a.S = h->shard;
+  a.c0 = (int64_t)h->rank * a.S;
+  for (int o = 0; o <= a.world; ++o) a.p_bounds[o] = (int)((int64_t)o * a.L / a.world);
+  a.p_lo = a.p_bounds[a.rank];
+  a.Lr = a.p_bounds[a.rank + 1] - a.p_lo;
+  a.Qloc = a.K * a.P * a.Lr;
+  a.Qtloc = (int64_t)a.n * a.P * a.Lr;
+  a.elite_len = 2 + a.L + (a.L + 7) / 8;
   const int64_t D = 1LL << a.n;
+  const int64_t nc = a.S * a.L;                  // circuit-side touches
+  const int64_t no = (int64_t)a.world * a.S * a.Lr;  // owner-side touches
   TRYA(cudaSetDevice(device));
   TRYA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
-  TRYA(cudaMalloc((void**)&a.rot, a.Qt * sizeof(RotRec)));
-  TRYA(cudaMalloc((void**)&a.inter, (a.Q - a.Qt) * sizeof(IntRec)));
-  TRYA(cudaMalloc((void**)&a.claim, a.Q * 4));
-  TRYA(cudaMalloc((void**)&a.fitness, h->shard * h->world * 8));
-  TRYA(cudaMalloc((void**)&a.flats, a.P * a.L * 4));
-  TRYA(cudaMalloc((void**)&a.gate_codes, h->shard * a.L));
-  TRYA(cudaMalloc((void**)&a.gate_thetas, h->shard * a.L * 8));
-  TRYA(cudaMalloc((void**)&a.touch_fbefore, h->shard * a.L * 8));
-  TRYA(cudaMalloc((void**)&a.touch_mutated, h->shard * a.L));
-  a.fused_commit = h->world == 1 ? 1 : 0;
+  TRYA(cudaMalloc((void**)&a.rot, a.Qtloc * sizeof(RotRec)));
+  TRYA(cudaMalloc((void**)&a.inter, (a.Qloc - a.Qtloc) * sizeof(IntRec)));
+  TRYA(cudaMalloc((void**)&a.claim, a.Qloc * 4));
+  TRYA(cudaMalloc((void**)&a.fitness, a.S * a.world * 8));
+  TRYA(cudaMalloc((void**)&a.flats, nc * 4));
+  TRYA(cudaMalloc((void**)&a.gate_codes, nc));
+  TRYA(cudaMalloc((void**)&a.gate_thetas, nc * 8));
+  TRYA(cudaMalloc((void**)&a.touch_fbefore, no * 8));
+  TRYA(cudaMalloc((void**)&a.touch_mutated, no));
+  if (a.world > 1) {
+    TRYA(cudaMalloc((void**)&a.owner_flats, no * 4));
+    TRYA(cudaMalloc((void**)&a.owner_codes, no));
+    TRYA(cudaMalloc((void**)&a.owner_thetas, no * 8));
+    TRYA(cudaMalloc((void**)&a.send_flats, nc * 4));
+    TRYA(cudaMalloc((void**)&a.recv_codes, nc));
+    TRYA(cudaMalloc((void**)&a.recv_thetas, nc * 8));
+    TRYA(cudaMalloc((void**)&a.elite, (int64_t)a.world * a.elite_len * 8));
+  } else {
+    a.owner_flats = a.flats;
+    a.owner_codes = a.gate_codes;
+    a.owner_thetas = a.gate_thetas;
+  }
   TRYA(cudaMalloc((void**)&a.st, sizeof(QeqeaDevState)));
   TRYA(cudaMalloc((void**)&a.records, sizeof(GenRecord) * h->max_batch));
   TRYA(cudaMalloc((void**)&a.best_codes, a.L));
@@ -196,39 +218,63 @@ isq_status isq_qeqea_begin_batch(void* handle) {
   return ISQ_OK;
 }
 
-isq_status isq_qeqea_eval(void* handle) {
-  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
-  ISQ_CUDA_TRY(cudaSetDevice(h->device));
-  const int64_t c0 = h->rank * h->shard;
-  const int64_t c1 = c0 + h->shard < h->a.P ? c0 + h->shard : h->a.P;
-  return qeqea_launch_eval(h->a, c0, c1, h->stream);
+static isq_status need_world1(const QeqeaHandle* h, const char* what) {
+  if (h->world == 1) return ISQ_OK;
+  set_error(std::string(what) + " drives a single rank; at world > 1 use prepare / values / score / finish");
+  return ISQ_ERR_CONFIG;
 }
 
-static void shard_range(const QeqeaHandle* h, int64_t* c0, int64_t* c1) {
-  *c0 = h->rank * h->shard;
-  *c1 = *c0 + h->shard < h->a.P ? *c0 + h->shard : h->a.P;
+isq_status isq_qeqea_eval(void* handle) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  isq_status st = need_world1(h, "isq_qeqea_eval");
+  if (st != ISQ_OK) return st;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  return qeqea_launch_eval(h->a, h->stream);
 }
 
 isq_status isq_qeqea_prepare(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
-  int64_t c0, c1;
-  shard_range(h, &c0, &c1);
-  return qeqea_launch_prepare(h->a, c0, c1, h->stream);
+  return qeqea_launch_prepare(h->a, h->stream);
+}
+
+isq_status isq_qeqea_values(void* handle) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  return qeqea_launch_values(h->a, h->stream);
 }
 
 isq_status isq_qeqea_score(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
-  int64_t c0, c1;
-  shard_range(h, &c0, &c1);
-  return qeqea_launch_score(h->a, c0, c1, h->stream);
+  return qeqea_launch_score(h->a, h->stream);
 }
 
 isq_status isq_qeqea_finish(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   return qeqea_launch_finish(h->a, h->stream);
+}
+
+isq_status isq_qeqea_exchange(void* handle, isq_qeqea_exchange_buffers* x) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  const QeqeaArgs& a = h->a;
+  std::memset(x, 0, sizeof(*x));
+  x->world = a.world;
+  x->rank = a.rank;
+  x->shard = a.S;
+  x->elite_len = a.elite_len;
+  for (int o = 0; o <= a.world; ++o) x->position_bounds[o] = a.p_bounds[o];
+  x->send_flats = a.send_flats;
+  x->recv_flats = a.world > 1 ? a.owner_flats : nullptr;
+  x->send_codes = a.world > 1 ? a.owner_codes : nullptr;
+  x->recv_codes = a.recv_codes;
+  x->send_thetas = a.world > 1 ? a.owner_thetas : nullptr;
+  x->recv_thetas = a.recv_thetas;
+  x->fitness = a.fitness;
+  x->elite = a.elite;
+  x->stream = h->stream;
+  return ISQ_OK;
 }
 
 isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
@@ -256,10 +302,8 @@ isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, in
 isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_record* records,
                           int32_t* n_done, int32_t* stop_reason) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
-  if (h->world != 1) {
-    set_error("isq_qeqea_step drives a single rank; use eval / all-gather / finish for world > 1");
-    return ISQ_ERR_CONFIG;
-  }
+  isq_status st0 = need_world1(h, "isq_qeqea_step");
+  if (st0 != ISQ_OK) return st0;
   if (n_generations > h->max_batch) {
     set_error("n_generations exceeds the handle's record capacity (max_batch)");
     return ISQ_ERR_CONFIG;
@@ -267,7 +311,7 @@ isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_re
   isq_status st = isq_qeqea_begin_batch(handle);
   if (st != ISQ_OK) return st;
   for (int i = 0; i < n_generations; ++i) {
-    st = qeqea_launch_eval(h->a, 0, h->a.P, h->stream);
+    st = qeqea_launch_eval(h->a, h->stream);
     if (st != ISQ_OK) return st;
     st = qeqea_launch_finish(h->a, h->stream);
     if (st != ISQ_OK) return st;
@@ -305,9 +349,9 @@ struct SoaTemps {
     cudaFree(smax);
   }
   cudaError_t alloc(const QeqeaArgs& a) {
-    cudaError_t e = cudaMalloc((void**)&theta, a.Q * 8);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&qamp, a.Qt * 48 + 16);
-    if (e == cudaSuccess) e = cudaMalloc((void**)&smax, a.Q * 8);
+    cudaError_t e = cudaMalloc((void**)&theta, a.Qloc * 8);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&qamp, a.Qtloc * 48 + 16);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&smax, a.Qloc * 8);
     return e;
   }
 };
@@ -324,9 +368,9 @@ isq_status isq_qeqea_get_state(void* handle, double* theta, double* qamp, double
     isq_status st = qeqea_launch_pack(a, t.theta, t.qamp, t.smax, h->stream);
     if (st != ISQ_OK) return st;
     ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    if (theta) ISQ_CUDA_TRY(cudaMemcpy(theta, t.theta, a.Q * 8, cudaMemcpyDeviceToHost));
-    if (qamp) ISQ_CUDA_TRY(cudaMemcpy(qamp, t.qamp, a.Qt * 48, cudaMemcpyDeviceToHost));
-    if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(slot_max, t.smax, a.Q * 8, cudaMemcpyDeviceToHost));
+    if (theta) ISQ_CUDA_TRY(cudaMemcpy(theta, t.theta, a.Qloc * 8, cudaMemcpyDeviceToHost));
+    if (qamp) ISQ_CUDA_TRY(cudaMemcpy(qamp, t.qamp, a.Qtloc * 48, cudaMemcpyDeviceToHost));
+    if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(slot_max, t.smax, a.Qloc * 8, cudaMemcpyDeviceToHost));
   }
   QeqeaDevState s;
   ISQ_CUDA_TRY(cudaMemcpy(&s, a.st, sizeof(s), cudaMemcpyDeviceToHost));
@@ -346,9 +390,9 @@ isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* 
   if (theta && qamp) {
     SoaTemps t;
     ISQ_CUDA_TRY(t.alloc(a));
-    ISQ_CUDA_TRY(cudaMemcpy(t.theta, theta, a.Q * 8, cudaMemcpyHostToDevice));
-    ISQ_CUDA_TRY(cudaMemcpy(t.qamp, qamp, a.Qt * 48, cudaMemcpyHostToDevice));
-    if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(t.smax, slot_max, a.Q * 8, cudaMemcpyHostToDevice));
+    ISQ_CUDA_TRY(cudaMemcpy(t.theta, theta, a.Qloc * 8, cudaMemcpyHostToDevice));
+    ISQ_CUDA_TRY(cudaMemcpy(t.qamp, qamp, a.Qtloc * 48, cudaMemcpyHostToDevice));
+    if (slot_max) ISQ_CUDA_TRY(cudaMemcpy(t.smax, slot_max, a.Qloc * 8, cudaMemcpyHostToDevice));
     isq_status st = qeqea_launch_unpack(a, t.theta, t.qamp, slot_max ? t.smax : nullptr, h->stream);
     if (st != ISQ_OK) return st;
     ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -375,8 +419,8 @@ isq_status isq_qeqea_live_population(void* handle, double* theta, double* qutrit
   const QeqeaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   double *d_t = nullptr, *d_q = nullptr;
-  ISQ_CUDA_TRY(cudaMalloc((void**)&d_t, a.Q * 8));
-  cudaError_t e = cudaMalloc((void**)&d_q, a.Qt * 48 + 16);
+  ISQ_CUDA_TRY(cudaMalloc((void**)&d_t, a.Qloc * 8));
+  cudaError_t e = cudaMalloc((void**)&d_q, a.Qtloc * 48 + 16);
   if (e != cudaSuccess) {
     cudaFree(d_t);
     set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
@@ -385,8 +429,8 @@ isq_status isq_qeqea_live_population(void* handle, double* theta, double* qutrit
   isq_status st = qeqea_launch_live(a, d_t, d_q, h->stream);
   if (st == ISQ_OK) {
     e = cudaStreamSynchronize(h->stream);
-    if (e == cudaSuccess) e = cudaMemcpy(theta, d_t, a.Q * 8, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess && qutrits) e = cudaMemcpy(qutrits, d_q, a.Qt * 48, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(theta, d_t, a.Qloc * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && qutrits) e = cudaMemcpy(qutrits, d_q, a.Qtloc * 48, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) {
       set_error(std::string("live population: ") + cudaGetErrorString(e));
       st = ISQ_ERR_CUDA;
@@ -401,6 +445,8 @@ isq_status isq_qeqea_sample(void* handle, int64_t c0, int64_t c1, int64_t* flats
                             double* thetas) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
   const QeqeaArgs& a = h->a;
+  isq_status st0 = need_world1(h, "isq_qeqea_sample");
+  if (st0 != ISQ_OK) return st0;
   if (c0 < 0 || c1 > a.P || c1 < c0) {
     set_error("circuit range out of bounds");
     return ISQ_ERR_CONFIG;

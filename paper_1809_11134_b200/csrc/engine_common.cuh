@@ -56,6 +56,15 @@ struct alignas(16) IntRec {
   double smax;
 };
 
+constexpr int kMaxWorld = 64;
+constexpr uint32_t kNoSlot = 0xffffffffu;  // padding touch of a padding circuit
+
+// Device view of one engine handle.  Multi-GPU layout (population sharding,
+// DESIGN.md §8): rank r scores circuits [c0, c0 + S) and owns the bank slots
+// of positions [p_lo, p_lo + Lr) (every slot kind and individual); a slot's
+// position is fixed by Eq. 9, so the touches of position p always go to the
+// same owner.  World 1: c0 = 0, S = P, p_lo = 0, Lr = L, and the owner-side
+// touch arrays alias the circuit-side ones.
 struct QeqeaArgs {
   // configuration (engine.py:33-43)
   int n, L;
@@ -64,18 +73,34 @@ struct QeqeaArgs {
   int n_meas;
   uint64_t max_generations;
   uint64_t seed;
-  // bank
-  RotRec* rot;     // Qt records
-  IntRec* inter;   // Q - Qt records
-  uint32_t* claim;
-  // per generation
-  double* fitness;   // P (padded to world * shard)
-  uint32_t* flats;   // P * L scratch between commit and table kernels
-  uint8_t* gate_codes;   // shard * L gate codes of the generation (params -> fitness)
-  double* gate_thetas;   // shard * L live angles
-  double* touch_fbefore;  // shard * L slot_max each touch started the generation from
-  uint8_t* touch_mutated; // shard * L: bit 0 pending mutation, bit 1 it is a qutrit mutation
-  int fused_commit;       // 1: single rank, commit+table fused over the touch records
+  // sharding
+  int world, rank;
+  int64_t S;       // circuits per rank (padded: world * S >= P)
+  int64_t c0;      // first circuit of this rank
+  int p_lo, Lr;    // owned positions
+  int p_bounds[kMaxWorld + 1];  // owner o holds positions [p_bounds[o], p_bounds[o + 1])
+  int64_t Qloc, Qtloc;  // owned slots / owned rotation-region slots
+  // bank (owned slots, local index, see slot_local)
+  RotRec* rot;     // Qtloc records
+  IntRec* inter;   // Qloc - Qtloc records
+  uint32_t* claim; // Qloc
+  // circuit side (this rank's S circuits x L positions)
+  double* fitness;       // world * S: the whole (gathered) fitness vector
+  uint32_t* flats;       // S * L sampled slots
+  uint8_t* gate_codes;   // S * L gate codes (fitness input)
+  double* gate_thetas;   // S * L live angles
+  // owner side (world * S circuits x Lr owned positions, row = global circuit)
+  uint32_t* owner_flats;    // touches of the owned slots
+  uint8_t* owner_codes;     // their gate codes / live angles (sent back to the circuit ranks)
+  double* owner_thetas;
+  double* touch_fbefore;    // slot_max each touch started the generation from
+  uint8_t* touch_mutated;   // bit 0 pending mutation, bit 1 it is a qutrit mutation
+  // world > 1 exchange buffers (send side of flats, receive side of codes / angles)
+  uint32_t* send_flats;     // S * L, grouped by owner
+  uint8_t* recv_codes;      // S * L, grouped by owner
+  double* recv_thetas;
+  double* elite;            // world * elite_len: per-rank shard best (fitness, circuit, L angles, L codes)
+  int elite_len;
   QeqeaDevState* st;
   GenRecord* records;
   uint8_t* best_codes;   // L
@@ -88,6 +113,16 @@ struct QeqeaArgs {
   int n_parts;
   int rec_cap;  // capacity of `records`
 };
+
+// Eq. 9 flat index s = (kind P + i) L + p  <->  owned local index (kind P + i) Lr + (p - p_lo).
+__host__ __device__ __forceinline__ int64_t slot_local(const QeqeaArgs& a, int64_t s) {
+  const int64_t ki = s / a.L;
+  return ki * a.Lr + (s - ki * a.L - a.p_lo);
+}
+__host__ __device__ __forceinline__ int64_t slot_global(const QeqeaArgs& a, int64_t loc) {
+  const int64_t ki = loc / a.Lr;
+  return ki * a.L + a.p_lo + (loc - ki * a.Lr);
+}
 
 constexpr double kTwoPiD = 6.283185307179586;   // encoding.py:13 TWO_PI = 2.0 * math.pi
 constexpr double kHalfPiD = 1.5707963267948966;  // math.pi / 2
@@ -108,14 +143,14 @@ struct LiveSlot {
   double2 q[3];
 };
 
-__device__ __forceinline__ double* smax_ptr(const QeqeaArgs& a, int64_t s) {
-  return s < a.Qt ? &a.rot[s].smax : &a.inter[s - a.Qt].smax;
+__device__ __forceinline__ double* smax_ptr(const QeqeaArgs& a, int64_t loc) {
+  return loc < a.Qtloc ? &a.rot[loc].smax : &a.inter[loc - a.Qtloc].smax;
 }
 
-// Committed value of slot s (one 64 B or 16 B record load); returns slot_max.
-__device__ __forceinline__ double load_committed(const QeqeaArgs& a, int64_t s, LiveSlot& v) {
-  if (s < a.Qt) {
-    const double2* r = reinterpret_cast<const double2*>(a.rot + s);
+// Committed value of the owned slot `loc` (one 64 B or 16 B record load); returns slot_max.
+__device__ __forceinline__ double load_committed(const QeqeaArgs& a, int64_t loc, LiveSlot& v) {
+  if (loc < a.Qtloc) {
+    const double2* r = reinterpret_cast<const double2*>(a.rot + loc);
     v.q[0] = r[0];
     v.q[1] = r[1];
     v.q[2] = r[2];
@@ -123,20 +158,20 @@ __device__ __forceinline__ double load_committed(const QeqeaArgs& a, int64_t s, 
     v.theta = ts.x;
     return ts.y;
   }
-  const double2 ts = *reinterpret_cast<const double2*>(a.inter + (s - a.Qt));
+  const double2 ts = *reinterpret_cast<const double2*>(a.inter + (loc - a.Qtloc));
   v.theta = ts.x;
   return ts.y;
 }
 
-__device__ __forceinline__ void store_committed(const QeqeaArgs& a, int64_t s, const LiveSlot& v) {
-  if (s < a.Qt) {
-    double2* r = reinterpret_cast<double2*>(a.rot + s);
+__device__ __forceinline__ void store_committed(const QeqeaArgs& a, int64_t loc, const LiveSlot& v) {
+  if (loc < a.Qtloc) {
+    double2* r = reinterpret_cast<double2*>(a.rot + loc);
     r[0] = v.q[0];
     r[1] = v.q[1];
     r[2] = v.q[2];
-    a.rot[s].theta = v.theta;
+    a.rot[loc].theta = v.theta;
   } else {
-    a.inter[s - a.Qt].theta = v.theta;
+    a.inter[loc - a.Qtloc].theta = v.theta;
   }
 }
 
@@ -201,11 +236,11 @@ __device__ __forceinline__ bool mutate_slot(const QeqeaArgs& a, int64_t s, uint6
   return true;
 }
 
-// Live value of slot s during generation g (committed value plus the pending
-// mutation drawn at the end of generation g-1).
+// Live value of the (owned) slot s during generation g (committed value plus
+// the pending mutation drawn at the end of generation g-1).
 __device__ __forceinline__ void live_slot(const QeqeaArgs& a, int64_t s, uint64_t g, LiveSlot& v,
                                           bool* mutated = nullptr) {
-  const double f = load_committed(a, s, v);
+  const double f = load_committed(a, slot_local(a, s), v);
   bool m = false;
   if (g > 0) m = mutate_slot(a, s, g - 1, f, v);
   if (mutated) *mutated = m;

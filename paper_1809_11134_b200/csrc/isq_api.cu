@@ -48,7 +48,7 @@ extern "C" {
 
 const char* isq_last_error(void) { return g_last_error.c_str(); }
 
-int32_t isq_abi_version(void) { return 1; }
+int32_t isq_abi_version(void) { return 2; }
 
 void isq_philox_block(uint64_t seed, uint64_t domain, uint64_t gen, uint64_t index, uint64_t sub,
                       uint64_t block, uint64_t* out) {

@@ -1,12 +1,16 @@
 // QEQEA generation loop kernels (QeqeaEngine.step, engine.py:318-361).
 //
 // One generation g is the launch sequence
-//   eval     circuits [c0, c1): sample + live slots + measure + compose + score  (K1-K3)
-//   (multi-GPU: all-gather of the fitness vector)
-//   reduce   gen max / first argmax / mean, best-so-far, record               (K4)
-//   capture  gates of the new best circuit (engine.py:341-343)
-//   commit   improved & mutated touched slots -> committed bank              (K5, lazy revert)
-//   table    slot_max scatter-max (SegmentFitnessTable.update)               (K4)
+//   sample   this rank's circuits: blueprints (flat slots)                     (K2)
+//   route    world > 1: touches grouped by the rank owning their position
+//            (caller: all-to-all of the flats)
+//   values   owned touches: live slot (lazy mutation) + measured gate code    (K1, K5)
+//            (caller, world > 1: all-to-all of codes / angles back)
+//   unroute  world > 1: codes / angles back into circuit order
+//   fitness  compose + score this rank's circuits                             (K3)
+//   elite    world > 1: shard best + its gates (caller: all-gather of fitness + elites)
+//   reduce   gen max / first argmax / mean, best-so-far, record, best gates   (K4)
+//   commit   owned touches: improved & mutated -> committed bank, slot_max    (K4, K5)
 //   advance  generation += 1, stop reason (engine.py:354-358)
 // Every kernel reads the generation from device state and returns
 // immediately once a stop reason is set, so batches of generations are
@@ -24,25 +28,60 @@ namespace isq {
 // keep each one's hot code inside the instruction cache and give the random
 // bank gathers thread-level memory parallelism.
 
-__global__ void __launch_bounds__(kThreadsPerBlock)
-    qeqea_sample_flats_kernel(QeqeaArgs a, int64_t c0, int64_t c1) {
+__global__ void __launch_bounds__(kThreadsPerBlock) qeqea_sample_flats_kernel(QeqeaArgs a) {
   __shared__ uint64_t blk[kWarpsPerBlock][36];
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
-  for (int64_t c = c0 + (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < c1; c += nwarps)
-    sample_circuit_warp(a, g, c, a.flats + c * a.L, blk[wib], lane);
+  const int64_t c1 = min(a.P, a.c0 + a.S);
+  for (int64_t c = a.c0 + (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < c1; c += nwarps)
+    sample_circuit_warp(a, g, c, a.flats + (c - a.c0) * a.L, blk[wib], lane);
 }
 
-// One thread per touch of the shard: committed record -> live value (pending
-// mutation of g-1).  Rotation touches (1/3 at C5) additionally need the Born
-// measurement; those are compacted into a shared-memory queue so the costly
-// measurement runs on full warps instead of on the 1/3 of lanes that need it.
-// Also records, per touch, the slot_max the generation started from and
-// whether the slot carries a pending mutation (the fused single-rank commit
-// consumes both).
+// Position p -> owning rank, and the offset of (circuit c_loc, position p) in
+// the owner-grouped exchange layout: block o holds S x Lr(o) entries, row =
+// circuit, starting at S * p_bounds[o].
+__device__ __forceinline__ int64_t routed_index(const QeqeaArgs& a, int64_t c_loc, int p) {
+  int o = 0;
+  while (p >= a.p_bounds[o + 1]) ++o;
+  const int lo = a.p_bounds[o], lr = a.p_bounds[o + 1] - lo;
+  return a.S * lo + c_loc * lr + (p - lo);
+}
+
+// world > 1: this rank's touches grouped by owner (padding circuits send kNoSlot).
+__global__ void qeqea_route_kernel(QeqeaArgs a) {
+  if (a.st->stop) return;
+  const int64_t n = a.S * a.L;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c_loc = i / a.L;
+    const int p = (int)(i - c_loc * a.L);
+    a.send_flats[routed_index(a, c_loc, p)] = a.c0 + c_loc < a.P ? a.flats[i] : kNoSlot;
+  }
+}
+
+// world > 1: the owners' gate codes / live angles back into circuit order.
+__global__ void qeqea_unroute_kernel(QeqeaArgs a) {
+  if (a.st->stop) return;
+  const int64_t n = a.S * a.L;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c_loc = i / a.L;
+    const int64_t src = routed_index(a, c_loc, (int)(i - c_loc * a.L));
+    a.gate_codes[i] = a.recv_codes[src];
+    a.gate_thetas[i] = a.recv_thetas[src];
+  }
+}
+
+// One thread per owned touch t (row = global circuit, column = owned
+// position): committed record -> live value (pending mutation of g-1).
+// Rotation touches (1/3 at C5) additionally need the Born measurement; those
+// are compacted into a shared-memory queue so the costly measurement runs on
+// full warps instead of on the 1/3 of lanes that need it.  Also records, per
+// touch, the slot_max the generation started from and whether the slot
+// carries a pending mutation (the commit consumes both).
 constexpr int kValThreads = 256;
 constexpr int kValPerThread = 3;  // touches per thread per tile: ~1 measurement task per thread
 
@@ -52,28 +91,34 @@ struct MeasureTask {  // 56 B: 768 tasks fit the 48 KB static shared limit
   uint32_t out;
 };
 
-__global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t0, int64_t t1) {
+__global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t1) {
   __shared__ MeasureTask tasks[kValThreads * kValPerThread];
   __shared__ int ntask;
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   constexpr int kTile = kValThreads * kValPerThread;
-  for (int64_t base = t0 + (int64_t)blockIdx.x * kTile; base < t1; base += (int64_t)gridDim.x * kTile) {
+  for (int64_t base = (int64_t)blockIdx.x * kTile; base < t1; base += (int64_t)gridDim.x * kTile) {
     if (threadIdx.x == 0) ntask = 0;
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kValPerThread; ++u) {
-      const int64_t i = base + u * kValThreads + threadIdx.x;
-      if (i >= t1) break;
-      const uint32_t s = a.flats[i];
+      const int64_t t = base + u * kValThreads + threadIdx.x;
+      if (t >= t1) break;
+      const uint32_t s = a.owner_flats[t];
+      if (s == kNoSlot) {  // padding circuit: never commits (fitness <= 1 < 2)
+        a.owner_codes[t] = 0;
+        a.owner_thetas[t] = 0.0;
+        a.touch_fbefore[t] = 2.0;
+        a.touch_mutated[t] = 0;
+        continue;
+      }
       LiveSlot v;
-      const double f = load_committed(a, s, v);
+      const double f = load_committed(a, slot_local(a, s), v);
       bool qpath = false;
       const bool mutated = g > 0 && mutate_slot(a, s, g - 1, f, v, &qpath);
-      const int64_t o = i - t0;
-      a.gate_thetas[o] = v.theta;
-      a.touch_fbefore[o] = f;
-      a.touch_mutated[o] = (uint8_t)((mutated ? 1 : 0) | (mutated && qpath ? 2 : 0));
+      a.owner_thetas[t] = v.theta;
+      a.touch_fbefore[t] = f;
+      a.touch_mutated[t] = (uint8_t)((mutated ? 1 : 0) | (mutated && qpath ? 2 : 0));
       const int64_t kind = (int64_t)s / (a.L * a.P);
       if (kind < a.n) {
         const int k = atomicAdd(&ntask, 1);
@@ -83,24 +128,68 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
           tasks[k].im[c] = v.q[c].y;
         }
         tasks[k].s = s;
-        tasks[k].out = (uint32_t)o;
+        tasks[k].out = (uint32_t)(t - base);
       } else {
-        a.gate_codes[o] = (uint8_t)(3 * a.n + (kind - a.n));
+        a.owner_codes[t] = (uint8_t)(3 * a.n + (kind - a.n));
       }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < ntask; k += kValThreads) {
-      const MeasureTask& t = tasks[k];
+      const MeasureTask& mt = tasks[k];
       NpStream st;
-      st.init(a.seed, DOM_MEASURE, g, (uint64_t)t.s, 0);
-      double re[3] = {t.re[0], t.re[1], t.re[2]};
-      double im[3] = {t.im[0], t.im[1], t.im[2]};
+      st.init(a.seed, DOM_MEASURE, g, (uint64_t)mt.s, 0);
+      double re[3] = {mt.re[0], mt.re[1], mt.re[2]};
+      double im[3] = {mt.im[0], mt.im[1], mt.im[2]};
       bool ok = true;
       const int axis = measure_axis(re, im, a.n_meas, st, &ok);
-      const int64_t kind = (int64_t)t.s / (a.L * a.P);
-      a.gate_codes[t.out] = (uint8_t)(3 * kind + axis);
+      const int64_t kind = (int64_t)mt.s / (a.L * a.P);
+      a.owner_codes[base + mt.out] = (uint8_t)(3 * kind + axis);
     }
     __syncthreads();
+  }
+}
+
+// world > 1: best circuit of this rank's shard (first index on ties) and its
+// gates, packed for the all-gather as [fitness, circuit, L angles, L code bytes].
+__global__ void __launch_bounds__(256) qeqea_elite_kernel(QeqeaArgs a) {
+  __shared__ double smax[256];
+  __shared__ int64_t sarg[256];
+  if (a.st->stop) return;
+  const int64_t c1 = min(a.P, a.c0 + a.S);
+  double m = -1.0;
+  int64_t arg = INT64_MAX;
+  for (int64_t c = a.c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const double f = a.fitness[c];
+    if (f > m) {
+      m = f;
+      arg = c;
+    }
+  }
+  smax[threadIdx.x] = m;
+  sarg[threadIdx.x] = arg;
+  __syncthreads();
+  for (int off = 128; off >= 1; off >>= 1) {
+    if (threadIdx.x < off) {
+      const double m2 = smax[threadIdx.x + off];
+      const int64_t a2 = sarg[threadIdx.x + off];
+      if (m2 > smax[threadIdx.x] || (m2 == smax[threadIdx.x] && a2 < sarg[threadIdx.x])) {
+        smax[threadIdx.x] = m2;
+        sarg[threadIdx.x] = a2;
+      }
+    }
+    __syncthreads();
+  }
+  double* e = a.elite + (int64_t)a.rank * a.elite_len;
+  const int64_t best = sarg[0];
+  if (threadIdx.x == 0) {
+    e[0] = smax[0];
+    e[1] = (double)(best == INT64_MAX ? -1 : best);
+  }
+  if (best == INT64_MAX) return;
+  uint8_t* codes = reinterpret_cast<uint8_t*>(e + 2 + a.L);
+  for (int p = threadIdx.x; p < a.L; p += blockDim.x) {
+    e[2 + p] = a.gate_thetas[(best - a.c0) * a.L + p];
+    codes[p] = a.gate_codes[(best - a.c0) * a.L + p];
   }
 }
 
@@ -192,96 +281,59 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
   const int lane = threadIdx.x;
   const uint64_t g = st->generation;
   for (int p = lane; p < a.L; p += 32) {
-    if (a.fused_commit) {
-      // single rank: the generation's gate codes / live angles of every
-      // circuit are still in place (and the commit may already be rewriting
-      // the bank, so do not recompute them from it)
+    if (a.world == 1) {
+      // the generation's gate codes / live angles of every circuit are still
+      // in place (do not recompute them from the bank: the commit rewrites it)
       a.best_codes[p] = a.gate_codes[s_best * a.L + p];
       a.best_thetas[p] = a.gate_thetas[s_best * a.L + p];
     } else {
-      const int64_t s = a.flats[s_best * a.L + p];
-      LiveSlot v;
-      live_slot(a, s, g, v);
-      a.best_codes[p] = (uint8_t)slot_gate_code(a, s, g, v);
-      a.best_thetas[p] = v.theta;
+      // gathered elite record of the rank that scored the best circuit
+      const double* e = a.elite + (s_best / a.S) * a.elite_len;
+      a.best_codes[p] = reinterpret_cast<const uint8_t*>(e + 2 + a.L)[p];
+      a.best_thetas[p] = e[2 + p];
     }
   }
 }
 
 // -------------------------------------------------------------- commit ---
 
-// Elitist accept (engine.py:345-351 + 211-222): a slot mutated at g-1 keeps
-// its mutation iff some circuit of generation g that touched it beat its
-// slot_max.  Only touched slots can be improved, so walk the touches (thread
-// per touch); one improving touch per slot wins the claim stamp and writes
-// the live value into the committed bank.
-__global__ void __launch_bounds__(256) qeqea_commit_kernel(QeqeaArgs a) {
-  if (a.st->stop) return;
-  const uint64_t g = a.st->generation;
-  if (g == 0) return;
-  const int64_t total = a.P * a.L;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = a.flats[i];
-    const double fit = a.fitness[i / a.L];
-    if (!(fit > *smax_ptr(a, s))) continue;
-    LiveSlot v;
-    const double f = load_committed(a, s, v);
-    if (!mutate_slot(a, s, g - 1, f, v)) continue;
-    if (atomicMax(&a.claim[s], (uint32_t)(g + 1)) >= (uint32_t)(g + 1)) continue;
-    store_committed(a, s, v);
-  }
-}
-
 constexpr int kCommitThreads = 256;
 
-// Single-rank fused commit + table (every touch of the generation went through
-// qeqea_values_kernel, which recorded the slot_max it started from and the
-// pending-mutation flag): only improving touches do random bank traffic.
-__global__ void __launch_bounds__(kCommitThreads)
-    qeqea_commit_table_kernel(QeqeaArgs a, int64_t t0, int64_t t1) {
+// Elitist accept + table update over the owned touches (engine.py:345-351 +
+// 202-222): a slot mutated at g-1 keeps its mutation iff some circuit of
+// generation g that touched it beat its slot_max, and slot_max becomes the
+// max over its touches (u64 atomicMax; fitness >= 0, so integer order ==
+// double order).  The values kernel recorded each touch's starting slot_max
+// and pending-mutation flag, so only improving touches do random bank traffic.
+__global__ void __launch_bounds__(kCommitThreads) qeqea_commit_table_kernel(QeqeaArgs a, int64_t t1) {
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
-  for (int64_t i = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t1;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double fit = a.fitness[i / a.L];
-    const double fb = a.touch_fbefore[i];
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t1;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double fit = a.fitness[t / a.Lr];
+    const double fb = a.touch_fbefore[t];
     if (!(fit > fb)) continue;
-    const uint32_t s = a.flats[i];
-    const uint8_t mf = a.touch_mutated[i];
+    const uint32_t s = a.owner_flats[t];
+    const int64_t loc = slot_local(a, s);
+    const uint8_t mf = a.touch_mutated[t];
     if (mf & 2) {
       // qutrit mutation: one improving touch per slot recomputes and writes it
-      if (atomicMax(&a.claim[s], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
+      if (atomicMax(&a.claim[loc], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
         LiveSlot v;
-        load_committed(a, s, v);  // commit writes only theta / qutrit, never slot_max
+        load_committed(a, loc, v);  // commit writes only theta / qutrit, never slot_max
         mutate_slot(a, s, g - 1, fb, v);
-        store_committed(a, s, v);
+        store_committed(a, loc, v);
       }
     } else if (mf & 1) {
       // angle mutation: every improving touch holds the same live angle
       // (values kernel), so the idempotent store needs no arbitration
-      if (s < a.Qt)
-        a.rot[s].theta = a.gate_thetas[i];
+      if (loc < a.Qtloc)
+        a.rot[loc].theta = a.owner_thetas[t];
       else
-        a.inter[s - a.Qt].theta = a.gate_thetas[i];
+        a.inter[loc - a.Qtloc].theta = a.owner_thetas[t];
     }
-    atomicMax(reinterpret_cast<unsigned long long*>(smax_ptr(a, s)),
+    atomicMax(reinterpret_cast<unsigned long long*>(smax_ptr(a, loc)),
               (unsigned long long)__double_as_longlong(fit));
-  }
-}
-
-// SegmentFitnessTable.update slot_max part: scatter-max of the circuit fitness
-// over its touched slots (fitness >= 0, so u64 order == double order).
-__global__ void qeqea_table_kernel(QeqeaArgs a) {
-  if (a.st->stop) return;
-  const int64_t total = a.P * a.L;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = a.flats[i];
-    const double fit = a.fitness[i / a.L];
-    double* sm = smax_ptr(a, s);
-    if (fit > *sm)
-      atomicMax(reinterpret_cast<unsigned long long*>(sm), (unsigned long long)__double_as_longlong(fit));
   }
 }
 
@@ -300,18 +352,19 @@ __global__ void qeqea_advance_kernel(QeqeaArgs a) {
 // Per-slot initial bank (init_population, engine.py:105-112; oracle/streams.py
 // init_slot): theta = uniform(0, 2pi) and a Box-Muller complex Gaussian qutrit.
 __global__ void qeqea_init_kernel(QeqeaArgs a) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q;
-       s += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; loc < a.Qloc;
+       loc += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = slot_global(a, loc);
     uint64_t w0[4], w1[4];
     stream_block(a.seed, DOM_INIT, 0, (uint64_t)s, 0, 1, w0);
     const double theta = __dadd_rn(0.0, __dmul_rn(kTwoPiD, u64_to_double(w0[0])));
-    a.claim[s] = 0;
-    if (s >= a.Qt) {
-      a.inter[s - a.Qt].theta = theta;
-      a.inter[s - a.Qt].smax = 0.0;
+    a.claim[loc] = 0;
+    if (loc >= a.Qtloc) {
+      a.inter[loc - a.Qtloc].theta = theta;
+      a.inter[loc - a.Qtloc].smax = 0.0;
     } else {
-      a.rot[s].theta = theta;
-      a.rot[s].smax = 0.0;
+      a.rot[loc].theta = theta;
+      a.rot[loc].smax = 0.0;
       stream_block(a.seed, DOM_INIT, 0, (uint64_t)s, 0, 2, w1);
       const uint64_t u[6] = {w0[1], w0[2], w0[3], w1[0], w1[1], w1[2]};
       double re[3], im[3], nn = 0.0;
@@ -327,60 +380,62 @@ __global__ void qeqea_init_kernel(QeqeaArgs a) {
       }
       const double nrm = sqrt(nn);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) a.rot[s].q[k] = make_double2(re[k] / nrm, im[k] / nrm);
+      for (int k = 0; k < 3; ++k) a.rot[loc].q[k] = make_double2(re[k] / nrm, im[k] / nrm);
     }
   }
 }
 
 // Live bank at the current generation (the reference's engine.pop after the
-// last step, i.e. committed values with the pending mutation applied).
+// last step, i.e. committed values with the pending mutation applied), over
+// the owned slots in local order (world 1: the reference's flat order).
 __global__ void qeqea_live_kernel(QeqeaArgs a, double* theta_out, double2* q_out) {
   const uint64_t g = a.st->generation;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q;
-       s += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; loc < a.Qloc;
+       loc += (int64_t)gridDim.x * blockDim.x) {
     LiveSlot v;
-    live_slot(a, s, g, v);
-    theta_out[s] = v.theta;
-    if (s < a.Qt) {
+    live_slot(a, slot_global(a, loc), g, v);
+    theta_out[loc] = v.theta;
+    if (loc < a.Qtloc) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) q_out[s * 3 + k] = v.q[k];
+      for (int k = 0; k < 3; ++k) q_out[loc * 3 + k] = v.q[k];
     }
   }
 }
 
-// Records <-> the reference's arrays: theta[Q], qamp[3][Qt] (axis-major), slot_max[Q].
+// Records <-> the reference's arrays (owned slots, local order): theta[Qloc],
+// qamp[3][Qtloc] (axis-major), slot_max[Qloc].
 __global__ void qeqea_pack_kernel(QeqeaArgs a, double* theta, double2* qamp, double* smax) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q;
-       s += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; loc < a.Qloc;
+       loc += (int64_t)gridDim.x * blockDim.x) {
     LiveSlot v;
-    const double f = load_committed(a, s, v);
-    theta[s] = v.theta;
-    smax[s] = f;
-    if (s < a.Qt) {
+    const double f = load_committed(a, loc, v);
+    theta[loc] = v.theta;
+    smax[loc] = f;
+    if (loc < a.Qtloc) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) qamp[k * a.Qt + s] = v.q[k];
+      for (int k = 0; k < 3; ++k) qamp[k * a.Qtloc + loc] = v.q[k];
     }
   }
 }
 
 __global__ void qeqea_unpack_kernel(QeqeaArgs a, const double* theta, const double2* qamp,
                                     const double* smax) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q;
-       s += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; loc < a.Qloc;
+       loc += (int64_t)gridDim.x * blockDim.x) {
     LiveSlot v;
-    v.theta = theta[s];
-    if (s < a.Qt) {
+    v.theta = theta[loc];
+    if (loc < a.Qtloc) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) v.q[k] = qamp[k * a.Qt + s];
+      for (int k = 0; k < 3; ++k) v.q[k] = qamp[k * a.Qtloc + loc];
     }
-    store_committed(a, s, v);
-    *smax_ptr(a, s) = smax ? smax[s] : 0.0;
-    a.claim[s] = 0;
+    store_committed(a, loc, v);
+    *smax_ptr(a, loc) = smax ? smax[loc] : 0.0;
+    a.claim[loc] = 0;
   }
 }
 
 // Blueprints and gate codes of circuits [c0, c1) at the current generation
-// (parity / introspection; same device functions as the eval kernel).
+// (parity / introspection, world 1; same device functions as the generation).
 __global__ void __launch_bounds__(kThreadsPerBlock)
     qeqea_sample_kernel(QeqeaArgs a, int64_t c0, int64_t c1, int64_t* flats_out, uint8_t* codes_out,
                         double* thetas_out) {
@@ -415,69 +470,82 @@ static int blocks_for(int64_t n, int threads) {
 
 
 
-isq_status qeqea_launch_prepare(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
-  const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, a.P);
-  qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a, 0, a.P);
-  if (c1 > c0)
-    qeqea_values_kernel<<<blocks_for((c1 - c0) * a.L, kValThreads), kValThreads, 0, s>>>(a, c0 * a.L, c1 * a.L);
+isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s) {
+  if (a.c0 < a.P) {
+    const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, a.S);
+    qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a);
+  }
+  if (a.world > 1) {
+    qeqea_route_kernel<<<blocks_for(a.S * a.L, 256), 256, 0, s>>>(a);
+  } else {
+    qeqea_values_kernel<<<blocks_for(a.P * a.L, kValThreads), kValThreads, 0, s>>>(a, a.P * a.L);
+  }
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
 
-isq_status qeqea_launch_score(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
-  if (c1 <= c0) return ISQ_OK;
-  return launch_fitness_batch_stoppable(a.n, a.L, c1 - c0, a.gate_codes, a.gate_thetas,
-                                        reinterpret_cast<const double*>(a.target), a.fitness + c0,
-                                        &a.st->stop, s);
+isq_status qeqea_launch_values(const QeqeaArgs& a, cudaStream_t s) {
+  if (a.world > 1) {
+    const int64_t t1 = a.world * a.S * a.Lr;
+    qeqea_values_kernel<<<blocks_for(t1, kValThreads), kValThreads, 0, s>>>(a, t1);
+    ISQ_CUDA_TRY(cudaGetLastError());
+  }
+  return ISQ_OK;
 }
 
-isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
-  isq_status st = qeqea_launch_prepare(a, c0, c1, s);
+isq_status qeqea_launch_score(const QeqeaArgs& a, cudaStream_t s) {
+  if (a.world > 1) qeqea_unroute_kernel<<<blocks_for(a.S * a.L, 256), 256, 0, s>>>(a);
+  const int64_t count = a.P - a.c0 < a.S ? a.P - a.c0 : a.S;
+  if (count > 0) {
+    isq_status st = launch_fitness_batch_stoppable(a.n, a.L, count, a.gate_codes, a.gate_thetas,
+                                                   reinterpret_cast<const double*>(a.target),
+                                                   a.fitness + a.c0, &a.st->stop, s);
+    if (st != ISQ_OK) return st;
+  }
+  if (a.world > 1) qeqea_elite_kernel<<<1, 256, 0, s>>>(a);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+isq_status qeqea_launch_eval(const QeqeaArgs& a, cudaStream_t s) {
+  isq_status st = qeqea_launch_prepare(a, s);
   if (st != ISQ_OK) return st;
-  return qeqea_launch_score(a, c0, c1, s);
-}
-
-static void launch_reduce(const QeqeaArgs& a, cudaStream_t s) {
-  qeqea_reduce_partials<<<a.n_parts, kRedThreads, 0, s>>>(a);
-  qeqea_reduce_final<<<1, kRedThreads, 0, s>>>(a);
+  return qeqea_launch_score(a, s);
 }
 
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
-  launch_reduce(a, s);
-  if (a.fused_commit) {
-    qeqea_commit_table_kernel<<<blocks_for(a.P * a.L, kCommitThreads), kCommitThreads, 0, s>>>(a, 0, a.P * a.L);
-  } else {
-    qeqea_commit_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
-    qeqea_table_kernel<<<blocks_for(a.P * a.L, 256), 256, 0, s>>>(a);
-  }
+  qeqea_reduce_partials<<<a.n_parts, kRedThreads, 0, s>>>(a);
+  qeqea_reduce_final<<<1, kRedThreads, 0, s>>>(a);
+  const int64_t t1 = a.world * a.S * a.Lr;
+  qeqea_commit_table_kernel<<<blocks_for(t1, kCommitThreads), kCommitThreads, 0, s>>>(a, t1);
   qeqea_advance_kernel<<<1, 1, 0, s>>>(a);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
 
 isq_status qeqea_launch_init(const QeqeaArgs& a, cudaStream_t s) {
-  qeqea_init_kernel<<<blocks_for(a.Q, 256), 256, 0, s>>>(a);
+  qeqea_init_kernel<<<blocks_for(a.Qloc, 256), 256, 0, s>>>(a);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
 
 isq_status qeqea_launch_pack(const QeqeaArgs& a, double* theta, double* qamp, double* smax,
                              cudaStream_t s) {
-  qeqea_pack_kernel<<<blocks_for(a.Q, 256), 256, 0, s>>>(a, theta, reinterpret_cast<double2*>(qamp), smax);
+  qeqea_pack_kernel<<<blocks_for(a.Qloc, 256), 256, 0, s>>>(a, theta, reinterpret_cast<double2*>(qamp), smax);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
 
 isq_status qeqea_launch_unpack(const QeqeaArgs& a, const double* theta, const double* qamp,
                                const double* smax, cudaStream_t s) {
-  qeqea_unpack_kernel<<<blocks_for(a.Q, 256), 256, 0, s>>>(
+  qeqea_unpack_kernel<<<blocks_for(a.Qloc, 256), 256, 0, s>>>(
       a, theta, reinterpret_cast<const double2*>(qamp), smax);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
 
 isq_status qeqea_launch_live(const QeqeaArgs& a, double* theta_out, double* q_out, cudaStream_t s) {
-  qeqea_live_kernel<<<blocks_for(a.Q, 256), 256, 0, s>>>(a, theta_out, reinterpret_cast<double2*>(q_out));
+  qeqea_live_kernel<<<blocks_for(a.Qloc, 256), 256, 0, s>>>(a, theta_out, reinterpret_cast<double2*>(q_out));
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }

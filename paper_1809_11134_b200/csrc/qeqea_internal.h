@@ -5,9 +5,12 @@
 
 namespace isq {
 
-isq_status qeqea_launch_prepare(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s);
-isq_status qeqea_launch_score(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s);
-isq_status qeqea_launch_eval(const QeqeaArgs& a, int64_t c0, int64_t c1, cudaStream_t s);
+// world 1: prepare = sample + values; world > 1: prepare = sample + route,
+// values = values of the received owned touches, score = unroute + fitness + elite.
+isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s);
+isq_status qeqea_launch_values(const QeqeaArgs& a, cudaStream_t s);
+isq_status qeqea_launch_score(const QeqeaArgs& a, cudaStream_t s);
+isq_status qeqea_launch_eval(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_init(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_pack(const QeqeaArgs& a, double* theta, double* qamp, double* smax,

@@ -1,53 +1,114 @@
-"""Population sharding across the GPUs of one box (SURVEY.md §8(e)).
+"""Population sharding across the GPUs of one box (SURVEY.md §8(e), DESIGN.md §8).
 
-One process per GPU (torchrun).  Every rank holds an identical replica of the
-bank (QEQEA) or of the genomes (GA) and evaluates only its shard of the P
-candidates: rank r scores circuits [r*S, (r+1)*S), S = ceil(P / world).  The
-only per-generation exchange is an all-gather of the fitness shards (P fp64,
-1 MiB per rank at C5) over NCCL / NVLink; every rank then replays the
-O(P*L) reductions, commit and table update (QEQEA) or SUS + breeding (GA)
-identically from counter-based RNG streams, so the replicas never diverge
-and no genome or bank traffic crosses the links.
+One process per GPU (torchrun).  Rank r of `world`:
 
-`ShardedRunner` is transport-agnostic: it drives an `ops` object
+* scores circuits [r*S, (r+1)*S) (S = ceil(P / world));
+* owns the bank slots of positions [b[r], b[r+1]) of every slot kind and
+  individual (b = `position_bounds(L, world)`).  A slot's position is fixed by
+  Eq. 9 (engine.py:82-87), so every touch of position p goes to the same owner
+  and the owners' bank shards never overlap.
 
-    ops.begin_batch()            mark the record window
-    ops.eval()                   score this rank's shard into ops.fitness_full
-    ops.finish()                 replay the generation's tail on the gathered vector
-    ops.read_batch() -> (records, stop_reason_code)
-    ops.fitness_full / ops.shard_len   the full (padded) fitness tensor, shard size
+Per QEQEA generation (include/isq.h split-phase protocol):
 
-and a torch.distributed process group; the device ops bind libisq handles
-(`DeviceQeqeaOps`, `DeviceGaOps`), the CPU tests bind the oracle.
+    prepare   sample this rank's circuits, group their touches by owner
+    a2a       flat slots -> owners                      (S*L*4 B per rank)
+    values    owners: live slot (lazy mutation) + measured gate code
+    a2a       gate codes + live angles -> circuit ranks (S*L*9 B per rank)
+    score     compose + score this rank's circuits, shard elite record
+    gather    fitness (P fp64) + elite records          (all-gather)
+    finish    reductions (replicated on the gathered vector), best gates from
+              the elite of the rank holding them, commit + table update of
+              the owned touches only
+
+so every O(P*L) pass (sampling, bank gathers, commit) and the O(P*L*4^n)
+fitness are divided by `world`; only the O(P) reduction is replicated.
+GA (`ga.py`): genomes are replicated, rank r scores its genome shard, the
+fitness vector is all-gathered and every rank breeds identically from the
+counter streams.
+
+`ShardedRunner` drives an `ops` object through `ops.generation(comm)`; the
+device ops bind libisq handles (`DeviceQeqeaOps`, `DeviceGaOps`), the CPU tests
+bind oracle replicas, and `Comm` is the only code that calls torch.distributed.
 """
 from __future__ import annotations
 
 import ctypes
-from typing import Optional
+from typing import List, Optional
 
 import numpy as np
 
 from . import _lib
-from .engine import STOP_REASONS
+from .engine import STOP_REASONS, position_bounds
 
 
-class _CAI:
-    """__cuda_array_interface__ view of a libisq-owned fp64 device buffer."""
+class Routing:
+    """Split sizes of the two all-to-alls (shared by the device and test ops).
 
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
-                                         "version": 3, "strides": None}
+    Exchange layout: the touches a circuit rank sends to owner o form a
+    block of S x Lr(o) entries (row = circuit, column = owned position) at
+    offset S * b[o]; an owner receives world blocks of S x Lr(r), i.e. one row
+    per global (padded) circuit."""
+
+    def __init__(self, length: int, shard: int, world: int, rank: int):
+        self.L, self.S, self.world, self.rank = int(length), int(shard), int(world), int(rank)
+        self.bounds = position_bounds(self.L, self.world)
+        self.widths = [self.bounds[o + 1] - self.bounds[o] for o in range(self.world)]
+        self.Lr = self.widths[self.rank]
+
+    @property
+    def to_owners(self) -> List[int]:
+        """Send splits of the flats (and receive splits of the codes / angles)."""
+        return [self.S * w for w in self.widths]
+
+    @property
+    def from_circuits(self) -> List[int]:
+        """Receive splits of the flats (and send splits of the codes / angles)."""
+        return [self.S * self.Lr] * self.world
+
+    def route(self, circuit_major: np.ndarray) -> np.ndarray:
+        """(S, L) -> owner-grouped flat layout (host restatement of qeqea_route_kernel)."""
+        return np.concatenate([circuit_major[:, self.bounds[o]:self.bounds[o + 1]].reshape(-1)
+                               for o in range(self.world)])
+
+    def unroute(self, grouped: np.ndarray) -> np.ndarray:
+        """Owner-grouped flat layout -> (S, L) (host restatement of qeqea_unroute_kernel)."""
+        out = np.empty((self.S, self.L), dtype=grouped.dtype)
+        for o in range(self.world):
+            off = self.S * self.bounds[o]
+            out[:, self.bounds[o]:self.bounds[o + 1]] = grouped[off:off + self.S * self.widths[o]].reshape(
+                self.S, self.widths[o])
+        return out
+
+
+class Comm:
+    """The collectives of one generation over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_to_all(self, out, inp, out_splits: List[int], in_splits: List[int]):
+        self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def all_gather(self, full, chunk: int):
+        """In-place all-gather: rank r contributes full[r*chunk:(r+1)*chunk]."""
+        mine = full[self.rank * chunk:(self.rank + 1) * chunk].clone()
+        self.dist.all_gather_into_tensor(full, mine, group=self.group)
 
 
 class ShardedRunner:
-    def __init__(self, ops, group=None):
-        import torch.distributed as dist
+    """Generation loop of one rank.  `comm` defaults to torch.distributed over
+    `group`; anything with the same three methods works (the single-GPU
+    emulation in tests/test_sharded_gpu.py passes an in-process one)."""
 
+    def __init__(self, ops, group=None, comm=None):
         self.ops = ops
-        self.group = group
-        self.dist = dist
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        self.comm = comm if comm is not None else Comm(group)
+        self.world, self.rank = self.comm.world, self.comm.rank
         self.generation = 0
         self.best_fitness = 0.0
         self.stop_reason: Optional[str] = None
@@ -55,11 +116,6 @@ class ShardedRunner:
     @property
     def done(self) -> bool:
         return self.stop_reason is not None
-
-    def _exchange(self):
-        full, S = self.ops.fitness_full, self.ops.shard_len
-        mine = full[self.rank * S:(self.rank + 1) * S].clone()
-        self.dist.all_gather_into_tensor(full, mine, group=self.group)
 
     def steps(self, n: int) -> np.ndarray:
         """Up to n generations; stops where the single-device engine would."""
@@ -69,9 +125,7 @@ class ShardedRunner:
             k = min(remaining, getattr(self.ops, "max_batch", remaining))
             self.ops.begin_batch()
             for _ in range(k):
-                self.ops.eval()
-                self._exchange()
-                self.ops.finish()
+                self.ops.generation(self.comm)
             rec, stop = self.ops.read_batch()
             if rec.size:
                 self.generation += int(rec.size)
@@ -80,6 +134,17 @@ class ShardedRunner:
             out.append(rec)
             remaining -= k
         return np.concatenate(out) if out else np.zeros(0, dtype=_lib.GEN_RECORD)
+
+
+def _device_view(ptr: int, n: int, typestr: str, device: int):
+    """torch view of a libisq-owned device buffer (__cuda_array_interface__)."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_CAI(), device=f"cuda:{device}")
 
 
 class _DeviceOps:
@@ -93,14 +158,7 @@ class _DeviceOps:
         self.h = engine._handle()
         self.max_batch = engine.max_batch
         self.stream = torch.cuda.current_stream(engine.device)
-        f = getattr(self.lib, f"isq_{self._prefix}_set_stream")
-        _lib.check(f(self.h, ctypes.c_void_p(self.stream.cuda_stream)))
-        ptr, shard = ctypes.c_void_p(), ctypes.c_int64()
-        _lib.check(getattr(self.lib, f"isq_{self._prefix}_buffers")(self.h, ctypes.byref(ptr),
-                                                                     ctypes.byref(shard), None))
-        self.shard_len = int(shard.value)
-        self.fitness_full = torch.as_tensor(_CAI(ptr.value, self.shard_len * engine.world),
-                                            device=f"cuda:{engine.device}")
+        self._call("set_stream", ctypes.c_void_p(self.stream.cuda_stream))
 
     def _call(self, name, *args):
         _lib.check(getattr(self.lib, f"isq_{self._prefix}_{name}")(self.h, *args))
@@ -108,25 +166,79 @@ class _DeviceOps:
     def begin_batch(self):
         self._call("begin_batch")
 
-    def eval(self):
-        self._call("eval")
-
-    def finish(self):
-        self._call("finish")
-
     def read_batch(self):
         rec = np.zeros(self.max_batch, dtype=_lib.GEN_RECORD)
         nd, stop = ctypes.c_int32(), ctypes.c_int32()
         self._call("read_batch", _lib.ptr(rec), ctypes.byref(nd), ctypes.byref(stop), None, None)
-        return rec[: nd.value], int(stop.value)
+        rec = rec[: nd.value]
+        self.engine._absorb(rec, int(stop.value))  # keep the engine's host mirror (generation, best) current
+        return rec, int(stop.value)
 
 
 class DeviceQeqeaOps(_DeviceOps):
     _prefix = "qeqea"
 
+    def __init__(self, engine):
+        super().__init__(engine)
+        x = _lib.QeqeaExchange()
+        self._call("exchange", ctypes.byref(x))
+        self.world, self.rank, self.S = x.world, x.rank, x.shard
+        self.routing = Routing(engine.cfg.size_of_individual, self.S, self.world, self.rank)
+        L, dev, no = engine.cfg.size_of_individual, engine.device, self.world * self.S * self.routing.Lr
+        self.fitness = _device_view(x.fitness, self.world * self.S, "<f8", dev)
+        if self.world > 1:
+            self.elite_len = x.elite_len
+            self.elite = _device_view(x.elite, self.world * x.elite_len, "<f8", dev)
+            # uint32 slot indices travel as int32 (same bytes)
+            self.send_flats = _device_view(x.send_flats, self.S * L, "<i4", dev)
+            self.recv_flats = _device_view(x.recv_flats, no, "<i4", dev)
+            self.send_codes = _device_view(x.send_codes, no, "|u1", dev)
+            self.recv_codes = _device_view(x.recv_codes, self.S * L, "|u1", dev)
+            self.send_thetas = _device_view(x.send_thetas, no, "<f8", dev)
+            self.recv_thetas = _device_view(x.recv_thetas, self.S * L, "<f8", dev)
+
+    def generation(self, comm: Optional[Comm], marks=None):
+        """One generation; `marks` (4 torch.cuda.Events, optional) are recorded
+        on the handle's stream before prepare, before score, after score and
+        after finish (bench.py phase timing)."""
+        r = self.routing
+        if marks:
+            marks[0].record(self.stream)
+        self._call("prepare")
+        if self.world > 1:
+            comm.all_to_all(self.recv_flats, self.send_flats, r.from_circuits, r.to_owners)
+        self._call("values")
+        if self.world > 1:
+            comm.all_to_all(self.recv_codes, self.send_codes, r.to_owners, r.from_circuits)
+            comm.all_to_all(self.recv_thetas, self.send_thetas, r.to_owners, r.from_circuits)
+        if marks:
+            marks[1].record(self.stream)
+        self._call("score")
+        if marks:
+            marks[2].record(self.stream)
+        if self.world > 1:
+            comm.all_gather(self.fitness, self.S)
+            comm.all_gather(self.elite, self.elite_len)
+        self._call("finish")
+        if marks:
+            marks[3].record(self.stream)
+
 
 class DeviceGaOps(_DeviceOps):
     _prefix = "ga"
+
+    def __init__(self, engine):
+        super().__init__(engine)
+        ptr, shard = ctypes.c_void_p(), ctypes.c_int64()
+        _lib.check(self.lib.isq_ga_buffers(self.h, ctypes.byref(ptr), ctypes.byref(shard), None))
+        self.S = int(shard.value)
+        self.fitness = _device_view(ptr.value, self.S * engine.world, "<f8", engine.device)
+
+    def generation(self, comm: Optional[Comm]):
+        self._call("eval")
+        if comm is not None and comm.world > 1:
+            comm.all_gather(self.fitness, self.S)
+        self._call("finish")
 
 
 def sharded_qeqea(cfg, target, seed: int, group=None, **kw) -> ShardedRunner:

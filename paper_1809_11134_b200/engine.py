@@ -118,6 +118,21 @@ class SegmentTableView:
         return self._engine._get_state()[2]
 
 
+def position_bounds(length: int, world: int) -> List[int]:
+    """Rank o of a sharded run owns the bank slots of positions [b[o], b[o+1])
+    (csrc/api_qeqea.cu isq_qeqea_create)."""
+    return [o * length // world for o in range(world + 1)]
+
+
+def owned_slots(cfg: PopulationConfig, rank: int, world: int) -> np.ndarray:
+    """Flat slot indices (Eq. 9, engine.py:82-87) owned by `rank`, in the
+    device's local order (slot kind, individual, owned position)."""
+    b = position_bounds(cfg.size_of_individual, world)
+    ki = np.arange(cfg.slot_kind_count * cfg.size_of_population, dtype=np.int64)[:, None]
+    pos = np.arange(b[rank], b[rank + 1], dtype=np.int64)[None, :]
+    return (ki * cfg.size_of_individual + pos).reshape(-1)
+
+
 def _target_array(target: TargetSpec | np.ndarray, n: int, name: str = "target") -> np.ndarray:
     m = target.matrix if isinstance(target, TargetSpec) else np.asarray(target)
     if m.shape[0] != 2 ** n:
@@ -210,11 +225,19 @@ class QeqeaEngine:
         return self._h
 
     # ------------------------------------------------------------- state --
-    def _get_state(self):
+    def _local_counts(self):
+        """(owned slots, owned rotation-region slots): Q and Qt at world 1."""
         c = self.cfg
-        th = np.empty(c.qubit_count)
-        qa = np.empty((3, c.qutrit_count), dtype=np.complex128)
-        sm = np.empty(c.qubit_count)
+        b = position_bounds(c.size_of_individual, self.world)
+        lr = b[self.rank + 1] - b[self.rank]
+        return (c.slot_kind_count * c.size_of_population * lr,
+                c.number_of_wires * c.size_of_population * lr)
+
+    def _get_state(self):
+        ql, qtl = self._local_counts()
+        th = np.empty(ql)
+        qa = np.empty((3, qtl), dtype=np.complex128)
+        sm = np.empty(ql)
         gen = ctypes.c_uint64()
         best = ctypes.c_double()
         stop = ctypes.c_int32()
@@ -223,24 +246,38 @@ class QeqeaEngine:
         return th, qa, sm, int(gen.value), float(best.value), int(stop.value)
 
     def _set_population(self, pop: PopulationState):
+        """Injects the reference's full arrays (init_population); a sharded
+        rank keeps the slots it owns."""
         c = self.cfg
-        th = np.ascontiguousarray(pop.thetas, dtype=np.float64)
+        th = np.asarray(pop.thetas, dtype=np.float64)
         q = np.asarray(pop.qutrits, dtype=np.complex128)
         if th.shape != (c.qubit_count,) or q.shape != (c.qutrit_count, 3):
             raise ConfigurationError("population shape does not match the configuration")
+        if self.world > 1:
+            own = owned_slots(c, self.rank, self.world)
+            th = th[own]
+            q = q[own[own < c.qutrit_count]]
+        th = np.ascontiguousarray(th)
         qa = np.ascontiguousarray(q.T)
         _lib.check(self._lib.isq_qeqea_set_state(self._handle(), _lib.ptr(th), _lib.ptr(qa), None,
                                                  self.generation, self.best_fitness,
                                                  _STOP_CODES[self.stop_reason], None, None))
 
+    def owned_population(self):
+        """(flat slots, PopulationState) of the live bank slots this rank
+        owns; at world 1 the whole bank in flat order (== pop)."""
+        ql, qtl = self._local_counts()
+        th = np.empty(ql)
+        q = np.empty((qtl, 3), dtype=np.complex128)
+        _lib.check(self._lib.isq_qeqea_live_population(self._handle(), _lib.ptr(th), _lib.ptr(q)))
+        return owned_slots(self.cfg, self.rank, self.world), PopulationState(thetas=th, qutrits=q)
+
     @property
     def pop(self) -> PopulationState:
         """The live bank (engine.pop after the last step)."""
-        c = self.cfg
-        th = np.empty(c.qubit_count)
-        q = np.empty((c.qutrit_count, 3), dtype=np.complex128)
-        _lib.check(self._lib.isq_qeqea_live_population(self._handle(), _lib.ptr(th), _lib.ptr(q)))
-        return PopulationState(thetas=th, qutrits=q)
+        if self.world > 1:
+            raise ConfigurationError("the bank is sharded over the ranks; use owned_population()")
+        return self.owned_population()[1]
 
     @property
     def table(self) -> SegmentTableView:

@@ -167,15 +167,18 @@ class GaEngine:
             _lib.check(self._lib.isq_ga_step(self._handle(), k, _lib.ptr(rec), ctypes.byref(nd),
                                              ctypes.byref(stop)))
             rec = rec[: nd.value]
-            if rec.size:
-                self.generation += int(rec.size)
-                if rec["best_fitness"][-1] > self.best_fitness:
-                    self._best_dirty = True
-                self.best_fitness = float(rec["best_fitness"][-1])
-            self.stop_reason = STOP_REASONS[int(stop.value)]
+            self._absorb(rec, stop.value)
             out.append(rec)
             remaining -= k
         return np.concatenate(out) if out else np.zeros(0, dtype=_lib.GEN_RECORD)
+
+    def _absorb(self, rec: np.ndarray, stop: int):
+        if rec.size:
+            self.generation += int(rec.size)
+            if rec["best_fitness"][-1] > self.best_fitness:
+                self._best_dirty = True
+            self.best_fitness = float(rec["best_fitness"][-1])
+        self.stop_reason = STOP_REASONS[int(stop)]
 
     def step(self) -> Tuple[float, float]:
         """One generation (ga.py:165-194); returns (generation best, mean)."""

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
-    assert lib.isq_abi_version() == 1
+    assert lib.isq_abi_version() == 2
 
 
 @pytest.mark.parametrize("key", [(0, 1, 0, 0, 0), (7, 3, 12, 999, 0), (2**63 + 5, 8, 2**40, 3, 17)])
