@@ -16,6 +16,7 @@ struct QeqeaHandle {
   int max_batch = 0;
   GenRecord* h_records = nullptr;  // pinned
   QeqeaDevState* h_state = nullptr;  // pinned
+  GenGraph graph;                    // isq_qeqea_step on small populations
 };
 
 static void free_handle(QeqeaHandle* h) {
@@ -34,6 +35,7 @@ static void free_handle(QeqeaHandle* h) {
     cudaFree(a.owner_codes);
     cudaFree(a.owner_thetas);
   }
+  h->graph.reset();
   if (h->h_records) cudaFreeHost(h->h_records);
   if (h->h_state) cudaFreeHost(h->h_state);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -310,12 +312,13 @@ isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_re
   }
   isq_status st = isq_qeqea_begin_batch(handle);
   if (st != ISQ_OK) return st;
-  for (int i = 0; i < n_generations; ++i) {
-    st = qeqea_launch_eval(h->a, h->stream);
-    if (st != ISQ_OK) return st;
-    st = qeqea_launch_finish(h->a, h->stream);
-    if (st != ISQ_OK) return st;
-  }
+  const QeqeaArgs& a = h->a;
+  st = run_generations(h->graph, h->stream, n_generations, graph_generations(a.P * a.L),
+                       [&a](cudaStream_t s) {
+                         isq_status r = qeqea_launch_eval(a, s);
+                         return r != ISQ_OK ? r : qeqea_launch_finish(a, s);
+                       });
+  if (st != ISQ_OK) return st;
   return isq_qeqea_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
 }
 

@@ -44,6 +44,55 @@ isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uin
                                           double* fitness_dev, const int32_t* stop,
                                           cudaStream_t stream, int blocks_per_sm = 0);
 
+// Launch-bound small populations: `per_graph` generations captured once into
+// a CUDA graph (on a private capture stream, so the caller's stream may be the
+// legacy default stream) and replayed on the handle's stream.  Valid because
+// every generation kernel reads the generation / stop flag from device state
+// and takes only handle-constant arguments.
+struct GenGraph {
+  cudaGraphExec_t exec = nullptr;
+  int gens = 0;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    gens = 0;
+  }
+};
+
+template <class EnqueueOne>
+isq_status run_generations(GenGraph& g, cudaStream_t stream, int n, int per_graph, EnqueueOne enqueue_one) {
+  int done = 0;
+  if (per_graph > 1 && n >= per_graph) {
+    if (g.exec == nullptr || g.gens != per_graph) {
+      g.reset();
+      cudaStream_t cap = nullptr;
+      ISQ_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+      isq_status st = ISQ_OK;
+      for (int i = 0; e == cudaSuccess && st == ISQ_OK && i < per_graph; ++i) st = enqueue_one(cap);
+      cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+      if (e == cudaSuccess) e = e2;
+      if (e == cudaSuccess && st == ISQ_OK) e = cudaGraphInstantiate(&g.exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      cudaStreamDestroy(cap);
+      if (st != ISQ_OK) return st;
+      ISQ_CUDA_TRY(e);
+      g.gens = per_graph;
+    }
+    for (; done + per_graph <= n; done += per_graph) ISQ_CUDA_TRY(cudaGraphLaunch(g.exec, stream));
+  }
+  for (; done < n; ++done) {
+    isq_status st = enqueue_one(stream);
+    if (st != ISQ_OK) return st;
+  }
+  return ISQ_OK;
+}
+
+// Generations per graph for a population of `touches` = P * L gate slots
+// (0: plain launches; large populations are not launch-bound).
+inline int graph_generations(int64_t touches) { return touches <= (1LL << 18) ? 16 : 0; }
+
 isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, const double* T,
                                   double* out, cudaStream_t stream);
 

@@ -287,12 +287,14 @@ struct GaHandle {
   int rank = 0, world = 1;
   int64_t shard = 0;
   int max_batch = 0;
+  GenGraph graph;  // isq_ga_step on small populations
 };
 
 static void ga_free(GaHandle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  h->graph.reset();
   GaArgs& a = h->a;
   for (int b = 0; b < 2; ++b) {
     cudaFree(a.codes[b]);
@@ -509,12 +511,12 @@ isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, 
   }
   isq_status st = isq_ga_begin_batch(handle);
   if (st != ISQ_OK) return st;
-  for (int i = 0; i < n; ++i) {
-    st = ga_launch_eval(h->a, 0, h->a.P, h->stream);
-    if (st != ISQ_OK) return st;
-    st = ga_launch_finish(h->a, h->stream);
-    if (st != ISQ_OK) return st;
-  }
+  const GaArgs& a = h->a;
+  st = run_generations(h->graph, h->stream, n, graph_generations(a.P * a.L), [&a](cudaStream_t s) {
+    isq_status r = ga_launch_eval(a, 0, a.P, s);
+    return r != ISQ_OK ? r : ga_launch_finish(a, s);
+  });
+  if (st != ISQ_OK) return st;
   return isq_ga_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
 }
 
