@@ -38,6 +38,8 @@ struct FastChunk {
   int dmask[32];       // diag: row mask whose parity picks up e^{i th}; 0 for rotations
   int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit
   double2 fac[32];     // flush factors / final row weights, indexed by physical row
+  double nth[32];      // next chunk's angles / codes, staged by cp.async (no registers held)
+  uint32_t ncode[8];
 };
 
 enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
@@ -252,6 +254,31 @@ struct FastEval {
   }
 };
 
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Stage the (code, theta) row slice [nb, nb + 32) of circuit nc in shared
+// memory with cp.async, so the prefetch holds no registers (a register
+// prefetch was spilled and its store waited on the load right away).
+__device__ __forceinline__ void stage_chunk(FastChunk& sm, int64_t count, int L, const uint8_t* codes,
+                                            const double* thetas, int64_t nc, int nb, int lane) {
+  if (nc >= count) return;
+  const int64_t row = nc * (int64_t)L + nb;
+  if (nb + lane < L) cp_async(&sm.nth[lane], thetas + row + lane, 8);
+  const uint8_t* src = codes + row;
+  if (nb + 32 <= L && ((reinterpret_cast<uintptr_t>(src) & 3) == 0)) {
+    if (lane < 8) cp_async(&sm.ncode[lane], src + 4 * lane, 4);
+  } else {
+    if (nb + lane < L) reinterpret_cast<uint8_t*>(sm.ncode)[lane] = src[lane];
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
 // Grid-stride body shared by the explicit-gate fitness kernels: warp per
 // circuit over circuits [0, count) of (codes, thetas) rows of length L.
 template <int NQ>
@@ -264,33 +291,29 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
   FastChunk& cs = sh[wib];
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
   int64_t c = (int64_t)blockIdx.x * warps_per_block + wib;
-  // (code, theta) of the next chunk are loaded one chunk ahead
-  int code = 0;
-  double th = 0.0;
-  if (c < count && lane < L) {
-    code = codes[c * (int64_t)L + lane];
-    th = thetas[c * (int64_t)L + lane];
-  }
+  stage_chunk(cs, count, L, codes, thetas, c, 0, lane);
   for (; c < count; c += nwarps) {
     FastEval<NQ> ev;
     ev.begin(lane);
     for (int base = 0; base < L; base += 32) {
       const int nq = min(32, L - base);
+      asm volatile("cp.async.wait_all;\n" ::);
+      __syncwarp();
+      int code = 0;
+      double th = 0.0;
+      if (lane < nq) {
+        code = reinterpret_cast<const uint8_t*>(cs.ncode)[lane];
+        th = cs.nth[lane];
+      }
+      __syncwarp();
       int64_t nc = c;
       int nb = base + 32;
       if (nb >= L) {
         nc = c + nwarps;
         nb = 0;
       }
-      int ncode = 0;
-      double nth = 0.0;
-      if (nc < count && nb + lane < L) {
-        ncode = codes[nc * (int64_t)L + nb + lane];
-        nth = thetas[nc * (int64_t)L + nb + lane];
-      }
+      stage_chunk(cs, count, L, codes, thetas, nc, nb, lane);
       ev.chunk(code, th, nq, cs, lane);
-      code = ncode;
-      th = nth;
     }
     const double f = ev.finish(Ts, cs, lane);
     if (lane == 0) fitness[c] = f;

@@ -14,7 +14,7 @@ if [ "${PROFILE:-1}" = "1" ]; then
   timeout 300 python tools/engine_bench.py --P 1048576 --gens 2 > $OUT/plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $OUT/launches_c5.csv python tools/engine_bench.py --P 1048576 --gens 2 > $OUT/ncu_launch.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fitness_fast|qeqea_values|qeqea_commit" -s 10 -c 3 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fitness_fast|qeqea_values|qeqea_commit" -s 9 -c 3 \
       -o $OUT/prof_c5 python tools/engine_bench.py --P 1048576 --gens 2 > $OUT/ncu_full.log 2>&1
   echo "ncu rc=$?" >> $OUT/ncu_full.log
 fi
