@@ -313,6 +313,11 @@ isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_re
   isq_status st = isq_qeqea_begin_batch(handle);
   if (st != ISQ_OK) return st;
   const QeqeaArgs& a = h->a;
+  if (qeqea_small(a)) {
+    st = n_generations > 0 ? qeqea_launch_small(a, n_generations, h->stream) : ISQ_OK;
+    if (st != ISQ_OK) return st;
+    return isq_qeqea_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
+  }
   st = run_generations(h->graph, h->stream, n_generations, graph_generations(a.P * a.L),
                        [&a](cudaStream_t s) {
                          isq_status r = qeqea_launch_eval(a, s);

@@ -91,6 +91,43 @@ struct MeasureTask {  // 56 B: 768 tasks fit the 48 KB static shared limit
   uint32_t out;
 };
 
+// Values phase of owned touch t up to the Born measurement: the live value
+// goes to v, the angle / starting slot_max / mutation flags to the touch
+// arrays, and interaction slots get their gate code.  Returns true when the
+// touch is a rotation slot still to be measured (measure_code).
+__device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, uint64_t g, uint32_t& s,
+                                                 LiveSlot& v) {
+  s = a.owner_flats[t];
+  if (s == kNoSlot) {  // padding circuit: never commits (fitness <= 1 < 2)
+    a.owner_codes[t] = 0;
+    a.owner_thetas[t] = 0.0;
+    a.touch_fbefore[t] = 2.0;
+    a.touch_mutated[t] = 0;
+    return false;
+  }
+  const double f = load_committed(a, slot_local(a, s), v);
+  bool qpath = false;
+  const bool mutated = g > 0 && mutate_slot(a, s, g - 1, f, v, &qpath);
+  a.owner_thetas[t] = v.theta;
+  a.touch_fbefore[t] = f;
+  a.touch_mutated[t] = (uint8_t)((mutated ? 1 : 0) | (mutated && qpath ? 2 : 0));
+  const int64_t kind = (int64_t)s / (a.L * a.P);
+  if (kind < a.n) return true;
+  a.owner_codes[t] = (uint8_t)(3 * a.n + (kind - a.n));
+  return false;
+}
+
+// construct_segments for one rotation slot (engine.py:167-170): Born
+// measurement on the slot's (generation, slot) stream -> gate code.
+__device__ __forceinline__ uint8_t measure_code(const QeqeaArgs& a, uint32_t s, uint64_t g, double re[3],
+                                                double im[3]) {
+  NpStream st;
+  st.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);
+  bool ok = true;
+  const int axis = measure_axis(re, im, a.n_meas, st, &ok);
+  return (uint8_t)(3 * ((int64_t)s / (a.L * a.P)) + axis);
+}
+
 __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t1) {
   __shared__ MeasureTask tasks[kValThreads * kValPerThread];
   __shared__ int ntask;
@@ -104,23 +141,9 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
     for (int u = 0; u < kValPerThread; ++u) {
       const int64_t t = base + u * kValThreads + threadIdx.x;
       if (t >= t1) break;
-      const uint32_t s = a.owner_flats[t];
-      if (s == kNoSlot) {  // padding circuit: never commits (fitness <= 1 < 2)
-        a.owner_codes[t] = 0;
-        a.owner_thetas[t] = 0.0;
-        a.touch_fbefore[t] = 2.0;
-        a.touch_mutated[t] = 0;
-        continue;
-      }
+      uint32_t s;
       LiveSlot v;
-      const double f = load_committed(a, slot_local(a, s), v);
-      bool qpath = false;
-      const bool mutated = g > 0 && mutate_slot(a, s, g - 1, f, v, &qpath);
-      a.owner_thetas[t] = v.theta;
-      a.touch_fbefore[t] = f;
-      a.touch_mutated[t] = (uint8_t)((mutated ? 1 : 0) | (mutated && qpath ? 2 : 0));
-      const int64_t kind = (int64_t)s / (a.L * a.P);
-      if (kind < a.n) {
+      if (value_touch_head(a, t, g, s, v)) {
         const int k = atomicAdd(&ntask, 1);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -129,21 +152,14 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
         }
         tasks[k].s = s;
         tasks[k].out = (uint32_t)(t - base);
-      } else {
-        a.owner_codes[t] = (uint8_t)(3 * a.n + (kind - a.n));
       }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < ntask; k += kValThreads) {
       const MeasureTask& mt = tasks[k];
-      NpStream st;
-      st.init(a.seed, DOM_MEASURE, g, (uint64_t)mt.s, 0);
       double re[3] = {mt.re[0], mt.re[1], mt.re[2]};
       double im[3] = {mt.im[0], mt.im[1], mt.im[2]};
-      bool ok = true;
-      const int axis = measure_axis(re, im, a.n_meas, st, &ok);
-      const int64_t kind = (int64_t)mt.s / (a.L * a.P);
-      a.owner_codes[base + mt.out] = (uint8_t)(3 * kind + axis);
+      a.owner_codes[base + mt.out] = measure_code(a, mt.s, g, re, im);
     }
     __syncthreads();
   }
@@ -197,17 +213,16 @@ __global__ void __launch_bounds__(256) qeqea_elite_kernel(QeqeaArgs a) {
 
 constexpr int kRedThreads = 256;
 
-// Deterministic block partials of (max with first argmax, sum) over fitness[0, P).
-__global__ void __launch_bounds__(kRedThreads) qeqea_reduce_partials(QeqeaArgs a) {
-  if (a.st->stop) return;
-  __shared__ double smax[kRedThreads], ssum[kRedThreads];
-  __shared__ int64_t sarg[kRedThreads];
+// Deterministic block partial `part` of (max with first argmax, sum) over
+// fitness[0, P); kRedThreads threads, shared scratch of kRedThreads each.
+__device__ __forceinline__ void reduce_partial_body(const QeqeaArgs& a, int part, double* smax,
+                                                    double* ssum, int64_t* sarg) {
   const int64_t per = (a.P + a.n_parts - 1) / a.n_parts;
-  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t lo = (int64_t)part * per;
   const int64_t hi = min(a.P, lo + per);
   double m = -1.0, sum = 0.0;
   int64_t arg = INT64_MAX;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kRedThreads) {
     const double f = a.fitness[i];
     sum += f;
     if (f > m) {
@@ -232,20 +247,24 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_partials(QeqeaArgs a
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    a.part_max[blockIdx.x] = smax[0];
-    a.part_sum[blockIdx.x] = ssum[0];
-    a.part_arg[blockIdx.x] = sarg[0];
+    a.part_max[part] = smax[0];
+    a.part_sum[part] = ssum[0];
+    a.part_arg[part] = sarg[0];
   }
+}
+
+__global__ void __launch_bounds__(kRedThreads) qeqea_reduce_partials(QeqeaArgs a) {
+  if (a.st->stop) return;
+  __shared__ double smax[kRedThreads], ssum[kRedThreads];
+  __shared__ int64_t sarg[kRedThreads];
+  reduce_partial_body(a, blockIdx.x, smax, ssum, sarg);
 }
 
 // Final reduction, best-so-far update (strict >, first circuit on ties,
 // engine.py:341-343), the generation record, and capture of the new best
-// circuit's gates by warp 0.
-__global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
-  __shared__ int s_improved;
-  __shared__ int64_t s_best;
+// circuit's gates by warp 0.  All threads of the block call it.
+__device__ __forceinline__ void reduce_final_body(const QeqeaArgs& a, int* s_improved, int64_t* s_best) {
   QeqeaDevState* st = a.st;
-  if (st->stop) return;
   if (threadIdx.x == 0) {
     double m = -1.0, sum = 0.0;
     int64_t arg = INT64_MAX;
@@ -273,26 +292,33 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
     r.pad = 0.0;
     const uint64_t ri = st->generation - st->rec_base;
     if (ri < (uint64_t)a.rec_cap) a.records[ri] = r;
-    s_improved = improved;
-    s_best = arg;
+    *s_improved = improved;
+    *s_best = arg;
   }
   __syncthreads();
-  if (!s_improved || threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  const uint64_t g = st->generation;
-  for (int p = lane; p < a.L; p += 32) {
-    if (a.world == 1) {
-      // the generation's gate codes / live angles of every circuit are still
-      // in place (do not recompute them from the bank: the commit rewrites it)
-      a.best_codes[p] = a.gate_codes[s_best * a.L + p];
-      a.best_thetas[p] = a.gate_thetas[s_best * a.L + p];
-    } else {
-      // gathered elite record of the rank that scored the best circuit
-      const double* e = a.elite + (s_best / a.S) * a.elite_len;
-      a.best_codes[p] = reinterpret_cast<const uint8_t*>(e + 2 + a.L)[p];
-      a.best_thetas[p] = e[2 + p];
+  if (*s_improved && threadIdx.x < 32) {
+    const int64_t best = *s_best;
+    for (int p = threadIdx.x; p < a.L; p += 32) {
+      if (a.world == 1) {
+        // the generation's gate codes / live angles of every circuit are still
+        // in place (do not recompute them from the bank: the commit rewrites it)
+        a.best_codes[p] = a.gate_codes[best * a.L + p];
+        a.best_thetas[p] = a.gate_thetas[best * a.L + p];
+      } else {
+        // gathered elite record of the rank that scored the best circuit
+        const double* e = a.elite + (best / a.S) * a.elite_len;
+        a.best_codes[p] = reinterpret_cast<const uint8_t*>(e + 2 + a.L)[p];
+        a.best_thetas[p] = e[2 + p];
+      }
     }
   }
+}
+
+__global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
+  __shared__ int s_improved;
+  __shared__ int64_t s_best;
+  if (a.st->stop) return;
+  reduce_final_body(a, &s_improved, &s_best);
 }
 
 // -------------------------------------------------------------- commit ---
@@ -305,46 +331,53 @@ constexpr int kCommitThreads = 256;
 // max over its touches (u64 atomicMax; fitness >= 0, so integer order ==
 // double order).  The values kernel recorded each touch's starting slot_max
 // and pending-mutation flag, so only improving touches do random bank traffic.
+__device__ __forceinline__ void commit_touch(const QeqeaArgs& a, int64_t t, uint64_t g) {
+  const double fit = a.fitness[t / a.Lr];
+  const double fb = a.touch_fbefore[t];
+  if (!(fit > fb)) return;
+  const uint32_t s = a.owner_flats[t];
+  const int64_t loc = slot_local(a, s);
+  const uint8_t mf = a.touch_mutated[t];
+  if (mf & 2) {
+    // qutrit mutation: one improving touch per slot recomputes and writes it
+    if (atomicMax(&a.claim[loc], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
+      LiveSlot v;
+      load_committed(a, loc, v);  // commit writes only theta / qutrit, never slot_max
+      mutate_slot(a, s, g - 1, fb, v);
+      store_committed(a, loc, v);
+    }
+  } else if (mf & 1) {
+    // angle mutation: every improving touch holds the same live angle
+    // (values kernel), so the idempotent store needs no arbitration
+    if (loc < a.Qtloc)
+      a.rot[loc].theta = a.owner_thetas[t];
+    else
+      a.inter[loc - a.Qtloc].theta = a.owner_thetas[t];
+  }
+  atomicMax(reinterpret_cast<unsigned long long*>(smax_ptr(a, loc)),
+            (unsigned long long)__double_as_longlong(fit));
+}
+
 __global__ void __launch_bounds__(kCommitThreads) qeqea_commit_table_kernel(QeqeaArgs a, int64_t t1) {
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t1;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const double fit = a.fitness[t / a.Lr];
-    const double fb = a.touch_fbefore[t];
-    if (!(fit > fb)) continue;
-    const uint32_t s = a.owner_flats[t];
-    const int64_t loc = slot_local(a, s);
-    const uint8_t mf = a.touch_mutated[t];
-    if (mf & 2) {
-      // qutrit mutation: one improving touch per slot recomputes and writes it
-      if (atomicMax(&a.claim[loc], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
-        LiveSlot v;
-        load_committed(a, loc, v);  // commit writes only theta / qutrit, never slot_max
-        mutate_slot(a, s, g - 1, fb, v);
-        store_committed(a, loc, v);
-      }
-    } else if (mf & 1) {
-      // angle mutation: every improving touch holds the same live angle
-      // (values kernel), so the idempotent store needs no arbitration
-      if (loc < a.Qtloc)
-        a.rot[loc].theta = a.owner_thetas[t];
-      else
-        a.inter[loc - a.Qtloc].theta = a.owner_thetas[t];
-    }
-    atomicMax(reinterpret_cast<unsigned long long*>(smax_ptr(a, loc)),
-              (unsigned long long)__double_as_longlong(fit));
-  }
+       t += (int64_t)gridDim.x * blockDim.x)
+    commit_touch(a, t, g);
 }
 
-__global__ void qeqea_advance_kernel(QeqeaArgs a) {
+__device__ __forceinline__ void advance_body(const QeqeaArgs& a) {
   QeqeaDevState* st = a.st;
-  if (st->stop) return;
   st->generation += 1;
   if (st->best_fitness >= a.target_fitness)
     st->stop = 1;
   else if (st->generation >= a.max_generations)
     st->stop = 2;
+}
+
+__global__ void qeqea_advance_kernel(QeqeaArgs a) {
+  if (a.st->stop) return;
+  advance_body(a);
 }
 
 // ---------------------------------------------------------- population ---
@@ -460,6 +493,59 @@ __global__ void __launch_bounds__(kThreadsPerBlock)
   }
 }
 
+// --------------------------------------------------- small populations ---
+
+// Launch-bound populations (C1-C3: P*L of a few hundred touches): n whole
+// generations in one single-block launch, every phase a block-wide loop over
+// the same device bodies the multi-kernel generation uses (identical
+// results), separated by __syncthreads.
+template <int NQ>
+__global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a, int n_gens) {
+  using G = Geo<NQ>;
+  constexpr int kWarps = kRedThreads / 32;
+  __shared__ double2 Ts[G::D * G::D];
+  __shared__ FastChunk sh[kWarps];
+  __shared__ uint64_t blk[kWarps][36];
+  __shared__ double smax[kRedThreads], ssum[kRedThreads];
+  __shared__ int64_t sarg[kRedThreads];
+  __shared__ int s_improved;
+  __shared__ int64_t s_best;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < G::D * G::D; i += kRedThreads) Ts[i] = a.target[i];
+  const int64_t touches = a.P * a.L;
+  for (int it = 0; it < n_gens; ++it) {
+    __syncthreads();
+    if (a.st->stop) return;  // uniform: written by thread 0 before the barrier
+    const uint64_t g = a.st->generation;
+    for (int64_t c = wib; c < a.P; c += kWarps) sample_circuit_warp(a, g, c, a.flats + c * a.L, blk[wib], lane);
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < touches; t += kRedThreads) {
+      uint32_t s;
+      LiveSlot v;
+      if (value_touch_head(a, t, g, s, v)) {
+        double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
+        double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
+        a.owner_codes[t] = measure_code(a, s, g, re, im);
+      }
+    }
+    __syncthreads();
+    fitness_rows<NQ>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, a.fitness, kWarps);
+    __syncthreads();
+    for (int part = 0; part < a.n_parts; ++part) {
+      reduce_partial_body(a, part, smax, ssum, sarg);
+      __syncthreads();
+    }
+    reduce_final_body(a, &s_improved, &s_best);
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < touches; t += kRedThreads) commit_touch(a, t, g);
+    __syncthreads();
+    if (threadIdx.x == 0) advance_body(a);
+  }
+}
+
+// Single-rank populations up to this many touches run qeqea_small_kernel.
+constexpr int64_t kSmallTouches = 1 << 12;
+
 // ------------------------------------------------------------ launchers ---
 
 static int blocks_for(int64_t n, int threads) {
@@ -519,6 +605,22 @@ isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
   const int64_t t1 = a.world * a.S * a.Lr;
   qeqea_commit_table_kernel<<<blocks_for(t1, kCommitThreads), kCommitThreads, 0, s>>>(a, t1);
   qeqea_advance_kernel<<<1, 1, 0, s>>>(a);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
+bool qeqea_small(const QeqeaArgs& a) { return a.world == 1 && a.P * a.L <= kSmallTouches; }
+
+isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s) {
+  switch (a.n) {
+    case 2: qeqea_small_kernel<2><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
+    case 3: qeqea_small_kernel<3><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
+    case 4: qeqea_small_kernel<4><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
+    case 5: qeqea_small_kernel<5><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
+    default:
+      set_error("numberOfWires outside the compiled range 2..5");
+      return ISQ_ERR_UNSUPPORTED;
+  }
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }

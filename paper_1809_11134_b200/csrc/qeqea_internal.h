@@ -12,6 +12,9 @@ isq_status qeqea_launch_values(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_score(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_eval(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s);
+// Small single-rank populations: n generations in one single-block launch.
+bool qeqea_small(const QeqeaArgs& a);
+isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s);
 isq_status qeqea_launch_init(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_pack(const QeqeaArgs& a, double* theta, double* qamp, double* smax,
                              cudaStream_t s);
