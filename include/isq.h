@@ -128,6 +128,18 @@ isq_status isq_qeqea_set_stream(void* handle, void* stream);
  * is 0 (running), 1 (target-reached) or 2 (generation-limit). */
 isq_status isq_qeqea_step(void* handle, int32_t n, isq_generation_record* records,
                           int32_t* n_done, int32_t* stop_reason);
+/* How isq_qeqea_step / isq_ga_step launch their generations (results are
+ * identical in every mode):
+ *   AUTO     FUSED for <= 8 candidates and <= 4096 gate slots, GRAPH for
+ *            <= 2^18 gate slots, else KERNELS
+ *   KERNELS  one launch per kernel per generation
+ *   GRAPH    16-generation CUDA graphs replayed on the handle's stream
+ *   FUSED    n generations in one single-block launch */
+#define ISQ_LAUNCH_AUTO 0
+#define ISQ_LAUNCH_KERNELS 1
+#define ISQ_LAUNCH_GRAPH 2
+#define ISQ_LAUNCH_FUSED 3
+isq_status isq_qeqea_set_launch_mode(void* handle, int32_t mode);
 /*
  * Split-phase generation (population sharding over `world` ranks, one GPU
  * each).  Rank r scores circuits [r*S, (r+1)*S) (S = shard,
@@ -234,6 +246,7 @@ isq_status isq_ga_finish(void* handle);
 isq_status isq_ga_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
                              int32_t* stop_reason, uint64_t* generation, double* best_fitness);
 isq_status isq_ga_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream);
+isq_status isq_ga_set_launch_mode(void* handle, int32_t mode);
 isq_status isq_ga_best(void* handle, uint8_t* codes, double* thetas, double* fitness);
 /* Current genomes (engine.genomes) as P x L codes + angles; set_state injects them. */
 isq_status isq_ga_get_state(void* handle, uint8_t* codes, double* thetas, uint64_t* generation,

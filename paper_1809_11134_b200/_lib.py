@@ -74,6 +74,7 @@ class GaConfigC(ctypes.Structure):
 
 
 MAX_WORLD = 64
+LAUNCH_MODES = {"auto": 0, "kernels": 1, "graph": 2, "fused": 3}
 
 
 class QeqeaExchange(ctypes.Structure):
@@ -111,6 +112,8 @@ SIGNATURES: dict[str, tuple] = {
     "isq_qeqea_finish": (c_i32, [c_vp]),
     "isq_qeqea_prepare": (c_i32, [c_vp]),
     "isq_qeqea_values": (c_i32, [c_vp]),
+    "isq_qeqea_set_launch_mode": (c_i32, [c_vp, c_i32]),
+    "isq_ga_set_launch_mode": (c_i32, [c_vp, c_i32]),
     "isq_qeqea_exchange": (c_i32, [c_vp, c_vp]),
     "isq_qeqea_score": (c_i32, [c_vp]),
     "isq_qeqea_read_batch": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

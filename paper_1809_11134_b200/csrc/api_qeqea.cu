@@ -17,6 +17,7 @@ struct QeqeaHandle {
   GenRecord* h_records = nullptr;  // pinned
   QeqeaDevState* h_state = nullptr;  // pinned
   GenGraph graph;                    // isq_qeqea_step on small populations
+  int launch_mode = ISQ_LAUNCH_AUTO;
 };
 
 static void free_handle(QeqeaHandle* h) {
@@ -313,18 +314,32 @@ isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_re
   isq_status st = isq_qeqea_begin_batch(handle);
   if (st != ISQ_OK) return st;
   const QeqeaArgs& a = h->a;
-  if (qeqea_small(a)) {
+  const int mode = h->launch_mode;
+  if (mode == ISQ_LAUNCH_FUSED || (mode == ISQ_LAUNCH_AUTO && qeqea_small(a))) {
     st = n_generations > 0 ? qeqea_launch_small(a, n_generations, h->stream) : ISQ_OK;
     if (st != ISQ_OK) return st;
     return isq_qeqea_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
   }
-  st = run_generations(h->graph, h->stream, n_generations, graph_generations(a.P * a.L),
+  const int per_graph = mode == ISQ_LAUNCH_KERNELS ? 0
+                        : mode == ISQ_LAUNCH_GRAPH  ? 16
+                                                    : graph_generations(a.P * a.L);
+  st = run_generations(h->graph, h->stream, n_generations, per_graph,
                        [&a](cudaStream_t s) {
                          isq_status r = qeqea_launch_eval(a, s);
                          return r != ISQ_OK ? r : qeqea_launch_finish(a, s);
                        });
   if (st != ISQ_OK) return st;
   return isq_qeqea_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
+}
+
+isq_status isq_qeqea_set_launch_mode(void* handle, int32_t mode) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (mode < ISQ_LAUNCH_AUTO || mode > ISQ_LAUNCH_FUSED) {
+    set_error("unknown launch mode");
+    return ISQ_ERR_CONFIG;
+  }
+  h->launch_mode = mode;
+  return ISQ_OK;
 }
 
 isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len,

@@ -72,16 +72,14 @@ __global__ void __launch_bounds__(kFitThreads, 6) ga_eval_kernel(GaArgs a, int64
 // ---------------------------------------------------------------- reduce ---
 constexpr int kGaRed = 256;
 
-__global__ void __launch_bounds__(kGaRed) ga_reduce_partials(GaArgs a) {
-  if (a.st->stop) return;
-  __shared__ double smax[kGaRed], ssum[kGaRed];
-  __shared__ int64_t sarg[kGaRed];
+__device__ __forceinline__ void ga_reduce_partial_body(const GaArgs& a, int part, double* smax, double* ssum,
+                                                       int64_t* sarg) {
   const int64_t per = (a.P + a.n_parts - 1) / a.n_parts;
-  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t lo = (int64_t)part * per;
   const int64_t hi = min(a.P, lo + per);
   double m = -1.0, sum = 0.0;
   int64_t arg = INT64_MAX;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kGaRed) {
     const double f = a.fitness[i];
     sum += f;
     if (f > m) {
@@ -106,10 +104,17 @@ __global__ void __launch_bounds__(kGaRed) ga_reduce_partials(GaArgs a) {
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    a.part_max[blockIdx.x] = smax[0];
-    a.part_sum[blockIdx.x] = ssum[0];
-    a.part_arg[blockIdx.x] = sarg[0];
+    a.part_max[part] = smax[0];
+    a.part_sum[part] = ssum[0];
+    a.part_arg[part] = sarg[0];
   }
+}
+
+__global__ void __launch_bounds__(kGaRed) ga_reduce_partials(GaArgs a) {
+  if (a.st->stop) return;
+  __shared__ double smax[kGaRed], ssum[kGaRed];
+  __shared__ int64_t sarg[kGaRed];
+  ga_reduce_partial_body(a, blockIdx.x, smax, ssum, sarg);
 }
 
 // numpy's pairwise summation of a contiguous float64 array (np.sum, used by
@@ -143,11 +148,10 @@ __device__ double np_pairwise_sum(const double* a, int64_t n) {
 // Final reduction + best-so-far update (ga.py:171-174) + SUS (ga.py:95-116).
 // SUS is inherently sequential (cumulative sums compared against pointer +=
 // spacing): thread 0 replays it exactly; warp 0 copies the elite genome.
-__global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
-  __shared__ int s_improved;
-  __shared__ int64_t s_elite;
+__device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_improved_p, int64_t* s_elite_p) {
+  int& s_improved = *s_improved_p;
+  int64_t& s_elite = *s_elite_p;
   GaDevState* st = a.st;
-  if (st->stop) return;
   const int cur = ga_cur(a);
   if (threadIdx.x == 0) {
     double m = -1.0, sum = 0.0;
@@ -204,64 +208,113 @@ __global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
+  __shared__ int s_improved;
+  __shared__ int64_t s_elite;
+  if (a.st->stop) return;
+  ga_reduce_sus_body(a, &s_improved, &s_elite);
+}
+
 // ----------------------------------------------------------------- breed ---
 // Child i >= 1 is the (i-1)%2-th child of pair k = (i-1)/2 of parents
 // (parents[2k % P], parents[(2k+1) % P]) (ga.py:177-187); slot 0 is the elite.
+__device__ __forceinline__ void ga_breed_gene(const GaArgs& a, int64_t t, uint64_t g, int cur, int64_t elite) {
+  const int nxt = cur ^ 1;
+  const int64_t i = t / a.L;
+  const int j = (int)(t - i * a.L);
+  if (i == 0) {
+    a.codes[nxt][j] = a.codes[cur][elite * a.L + j];
+    a.thetas[nxt][j] = a.thetas[cur][elite * a.L + j];
+    return;
+  }
+  const int64_t k = (i - 1) >> 1;
+  const bool first = ((i - 1) & 1) == 0;
+  const int64_t pa = a.parents[(2 * k) % a.P], pb = a.parents[(2 * k + 1) % a.P];
+  // two_point_crossover: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
+  int p = 0, q = 0;
+  if (a.L >= 2) {
+    NpStream cs;
+    cs.init(a.seed, DOM_GA_PAIR, g, (uint64_t)k, 0);
+    const int x = (int)cs.integers(a.L + 1), y = (int)cs.integers(a.L + 1);
+    p = x < y ? x : y;
+    q = x < y ? y : x;
+  }
+  const bool inside = j >= p && j < q;
+  const int64_t src = (first != inside) ? pa : pb;  // child a: a outside, b inside
+  int code = a.codes[cur][src * a.L + j];
+  double theta = a.thetas[cur][src * a.L + j];
+  // ga_mutate for this gene (ga.py:126-137)
+  NpStream ms;
+  ms.init(a.seed, DOM_GA_MUT, g, (uint64_t)i, (uint64_t)j);
+  if (ms.random() < a.rate) {
+    if (ms.random() < a.structural) {
+      code = (int)ms.integers(a.ncodes);
+    } else {
+      const double u = ms.uniform(-a.mrange, a.mrange);
+      theta = py_mod(__dadd_rn(theta, u), kTwoPiD);
+    }
+  }
+  a.codes[nxt][i * a.L + j] = (uint8_t)code;
+  a.thetas[nxt][i * a.L + j] = theta;
+}
+
 __global__ void ga_breed_kernel(GaArgs a) {
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
-  const int cur = ga_cur(a), nxt = cur ^ 1;
+  const int cur = ga_cur(a);
   const int64_t total = a.P * a.L;
   const int64_t elite = a.st->elite;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / a.L;
-    const int j = (int)(t - i * a.L);
-    if (i == 0) {
-      a.codes[nxt][j] = a.codes[cur][elite * a.L + j];
-      a.thetas[nxt][j] = a.thetas[cur][elite * a.L + j];
-      continue;
-    }
-    const int64_t k = (i - 1) >> 1;
-    const bool first = ((i - 1) & 1) == 0;
-    const int64_t pa = a.parents[(2 * k) % a.P], pb = a.parents[(2 * k + 1) % a.P];
-    // two_point_crossover: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
-    int p = 0, q = 0;
-    if (a.L >= 2) {
-      NpStream cs;
-      cs.init(a.seed, DOM_GA_PAIR, g, (uint64_t)k, 0);
-      const int x = (int)cs.integers(a.L + 1), y = (int)cs.integers(a.L + 1);
-      p = x < y ? x : y;
-      q = x < y ? y : x;
-    }
-    const bool inside = j >= p && j < q;
-    const int64_t src = (first != inside) ? pa : pb;  // child a: a outside, b inside
-    int code = a.codes[cur][src * a.L + j];
-    double theta = a.thetas[cur][src * a.L + j];
-    // ga_mutate for this gene (ga.py:126-137)
-    NpStream ms;
-    ms.init(a.seed, DOM_GA_MUT, g, (uint64_t)i, (uint64_t)j);
-    if (ms.random() < a.rate) {
-      if (ms.random() < a.structural) {
-        code = (int)ms.integers(a.ncodes);
-      } else {
-        const double u = ms.uniform(-a.mrange, a.mrange);
-        theta = py_mod(__dadd_rn(theta, u), kTwoPiD);
-      }
-    }
-    a.codes[nxt][i * a.L + j] = (uint8_t)code;
-    a.thetas[nxt][i * a.L + j] = theta;
-  }
+       t += (int64_t)gridDim.x * blockDim.x)
+    ga_breed_gene(a, t, g, cur, elite);
 }
 
-__global__ void ga_advance_kernel(GaArgs a) {
+__device__ __forceinline__ void ga_advance_body(const GaArgs& a) {
   GaDevState* st = a.st;
-  if (st->stop) return;
   st->generation += 1;
   if (st->best_fitness >= a.target_fitness)
     st->stop = 1;
   else if (st->generation >= a.max_generations)
     st->stop = 2;
+}
+
+__global__ void ga_advance_kernel(GaArgs a) {
+  if (a.st->stop) return;
+  ga_advance_body(a);
+}
+
+// Launch-bound populations (C2): n whole generations in one single-block
+// launch over the same device bodies as the multi-kernel generation.
+template <int NQ>
+__global__ void __launch_bounds__(kGaRed, 1) ga_small_kernel(GaArgs a, int n_gens) {
+  using G = Geo<NQ>;
+  constexpr int kWarps = kGaRed / 32;
+  __shared__ double2 Ts[G::D * G::D];
+  __shared__ FastChunk sh[kWarps];
+  __shared__ double smax[kGaRed], ssum[kGaRed];
+  __shared__ int64_t sarg[kGaRed];
+  __shared__ int s_improved;
+  __shared__ int64_t s_elite;
+  for (int i = threadIdx.x; i < G::D * G::D; i += kGaRed) Ts[i] = a.target[i];
+  const int64_t genes = a.P * a.L;
+  for (int it = 0; it < n_gens; ++it) {
+    __syncthreads();
+    if (a.st->stop) return;  // uniform: written by thread 0 before the barrier
+    const uint64_t g = a.st->generation;
+    const int cur = ga_cur(a);
+    fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
+    __syncthreads();
+    for (int part = 0; part < a.n_parts; ++part) {
+      ga_reduce_partial_body(a, part, smax, ssum, sarg);
+      __syncthreads();
+    }
+    ga_reduce_sus_body(a, &s_improved, &s_elite);
+    __syncthreads();
+    const int64_t elite = a.st->elite;
+    for (int64_t t = threadIdx.x; t < genes; t += kGaRed) ga_breed_gene(a, t, g, cur, elite);
+    __syncthreads();
+    if (threadIdx.x == 0) ga_advance_body(a);
+  }
 }
 
 // random_genome (ga.py:68-73), one stream per (genome, gene).
@@ -288,6 +341,7 @@ struct GaHandle {
   int64_t shard = 0;
   int max_batch = 0;
   GenGraph graph;  // isq_ga_step on small populations
+  int launch_mode = ISQ_LAUNCH_AUTO;
 };
 
 static void ga_free(GaHandle* h) {
@@ -340,6 +394,26 @@ static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaSt
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;
   }
+}
+
+// Single-block path: one fitness round (P <= 8 warps) and few genes; larger
+// launch-bound populations (C2, P = 50) run faster as a CUDA graph of the
+// multi-kernel generation, whose fitness kernel spreads the circuits over SMs.
+constexpr int64_t kGaSmallGenes = 1 << 12;
+constexpr int64_t kGaSmallPop = kGaRed / 32;
+
+static isq_status ga_launch_small(const GaArgs& a, int n_gens, cudaStream_t s) {
+  switch (a.n) {
+    case 2: ga_small_kernel<2><<<1, kGaRed, 0, s>>>(a, n_gens); break;
+    case 3: ga_small_kernel<3><<<1, kGaRed, 0, s>>>(a, n_gens); break;
+    case 4: ga_small_kernel<4><<<1, kGaRed, 0, s>>>(a, n_gens); break;
+    case 5: ga_small_kernel<5><<<1, kGaRed, 0, s>>>(a, n_gens); break;
+    default:
+      set_error("numberOfWires outside the compiled range 2..5");
+      return ISQ_ERR_UNSUPPORTED;
+  }
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
 }
 
 static isq_status ga_launch_finish(const GaArgs& a, cudaStream_t s) {
@@ -512,12 +586,32 @@ isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, 
   isq_status st = isq_ga_begin_batch(handle);
   if (st != ISQ_OK) return st;
   const GaArgs& a = h->a;
-  st = run_generations(h->graph, h->stream, n, graph_generations(a.P * a.L), [&a](cudaStream_t s) {
+  const int mode = h->launch_mode;
+  if (mode == ISQ_LAUNCH_FUSED ||
+      (mode == ISQ_LAUNCH_AUTO && a.P <= kGaSmallPop && a.P * a.L <= kGaSmallGenes)) {
+    st = n > 0 ? ga_launch_small(a, n, h->stream) : ISQ_OK;
+    if (st != ISQ_OK) return st;
+    return isq_ga_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
+  }
+  const int per_graph = mode == ISQ_LAUNCH_KERNELS ? 0
+                        : mode == ISQ_LAUNCH_GRAPH  ? 16
+                                                    : graph_generations(a.P * a.L);
+  st = run_generations(h->graph, h->stream, n, per_graph, [&a](cudaStream_t s) {
     isq_status r = ga_launch_eval(a, 0, a.P, s);
     return r != ISQ_OK ? r : ga_launch_finish(a, s);
   });
   if (st != ISQ_OK) return st;
   return isq_ga_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
+}
+
+isq_status isq_ga_set_launch_mode(void* handle, int32_t mode) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  if (mode < ISQ_LAUNCH_AUTO || mode > ISQ_LAUNCH_FUSED) {
+    set_error("unknown launch mode");
+    return ISQ_ERR_CONFIG;
+  }
+  h->launch_mode = mode;
+  return ISQ_OK;
 }
 
 isq_status isq_ga_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream) {

@@ -543,8 +543,11 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
   }
 }
 
-// Single-rank populations up to this many touches run qeqea_small_kernel.
+// Single-rank populations of at most one fitness round (P <= 8 warps) and this
+// many touches run qeqea_small_kernel; larger launch-bound ones run as a CUDA
+// graph of the multi-kernel generation (its fitness kernel spreads over SMs).
 constexpr int64_t kSmallTouches = 1 << 12;
+constexpr int64_t kSmallPop = kRedThreads / 32;
 
 // ------------------------------------------------------------ launchers ---
 
@@ -609,7 +612,9 @@ isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
   return ISQ_OK;
 }
 
-bool qeqea_small(const QeqeaArgs& a) { return a.world == 1 && a.P * a.L <= kSmallTouches; }
+bool qeqea_small(const QeqeaArgs& a) {
+  return a.world == 1 && a.P <= kSmallPop && a.P * a.L <= kSmallTouches;
+}
 
 isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s) {
   switch (a.n) {

@@ -308,6 +308,14 @@ class QeqeaEngine:
             remaining -= k
         return np.concatenate(out) if out else np.zeros(0, dtype=_lib.GEN_RECORD)
 
+    def set_launch_mode(self, mode: str) -> None:
+        """How steps() launches generations: "auto" (default), "kernels",
+        "graph" (16-generation CUDA graphs) or "fused" (one single-block
+        launch); every mode gives identical results (include/isq.h)."""
+        if mode not in _lib.LAUNCH_MODES:
+            raise ConfigurationError(f"launch mode must be one of {sorted(_lib.LAUNCH_MODES)}")
+        _lib.check(self._lib.isq_qeqea_set_launch_mode(self._handle(), _lib.LAUNCH_MODES[mode]))
+
     def _absorb(self, rec: np.ndarray, stop: int):
         if rec.size:
             self.generation += int(rec.size)

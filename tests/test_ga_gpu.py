@@ -26,9 +26,11 @@ def _engine(g):
 
 
 @pytest.mark.parametrize("name", ["cnot", "toffoli_c2", "odd13"])
-def test_ga_trajectory_matches_reference(name):
+@pytest.mark.parametrize("mode", ["auto", "kernels", "fused"])
+def test_ga_trajectory_matches_reference(name, mode):
     g = golden(f"traj_ga_{name}")
     eng = _engine(g)
+    eng.set_launch_mode(mode)
     codes, thetas = eng.genome_arrays()
     assert np.array_equal(codes, g["init_codes"])
     assert np.array_equal(thetas, g["init_thetas"])
@@ -96,3 +98,18 @@ def test_ga_population_and_elitism():
     assert all(b >= a - 1e-12 for a, b in zip(bests, bests[1:]))
     assert eng.stop_reason == "generation-limit"
     assert len(eng.gate_choices if hasattr(eng, "gate_choices") else cfg.gate_choices) == 7
+
+
+@pytest.mark.parametrize("mode", ["auto", "kernels", "graph", "fused"])
+def test_ga_batched_steps_equal_single_steps(mode):
+    g = golden("traj_ga_toffoli_c2")
+    a, b = _engine(g), _engine(g)
+    a.set_launch_mode("kernels")
+    b.set_launch_mode(mode)
+    ra = [a.step() for _ in range(int(g["gens"]))]
+    rb = b.steps(int(g["gens"]))
+    assert [x[0] for x in ra] == list(rb["gen_best"])
+    assert [x[1] for x in ra] == list(rb["gen_mean"])
+    ca, ta = a.genome_arrays()
+    cb, tb = b.genome_arrays()
+    assert np.array_equal(ca, cb) and np.array_equal(ta, tb)

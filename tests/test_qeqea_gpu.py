@@ -33,9 +33,11 @@ def _engine_from_golden(g, **kw):
 
 
 @pytest.mark.parametrize("name", TRAJ)
-def test_trajectory_matches_reference(name):
+@pytest.mark.parametrize("mode", ["auto", "kernels", "fused"])
+def test_trajectory_matches_reference(name, mode):
     g = golden(f"traj_qeqea_{name}")
     eng = _engine_from_golden(g)
+    eng.set_launch_mode(mode)
     gen = 0
     recs = []
     while not eng.done:
@@ -61,15 +63,22 @@ def test_trajectory_matches_reference(name):
     np.testing.assert_allclose(bt, g["best_thetas"], rtol=1e-11, atol=1e-12)
 
 
-def test_batched_steps_equal_single_steps():
+@pytest.mark.parametrize("mode", ["auto", "kernels", "graph", "fused"])
+def test_batched_steps_equal_single_steps(mode):
+    """steps(n) in every launch mode (CUDA graphs of 16 generations, one fused
+    launch, ...) equals n single steps on the plain kernels, bit for bit."""
     g = golden("traj_qeqea_toffoli_c1")
     a = _engine_from_golden(g)
     b = _engine_from_golden(g)
+    a.set_launch_mode("kernels")
+    b.set_launch_mode(mode)
     ra = [a.step() for _ in range(40)]
     rb = b.steps(40)
     assert [x[0] for x in ra] == list(rb["gen_best"])
     assert [x[1] for x in ra] == list(rb["gen_mean"])
     assert np.array_equal(a.pop.thetas, b.pop.thetas)
+    assert np.array_equal(a.table.slot_max, b.table.slot_max)
+    assert [x.to_dict() for x in a.best_gates] == [x.to_dict() for x in b.best_gates]
 
 
 def test_device_init_matches_oracle_init():
