@@ -308,9 +308,39 @@ def run_ours(args):
                            f"OPENBLAS_NUM_THREADS=1"),
                 "parity_max_rel_err_vs_gpu": float(rel.max()),
             }
+    eng.close()
+    # the fp32 variant of the fitness kernel (include/isq.h ISQ_PRECISION_FP32):
+    # a full C5 generation with fp32 fitness, and its error on the e2e circuits
+    if world == 1 and not args.skip_fp32:
+        fe = QeqeaEngine(cfg, TargetSpec("haar32", N, T), seed=2024, device=local, precision="fp32",
+                         max_batch=max(args.steps + args.warmup, 1) + 1)
+        with torch.cuda.stream(stream):
+            fops = DeviceQeqeaOps(fe)
+            fops.begin_batch()
+            for _ in range(args.warmup):
+                fops.generation(None)
+            fev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(args.steps)]
+            torch.cuda.synchronize()
+            start.record(stream)
+            for i in range(args.steps):
+                fops.generation(None, marks=fev[i])
+            end.record(stream)
+            torch.cuda.synchronize()
+        fms = start.elapsed_time(end)
+        fit_ms = sum(e[1].elapsed_time(e[2]) for e in fev) / args.steps
+        var = {"value": P * args.steps / (fms * 1e-3), "unit": "evals/s", "ms_per_step": fms / args.steps,
+               "fitness_kernel_ms": fit_ms,
+               "bound": "|fit32 - fit64| <= 1e-4 |fit64| + 1e-6 (tests/test_fitness_gpu.py)"}
+        fe.close()
+        if not args.skip_e2e:
+            h32 = np.empty_like(hf)
+            _lib.check(lib.isq_fitness_batch_ex(N, L, n_mine, _lib.ptr(hc), _lib.ptr(ht), _lib.ptr(Tc),
+                                                _lib.ptr(h32), local, _lib.PRECISIONS["fp32"]))
+            var["max_abs_err_vs_fp64"] = float(np.abs(h32 - hf).max())
+            var["max_rel_err_vs_fp64"] = float((np.abs(h32 - hf) / np.maximum(np.abs(hf), 1e-300)).max())
+        out["fp32_variant"] = var
     if rank == 0:
         emit(out)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -323,6 +353,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-fp32", action="store_true")
     ap.add_argument("--cpu-per-worker", type=int, default=400)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -67,6 +67,23 @@ isq_status isq_fitness_batch_device(int32_t n, int32_t length, int64_t count,
                                     double* unitary_dev, void* stream);
 
 /*
+ * Arithmetic of the fitness kernel.  FP64 meets the north-star bound
+ * (|dfitness| <= 1e-9 |fitness| + 1e-12 against the reference); FP32 keeps the
+ * composed unitary in single precision (gate parameters and the overlap
+ * accumulate in double): |dfitness| <= 1e-4 |fitness| + 1e-6, about 1.5x the
+ * throughput.  Composition (unitary_out) is always FP64.
+ */
+#define ISQ_PRECISION_FP64 0
+#define ISQ_PRECISION_FP32 1
+isq_status isq_fitness_batch_ex(int32_t n, int32_t length, int64_t count, const uint8_t* codes,
+                                const double* thetas, const double* target, double* fitness_out,
+                                int32_t device, int32_t precision);
+isq_status isq_fitness_batch_device_ex(int32_t n, int32_t length, int64_t count,
+                                       const uint8_t* codes_dev, const double* thetas_dev,
+                                       const double* target_dev, double* fitness_dev,
+                                       int32_t precision, void* stream);
+
+/*
  * fitness_value(S_c, T) for `count` explicit dim x dim matrices S (host,
  * count*2*dim*dim doubles) against one target T.  Replaces fitness.py:36-49
  * when the caller already holds a matrix.  Synchronous.
@@ -102,7 +119,7 @@ typedef struct isq_qeqea_config {
   double target_fitness;            /* default 0.999                         */
   uint64_t seed;
   int32_t world;                    /* number of ranks sharing the population */
-  int32_t reserved;
+  int32_t precision;                /* ISQ_PRECISION_FP64 (0) or _FP32 (1): fitness arithmetic */
 } isq_qeqea_config;
 
 typedef struct isq_generation_record {
@@ -232,6 +249,8 @@ typedef struct isq_ga_config {
   uint64_t seed;
   int32_t rank;
   int32_t world;
+  int32_t precision;         /* ISQ_PRECISION_FP64 (0) or _FP32 (1)        */
+  int32_t reserved;
 } isq_ga_config;
 
 isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t device,

@@ -53,7 +53,7 @@ class QeqeaConfig(ctypes.Structure):
         ("target_fitness", c_dbl),
         ("seed", c_u64),
         ("world", c_i32),
-        ("reserved", c_i32),
+        ("precision", c_i32),
     ]
 
 
@@ -70,11 +70,14 @@ class GaConfigC(ctypes.Structure):
         ("seed", c_u64),
         ("rank", c_i32),
         ("world", c_i32),
+        ("precision", c_i32),
+        ("reserved", c_i32),
     ]
 
 
 MAX_WORLD = 64
 LAUNCH_MODES = {"auto": 0, "kernels": 1, "graph": 2, "fused": 3}
+PRECISIONS = {"fp64": 0, "fp32": 1}
 
 
 class QeqeaExchange(ctypes.Structure):
@@ -142,6 +145,8 @@ SIGNATURES: dict[str, tuple] = {
     "isq_abi_version": (c_i32, []),
     "isq_fitness_batch": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),
     "isq_fitness_batch_device": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "isq_fitness_batch_ex": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32]),
+    "isq_fitness_batch_device_ex": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "isq_philox_block": (None, [c_u64, c_u64, c_u64, c_u64, c_u64, c_u64, c_vp]),
     "isq_fma_peak": (c_i32, [c_i32, c_i32, c_vp]),
     "isq_fitness_of_unitaries": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_i32]),

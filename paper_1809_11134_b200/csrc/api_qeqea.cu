@@ -80,6 +80,8 @@ static isq_status validate(const isq_qeqea_config* c) {
   }
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad("invalid rank/world");
   if (c->world > kMaxWorld) return bad("world exceeds " + std::to_string(kMaxWorld) + " ranks");
+  if (c->precision != ISQ_PRECISION_FP64 && c->precision != ISQ_PRECISION_FP32)
+    return bad("precision must be ISQ_PRECISION_FP64 or ISQ_PRECISION_FP32");
   if (c->world > c->size_of_individual)
     return bad("population sharding needs sizeOfIndividual >= world (each rank owns positions)");
   return ISQ_OK;
@@ -125,6 +127,7 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   a.n_meas = cfg->n_meas;
   a.max_generations = (uint64_t)cfg->max_generations;
   a.seed = cfg->seed;
+  a.precision = cfg->precision;
   a.rec_cap = h->max_batch;
   h->shard = (a.P + h->world - 1) / h->world;
   // sharding (engine_common.cuh QeqeaArgs): circuits [c0, c0 + S), positions [p_lo, p_lo + Lr)

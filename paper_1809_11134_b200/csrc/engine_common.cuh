@@ -73,6 +73,7 @@ struct QeqeaArgs {
   int n_meas;
   uint64_t max_generations;
   uint64_t seed;
+  int precision;   // fitness arithmetic: ISQ_PRECISION_FP64 / _FP32
   // sharding
   int world, rank;
   int64_t S;       // circuits per rank (padded: world * S >= P)

@@ -32,37 +32,57 @@
 
 namespace isq {
 
-// Per-warp shared scratch for one 32-gate chunk.
-struct FastChunk {
-  double2 cs2[32][2];  // diag: {(1, 0), (cos th, sin th)}; rotation: {(C = cos a, 0), (p, q)}
+template <class R>
+struct Cplx;
+template <>
+struct Cplx<double> {
+  using T = double2;
+  static __device__ __forceinline__ T make(double a, double b) { return make_double2(a, b); }
+};
+template <>
+struct Cplx<float> {
+  using T = float2;
+  static __device__ __forceinline__ T make(float a, float b) { return make_float2(a, b); }
+};
+
+// Per-warp shared scratch for one 32-gate chunk (R: arithmetic type of the
+// state, double or the fp32 variant's float).
+template <class R>
+struct FastChunkT {
+  using R2 = typename Cplx<R>::T;
+  R2 cs2[32][2];       // diag: {(1, 0), (cos th, sin th)}; rotation: {(C = cos a, 0), (p, q)}
   int dmask[32];       // diag: row mask whose parity picks up e^{i th}; 0 for rotations
   int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit
-  double2 fac[32];     // flush factors / final row weights, indexed by physical row
+  R2 fac[32];          // flush factors / final row weights, indexed by physical row
   double nth[32];      // next chunk's angles / codes, staged by cp.async (no registers held)
   uint32_t ncode[8];
 };
+using FastChunk = FastChunkT<double>;
 
 enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
 
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
 
-template <int NQ>
+template <int NQ, class R = double>
 struct FastEval {
   using G = Geo<NQ>;
-  WarpUnitary<NQ> st;
-  double wr, wi;  // pending phase factor e^{i phi} of physical row `lane` (lane < D)
+  using R2 = typename Cplx<R>::T;
+  using Chunk = FastChunkT<R>;
+  WarpUnitary<NQ, R> st;
+  R wr, wi;  // pending phase factor e^{i phi} of physical row `lane` (lane < D)
 
   __device__ __forceinline__ void begin(int lane) {
     st.set_identity(lane);
-    wr = 1.0;
-    wi = 0.0;
+    wr = R(1);
+    wi = R(0);
   }
 
   // Lane-parallel gate preparation for one position (one sincos call site
   // for every gate type, so a chunk pays for it once).
+  // Gate parameters are computed in fp64 for both arithmetic types.
   __device__ __forceinline__ static void prepare(int code, double theta, int& info, int& dmask,
-                                                 double2& e0, double2& e1) {
+                                                 R2& e0, R2& e1) {
     int b = -1, type = GT_DIAG, mask;
     if (code < 3 * NQ) {
       const int w0 = code / 3, axis = code - 3 * w0;
@@ -94,24 +114,24 @@ struct FastEval {
     if (b >= 0) {
       info = type | (b << 8);
       dmask = 0;
-      e0 = make_double2(fma(cs, cs, -sn * sn), 0.0);
-      e1 = make_double2(-sn / cs, 2.0 * sn * cs);
+      e0 = Cplx<R>::make(R(fma(cs, cs, -sn * sn)), R(0));
+      e1 = Cplx<R>::make(R(-sn / cs), R(2.0 * sn * cs));
     } else {
       info = GT_DIAG;
       dmask = mask;
-      e0 = make_double2(1.0, 0.0);
-      e1 = make_double2(cs, sn);
+      e0 = Cplx<R>::make(R(1), R(0));
+      e1 = Cplx<R>::make(R(cs), R(sn));
     }
   }
 
   // Multiply the register rows with bit B set by fac[row] (flush of pending deltas).
   template <int B>
-  __device__ __forceinline__ void flush_bit(const double2* fac, int lane) {
+  __device__ __forceinline__ void flush_bit(const R2* fac, int lane) {
     const int h = (lane >> NQ) & (G::LPC - 1);
 #pragma unroll
     for (int r = 0; r < G::E; ++r) {
       if (B < G::EB && !(r & (1 << B))) continue;
-      const double2 f = fac[h * G::E + r];
+      const R2 f = fac[h * G::E + r];
       st.cmul(r, f.x, f.y);
     }
   }
@@ -121,7 +141,7 @@ struct FastEval {
   // is rotated, so the compiler can overlap one pair's flush with another's
   // lifting.  Lane bits (n < 5) flush all rows of the upper lanes, then rotate.
   template <int B>
-  __device__ __forceinline__ void flush_lift(const double2* fac, double p, double q, double C, int lane) {
+  __device__ __forceinline__ void flush_lift(const R2* fac, R p, R q, R C, int lane) {
     if constexpr (B < G::EB) {
       constexpr int m = 1 << B;
       const int h = (lane >> NQ) & (G::LPC - 1);
@@ -129,7 +149,7 @@ struct FastEval {
       for (int r = 0; r < G::E; ++r) {
         if (r & m) continue;
         const int r1 = r | m;
-        const double2 f = fac[h * G::E + r1];
+        const R2 f = fac[h * G::E + r1];
         st.cmul(r1, f.x, f.y);
         st.re[r] = fma(p, st.im[r1], st.re[r]);
         st.im[r1] = fma(q, st.re[r], st.im[r1]);
@@ -144,8 +164,7 @@ struct FastEval {
     }
   }
 
-  __device__ __forceinline__ void flush_rotate(int b, const double2* fac, double p, double q, double C,
-                                               int lane) {
+  __device__ __forceinline__ void flush_rotate(int b, const R2* fac, R p, R q, R C, int lane) {
     switch (b) {
       case 0: flush_lift<0>(fac, p, q, C, lane); break;
       case 1: if constexpr (NQ > 1) flush_lift<1>(fac, p, q, C, lane); break;
@@ -159,11 +178,11 @@ struct FastEval {
   // Pending phase of this lane's row times the diagonal gates [q, qe) of the
   // chunk (all of them diagonal): branch-free, one predicated complex
   // multiply per gate.
-  __device__ __forceinline__ void diag_run(int q, int qe, const FastChunk& sm, int row) {
+  __device__ __forceinline__ void diag_run(int q, int qe, const Chunk& sm, int row) {
 #pragma unroll 2
     for (; q < qe; ++q) {
-      const double2 e = sm.cs2[q][__popc(row & sm.dmask[q]) & 1];
-      const double t = wr * e.y;
+      const R2 e = sm.cs2[q][__popc(row & sm.dmask[q]) & 1];
+      const R t = wr * e.y;
       wr = fma(wr, e.x, -wi * e.y);
       wi = fma(wi, e.x, t);
     }
@@ -173,9 +192,9 @@ struct FastEval {
   // The rotation positions are found with one ballot; the diagonal runs
   // between them touch only the pending phase (diag_run), the rotations
   // flush the non-commuting part of it and rotate the register state.
-  __device__ __forceinline__ void chunk(int code, double theta, int nq, FastChunk& sm, int lane) {
+  __device__ __forceinline__ void chunk(int code, double theta, int nq, Chunk& sm, int lane) {
     int info = GT_DIAG, dmask = 0;  // lanes past the end: neutral diagonal, empty mask
-    double2 e0 = make_double2(1.0, 0.0), e1 = e0;
+    R2 e0 = Cplx<R>::make(R(1), R(0)), e1 = e0;
     if (lane < nq) prepare(code, theta, info, dmask, e0, e1);
     sm.info[lane] = info;
     sm.dmask[lane] = dmask;
@@ -196,29 +215,29 @@ struct FastEval {
       const int m = 1 << b;
       const bool ry = (inf & 3) == GT_RY;
       if (ry && (row & m)) {  // S^dagger: rows with the wire bit set pick up -i
-        const double t = wr;
+        const R t = wr;
         wr = wi;
         wi = -t;
       }
       // flush factor of the rows with bit b set: w_r * conj(w_{r^m}) (1 elsewhere);
       // those rows then carry the phase of their partner, so it commutes with Rx
-      const double orr = __shfl_xor_sync(0xffffffffu, wr, m);
-      const double ori = __shfl_xor_sync(0xffffffffu, wi, m);
-      double fr = 1.0, fi = 0.0;
+      const R orr = __shfl_xor_sync(0xffffffffu, wr, m);
+      const R ori = __shfl_xor_sync(0xffffffffu, wi, m);
+      R fr = R(1), fi = R(0);
       if (row & m) {
         fr = fma(wr, orr, wi * ori);
         fi = fma(wi, orr, -wr * ori);
         wr = orr;
         wi = ori;
       }
-      sm.fac[lane] = make_double2(fr, fi);
-      const double2 pq = sm.cs2[qr][1];
-      const double C = sm.cs2[qr][0].x;
+      sm.fac[lane] = Cplx<R>::make(fr, fi);
+      const R2 pq = sm.cs2[qr][1];
+      const R C = sm.cs2[qr][0].x;
       __syncwarp();
       flush_rotate(b, sm.fac, pq.x, pq.y, C, lane);
       __syncwarp();
       if (ry && (row & m)) {  // S: rows with the wire bit set pick up +i
-        const double t = wr;
+        const R t = wr;
         wr = -wi;
         wi = t;
       }
@@ -227,8 +246,9 @@ struct FastEval {
   }
 
   // Fitness from the final state (fitness.py:36-49).
-  __device__ __forceinline__ double finish(const double2* __restrict__ T, FastChunk& sm, int lane) {
-    if (lane < G::D) sm.fac[lane] = make_double2(wr, -wi);  // e^{-i phi}
+  // The overlap is accumulated in fp64 for both arithmetic types.
+  __device__ __forceinline__ double finish(const double2* __restrict__ T, Chunk& sm, int lane) {
+    if (lane < G::D) sm.fac[lane] = Cplx<R>::make(wr, -wi);  // e^{-i phi}
     __syncwarp();
     const int j = lane & (G::D - 1);
     const int h = (lane >> NQ) & (G::LPC - 1);
@@ -237,12 +257,13 @@ struct FastEval {
     for (int r = 0; r < G::E; ++r) {
       const int k = h * G::E + r;
       const double2 t = T[k * G::D + j];
-      const double2 w = sm.fac[k];
+      const R2 wf = sm.fac[k];
+      const double wx = wf.x, wy = wf.y, xr = st.re[r], xi = st.im[r];
       // p = conj(x) * t ; acc += w * p
-      const double pr = fma(st.re[r], t.x, st.im[r] * t.y);
-      const double pi = fma(st.re[r], t.y, -st.im[r] * t.x);
-      ar = fma(w.x, pr, fma(-w.y, pi, ar));
-      ai = fma(w.x, pi, fma(w.y, pr, ai));
+      const double pr = fma(xr, t.x, xi * t.y);
+      const double pi = fma(xr, t.y, -xi * t.x);
+      ar = fma(wx, pr, fma(-wy, pi, ar));
+      ai = fma(wx, pi, fma(wy, pr, ai));
     }
 #pragma unroll
     for (int off = G::ACTIVE / 2; off >= 1; off >>= 1) {
@@ -265,7 +286,8 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes
 // Stage the (code, theta) row slice [nb, nb + 32) of circuit nc in shared
 // memory with cp.async, so the prefetch holds no registers (a register
 // prefetch was spilled and its store waited on the load right away).
-__device__ __forceinline__ void stage_chunk(FastChunk& sm, int64_t count, int L, const uint8_t* codes,
+template <class Chunk>
+__device__ __forceinline__ void stage_chunk(Chunk& sm, int64_t count, int L, const uint8_t* codes,
                                             const double* thetas, int64_t nc, int nb, int lane) {
   if (nc >= count) return;
   const int64_t row = nc * (int64_t)L + nb;
@@ -281,19 +303,19 @@ __device__ __forceinline__ void stage_chunk(FastChunk& sm, int64_t count, int L,
 
 // Grid-stride body shared by the explicit-gate fitness kernels: warp per
 // circuit over circuits [0, count) of (codes, thetas) rows of length L.
-template <int NQ>
+template <int NQ, class R = double>
 __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t* __restrict__ codes,
                                              const double* __restrict__ thetas,
-                                             const double2* __restrict__ Ts, FastChunk* sh,
+                                             const double2* __restrict__ Ts, FastChunkT<R>* sh,
                                              double* __restrict__ fitness, int warps_per_block) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  FastChunk& cs = sh[wib];
+  FastChunkT<R>& cs = sh[wib];
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
   int64_t c = (int64_t)blockIdx.x * warps_per_block + wib;
   stage_chunk(cs, count, L, codes, thetas, c, 0, lane);
   for (; c < count; c += nwarps) {
-    FastEval<NQ> ev;
+    FastEval<NQ, R> ev;
     ev.begin(lane);
     for (int base = 0; base < L; base += 32) {
       const int nq = min(32, L - base);

@@ -103,9 +103,9 @@ static BatchContext* batch_context(int device) {
   return ctx[device];
 }
 
-isq_status isq_fitness_batch(int32_t n, int32_t length, int64_t count, const uint8_t* codes,
-                             const double* thetas, const double* target, double* fitness_out,
-                             double* unitary_out, int32_t device) {
+static isq_status fitness_batch_host(int32_t n, int32_t length, int64_t count, const uint8_t* codes,
+                                     const double* thetas, const double* target, double* fitness_out,
+                                     double* unitary_out, int32_t device, int32_t precision) {
   isq_status st = check_shape(n, length, count);
   if (st != ISQ_OK) return st;
   const int64_t total = count * (int64_t)length;
@@ -179,13 +179,46 @@ isq_status isq_fitness_batch(int32_t n, int32_t length, int64_t count, const uin
     ISQ_CUDA_TRY(cudaEventRecord(c->loaded[b], c->copy));
     ISQ_CUDA_TRY(cudaStreamWaitEvent(c->comp, c->loaded[b], 0));
     st = launch_fitness_batch(n, length, m, c->codes[b], c->thetas[b], c->target, c->fit[b],
-                              nullptr, c->comp);
+                              nullptr, c->comp, precision);
     if (st != ISQ_OK) return st;
     ISQ_CUDA_TRY(cudaMemcpyAsync(fitness_out + off, c->fit[b], m * 8, cudaMemcpyDeviceToHost, c->comp));
     ISQ_CUDA_TRY(cudaEventRecord(c->done[b], c->comp));
   }
   ISQ_CUDA_TRY(cudaStreamSynchronize(c->comp));
   return ISQ_OK;
+}
+
+static isq_status check_precision(int32_t precision) {
+  if (precision == ISQ_PRECISION_FP64 || precision == ISQ_PRECISION_FP32) return ISQ_OK;
+  set_error("precision must be ISQ_PRECISION_FP64 or ISQ_PRECISION_FP32");
+  return ISQ_ERR_CONFIG;
+}
+
+isq_status isq_fitness_batch(int32_t n, int32_t length, int64_t count, const uint8_t* codes,
+                             const double* thetas, const double* target, double* fitness_out,
+                             double* unitary_out, int32_t device) {
+  return fitness_batch_host(n, length, count, codes, thetas, target, fitness_out, unitary_out, device,
+                            ISQ_PRECISION_FP64);
+}
+
+isq_status isq_fitness_batch_ex(int32_t n, int32_t length, int64_t count, const uint8_t* codes,
+                                const double* thetas, const double* target, double* fitness_out,
+                                int32_t device, int32_t precision) {
+  isq_status st = check_precision(precision);
+  if (st != ISQ_OK) return st;
+  return fitness_batch_host(n, length, count, codes, thetas, target, fitness_out, nullptr, device,
+                            precision);
+}
+
+isq_status isq_fitness_batch_device_ex(int32_t n, int32_t length, int64_t count,
+                                       const uint8_t* codes_dev, const double* thetas_dev,
+                                       const double* target_dev, double* fitness_dev,
+                                       int32_t precision, void* stream) {
+  isq_status st = check_shape(n, length, count);
+  if (st == ISQ_OK) st = check_precision(precision);
+  if (st != ISQ_OK) return st;
+  return launch_fitness_batch(n, length, count, codes_dev, thetas_dev, target_dev, fitness_dev,
+                              nullptr, (cudaStream_t)stream, precision);
 }
 
 isq_status isq_fitness_of_unitaries(int64_t dim, int64_t count, const double* unitaries,

@@ -17,19 +17,24 @@ struct ChunkShared {
 // (<= 168 registers) gives 3 warps per scheduler for the n = 5
 // register-resident state (measured: 2 warps per scheduler at 244 registers
 // is 11 % slower).
-template <int NQ, int MINB>
+template <int NQ, int MINB, class R>
 __global__ void __launch_bounds__(kFitThreads, MINB)
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
                         double* __restrict__ fitness, const int32_t* __restrict__ stop) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kFitWarps];
+  __shared__ FastChunkT<R> sh[kFitWarps];
   if (stop != nullptr && *stop) return;
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
   __syncthreads();
-  fitness_rows<NQ>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps);
+  fitness_rows<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps);
 }
+
+// fp32 variant: the column of S in 64 float registers: 8 resident 2-warp
+// blocks per SM (<= 128 registers, 4 warps per scheduler).
+constexpr int kFitMinBlocks64 = 6;
+constexpr int kFitMinBlocks32 = 8;
 
 // Composition with the exact global phase (compose_gates readout) + fitness.
 template <int NQ>
@@ -165,14 +170,6 @@ template <int NQ>
 static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const double* thetas,
                             const double* target, double* fitness, double* unitary,
                             cudaStream_t stream) {
-  if (unitary == nullptr) {
-    const void* k = (const void*)fitness_fast_kernel<NQ, 6>;
-    const int grid = persistent_grid(k, 0, count, kFitWarps);
-    fitness_fast_kernel<NQ, 6><<<grid, kFitThreads, 0, stream>>>(
-        count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, nullptr);
-    ISQ_CUDA_TRY(cudaGetLastError());
-    return ISQ_OK;
-  }
   const void* k = (const void*)compose_kernel<NQ>;
   const int grid = persistent_grid(k, 0, count);
   compose_kernel<NQ><<<grid, kThreadsPerBlock, 0, stream>>>(
@@ -182,30 +179,41 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
   return ISQ_OK;
 }
 
-template <int NQ, int MINB>
-static isq_status launch_fast_stoppable(int L, int64_t count, const uint8_t* codes,
-                                        const double* thetas, const double* target, double* fitness,
-                                        const int32_t* stop, int blocks_per_sm, cudaStream_t stream) {
-  const void* k = (const void*)fitness_fast_kernel<NQ, MINB>;
+template <int NQ, int MINB, class R>
+static isq_status launch_fast(int L, int64_t count, const uint8_t* codes, const double* thetas,
+                              const double* target, double* fitness, const int32_t* stop,
+                              int blocks_per_sm, cudaStream_t stream) {
+  const void* k = (const void*)fitness_fast_kernel<NQ, MINB, R>;
   int grid = persistent_grid(k, 0, count, kFitWarps);
   if (blocks_per_sm > 0 && grid > num_sms() * blocks_per_sm) grid = num_sms() * blocks_per_sm;
-  fitness_fast_kernel<NQ, MINB><<<grid, kFitThreads, 0, stream>>>(
+  fitness_fast_kernel<NQ, MINB, R><<<grid, kFitThreads, 0, stream>>>(
       count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
 
+template <int NQ>
+static isq_status launch_fast_prec(int L, int64_t count, const uint8_t* codes, const double* thetas,
+                                   const double* target, double* fitness, const int32_t* stop,
+                                   int blocks_per_sm, int precision, cudaStream_t stream) {
+  if (precision == ISQ_PRECISION_FP32)
+    return launch_fast<NQ, kFitMinBlocks32, float>(L, count, codes, thetas, target, fitness, stop,
+                                                    blocks_per_sm, stream);
+  return launch_fast<NQ, kFitMinBlocks64, double>(L, count, codes, thetas, target, fitness, stop,
+                                                  blocks_per_sm, stream);
+}
+
 isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
                                           const double* thetas, const double* target,
                                           double* fitness, const int32_t* stop,
-                                          cudaStream_t stream, int blocks_per_sm) {
+                                          cudaStream_t stream, int blocks_per_sm, int precision) {
   if (count <= 0) return ISQ_OK;
-  const int b = blocks_per_sm;
+  const int b = blocks_per_sm, p = precision;
   switch (n) {
-    case 2: return launch_fast_stoppable<2, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
-    case 3: return launch_fast_stoppable<3, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
-    case 4: return launch_fast_stoppable<4, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
-    case 5: return launch_fast_stoppable<5, 6>(L, count, codes, thetas, target, fitness, stop, b, stream);
+    case 2: return launch_fast_prec<2>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
+    case 3: return launch_fast_prec<3>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
+    case 4: return launch_fast_prec<4>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
+    case 5: return launch_fast_prec<5>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
     default:
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;
@@ -214,9 +222,12 @@ isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uin
 
 isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* codes,
                                 const double* thetas, const double* target, double* fitness,
-                                double* unitary, cudaStream_t stream) {
+                                double* unitary, cudaStream_t stream, int precision) {
   if (count <= 0) return ISQ_OK;
-  switch (n) {
+  if (unitary == nullptr)
+    return launch_fitness_batch_stoppable(n, L, count, codes, thetas, target, fitness, nullptr, stream,
+                                          0, precision);
+  switch (n) {  // composition readout: always fp64
     case 2: return launch_nq<2>(L, count, codes, thetas, target, fitness, unitary, stream);
     case 3: return launch_nq<3>(L, count, codes, thetas, target, fitness, unitary, stream);
     case 4: return launch_nq<4>(L, count, codes, thetas, target, fitness, unitary, stream);

@@ -51,22 +51,23 @@ struct GaArgs {
   double* part_sum;
   int64_t* part_arg;
   int n_parts;
+  int precision;  // fitness arithmetic: ISQ_PRECISION_FP64 / _FP32
 };
 
 __device__ __forceinline__ int ga_cur(const GaArgs& a) { return (int)(a.st->generation & 1); }
 
 // ------------------------------------------------------------------ eval ---
-template <int NQ>
-__global__ void __launch_bounds__(kFitThreads, 6) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
+template <int NQ, int MINB, class R>
+__global__ void __launch_bounds__(kFitThreads, MINB) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kFitWarps];
+  __shared__ FastChunkT<R> sh[kFitWarps];
   if (a.st->stop) return;
   const int cur = ga_cur(a);
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = a.target[i];
   __syncthreads();
-  fitness_rows<NQ>(c1 - c0, a.L, a.codes[cur] + c0 * a.L, a.thetas[cur] + c0 * a.L, Ts, sh,
-                   a.fitness + c0, kFitWarps);
+  fitness_rows<NQ, R>(c1 - c0, a.L, a.codes[cur] + c0 * a.L, a.thetas[cur] + c0 * a.L, Ts, sh,
+                      a.fitness + c0, kFitWarps);
 }
 
 // ---------------------------------------------------------------- reduce ---
@@ -374,22 +375,28 @@ static int ga_blocks(int64_t n) {
   return (int)(b < 1 ? 1 : b);
 }
 
-template <int NQ>
+template <int NQ, int MINB, class R>
 static isq_status ga_launch_eval_nq(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
-  const void* k = (const void*)ga_eval_kernel<NQ>;
+  const void* k = (const void*)ga_eval_kernel<NQ, MINB, R>;
   const int grid = persistent_grid(k, 0, c1 - c0, kFitWarps);
-  ga_eval_kernel<NQ><<<grid, kFitThreads, 0, s>>>(a, c0, c1);
+  ga_eval_kernel<NQ, MINB, R><<<grid, kFitThreads, 0, s>>>(a, c0, c1);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
+}
+
+template <int NQ>
+static isq_status ga_launch_eval_prec(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
+  if (a.precision == ISQ_PRECISION_FP32) return ga_launch_eval_nq<NQ, 8, float>(a, c0, c1, s);
+  return ga_launch_eval_nq<NQ, 6, double>(a, c0, c1, s);
 }
 
 static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
   if (c1 <= c0) return ISQ_OK;
   switch (a.n) {
-    case 2: return ga_launch_eval_nq<2>(a, c0, c1, s);
-    case 3: return ga_launch_eval_nq<3>(a, c0, c1, s);
-    case 4: return ga_launch_eval_nq<4>(a, c0, c1, s);
-    case 5: return ga_launch_eval_nq<5>(a, c0, c1, s);
+    case 2: return ga_launch_eval_prec<2>(a, c0, c1, s);
+    case 3: return ga_launch_eval_prec<3>(a, c0, c1, s);
+    case 4: return ga_launch_eval_prec<4>(a, c0, c1, s);
+    case 5: return ga_launch_eval_prec<5>(a, c0, c1, s);
     default:
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;
@@ -463,6 +470,8 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
                ISQ_ERR_UNSUPPORTED);
   if (cfg->population >= (1LL << 31)) return bad("population must be < 2^31", ISQ_ERR_UNSUPPORTED);
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return bad("invalid rank/world");
+  if (cfg->precision != ISQ_PRECISION_FP64 && cfg->precision != ISQ_PRECISION_FP32)
+    return bad("precision must be ISQ_PRECISION_FP64 or ISQ_PRECISION_FP32");
   GaHandle* h = new GaHandle();
   h->device = device;
   h->rank = cfg->rank;
@@ -480,6 +489,7 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
   a.target_fitness = cfg->target_fitness;
   a.max_generations = (uint64_t)cfg->max_generations;
   a.seed = cfg->seed;
+  a.precision = cfg->precision;
   a.rec_cap = h->max_batch;
   h->shard = (a.P + h->world - 1) / h->world;
   const int64_t D = 1LL << a.n;
@@ -587,8 +597,12 @@ isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, 
   if (st != ISQ_OK) return st;
   const GaArgs& a = h->a;
   const int mode = h->launch_mode;
-  if (mode == ISQ_LAUNCH_FUSED ||
-      (mode == ISQ_LAUNCH_AUTO && a.P <= kGaSmallPop && a.P * a.L <= kGaSmallGenes)) {
+  if (mode == ISQ_LAUNCH_FUSED && a.precision != ISQ_PRECISION_FP64) {
+    set_error("the fused single-block generation is fp64 only");
+    return ISQ_ERR_CONFIG;
+  }
+  if (mode == ISQ_LAUNCH_FUSED || (mode == ISQ_LAUNCH_AUTO && a.precision == ISQ_PRECISION_FP64 &&
+                                   a.P <= kGaSmallPop && a.P * a.L <= kGaSmallGenes)) {
     st = n > 0 ? ga_launch_small(a, n, h->stream) : ISQ_OK;
     if (st != ISQ_OK) return st;
     return isq_ga_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);

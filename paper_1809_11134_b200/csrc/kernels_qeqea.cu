@@ -588,7 +588,7 @@ isq_status qeqea_launch_score(const QeqeaArgs& a, cudaStream_t s) {
   if (count > 0) {
     isq_status st = launch_fitness_batch_stoppable(a.n, a.L, count, a.gate_codes, a.gate_thetas,
                                                    reinterpret_cast<const double*>(a.target),
-                                                   a.fitness + a.c0, &a.st->stop, s);
+                                                   a.fitness + a.c0, &a.st->stop, s, 0, a.precision);
     if (st != ISQ_OK) return st;
   }
   if (a.world > 1) qeqea_elite_kernel<<<1, 256, 0, s>>>(a);
@@ -613,10 +613,14 @@ isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
 }
 
 bool qeqea_small(const QeqeaArgs& a) {
-  return a.world == 1 && a.P <= kSmallPop && a.P * a.L <= kSmallTouches;
+  return a.world == 1 && a.precision == ISQ_PRECISION_FP64 && a.P <= kSmallPop && a.P * a.L <= kSmallTouches;
 }
 
 isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s) {
+  if (a.world != 1 || a.precision != ISQ_PRECISION_FP64) {
+    set_error("the fused single-block generation is single-rank fp64 only");
+    return ISQ_ERR_CONFIG;
+  }
   switch (a.n) {
     case 2: qeqea_small_kernel<2><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
     case 3: qeqea_small_kernel<3><<<1, kRedThreads, 0, s>>>(a, n_gens); break;

@@ -113,19 +113,21 @@ __device__ __forceinline__ GateParam gate_param(int code, double theta) {
   return g;
 }
 
-template <int NQ>
+// R = double for every exact path; R = float is the fitness kernel's fp32
+// variant (only set_identity / lift / cmul are used with it).
+template <int NQ, class R = double>
 struct WarpUnitary {
   using G = Geo<NQ>;
   static constexpr int E = G::E;
-  double re[E], im[E];
+  R re[E], im[E];
 
   __device__ __forceinline__ void set_identity(int lane) {
     const int j = lane & (G::D - 1);
     const int h = (lane >> NQ) & (G::LPC - 1);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
-      re[r] = (h * E + r == j) ? 1.0 : 0.0;
-      im[r] = 0.0;
+      re[r] = (h * E + r == j) ? R(1) : R(0);
+      im[r] = R(0);
     }
   }
 
@@ -203,7 +205,7 @@ struct WarpUnitary {
   // so no temporaries survive the case (no register moves); lane bits use the
   // direct form with (C, S) = (cos a, sin a) on the shuffled partner.
   template <int RB, int AX>
-  __device__ __forceinline__ void lift(double p, double q, double C, int lane) {
+  __device__ __forceinline__ void lift(R p, R q, R C, int lane) {
     if constexpr (RB < G::EB) {
       constexpr int m = 1 << RB;
 #pragma unroll
@@ -230,11 +232,11 @@ struct WarpUnitary {
       constexpr int lb = RB - G::EB;
       constexpr int lmask = G::D << lb;
       const bool hi = (lane >> (NQ + lb)) & 1;
-      const double S = (AX == 1 && !hi) ? -q : q;
+      const R S = (AX == 1 && !hi) ? -q : q;
 #pragma unroll
       for (int r = 0; r < E; ++r) {
-        const double yr = __shfl_xor_sync(0xffffffffu, re[r], lmask);
-        const double yi = __shfl_xor_sync(0xffffffffu, im[r], lmask);
+        const R yr = __shfl_xor_sync(0xffffffffu, re[r], lmask);
+        const R yi = __shfl_xor_sync(0xffffffffu, im[r], lmask);
         if constexpr (AX == 0) {  // x' = C x + i S y
           re[r] = fma(C, re[r], -S * yi);
           im[r] = fma(C, im[r], S * yr);
@@ -246,9 +248,9 @@ struct WarpUnitary {
     }
   }
 
-  __device__ __forceinline__ void cmul(int r, double fc, double fs) {
-    const double t1 = fs * im[r];
-    const double t2 = fs * re[r];
+  __device__ __forceinline__ void cmul(int r, R fc, R fs) {
+    const R t1 = fs * im[r];
+    const R t2 = fs * re[r];
     re[r] = fma(fc, re[r], -t1);
     im[r] = fma(fc, im[r], t2);
   }

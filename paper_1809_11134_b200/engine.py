@@ -157,8 +157,12 @@ class QeqeaEngine:
         rank: int = 0,
         world: int = 1,
         max_batch: int = 4096,
+        precision: str = "fp64",
     ):
         name = target.name if isinstance(target, TargetSpec) else "target"
+        if precision not in _lib.PRECISIONS:
+            raise ConfigurationError(f"precision must be one of {sorted(_lib.PRECISIONS)}")
+        self.precision = precision
         self._tmat = _target_array(target, cfg.number_of_wires, name)
         if seed < 0:
             raise ConfigurationError("seed must be non-negative")
@@ -197,7 +201,7 @@ class QeqeaEngine:
             target_fitness=c.target_fitness,
             seed=self.seed,
             world=self.world,
-            reserved=0,
+            precision=_lib.PRECISIONS[self.precision],
         )
         h = ctypes.c_void_p()
         _lib.check(lib.isq_qeqea_create(ctypes.byref(conf), _lib.ptr(self._tmat), self.device,

@@ -69,8 +69,11 @@ class GaEngine:
 
     def __init__(self, cfg: GaConfig, target: TargetSpec, seed: int, workers: int = 1, *,
                  device: int = 0, genomes: Optional[List[CircuitGenome]] = None,
-                 rank: int = 0, world: int = 1, max_batch: int = 4096):
+                 rank: int = 0, world: int = 1, max_batch: int = 4096, precision: str = "fp64"):
         name = target.name if isinstance(target, TargetSpec) else "target"
+        if precision not in _lib.PRECISIONS:
+            raise ConfigurationError(f"precision must be one of {sorted(_lib.PRECISIONS)}")
+        self.precision = precision
         self._tmat = _target_array(target, cfg.number_of_wires, name)
         if seed < 0:
             raise ConfigurationError("seed must be non-negative")
@@ -101,7 +104,8 @@ class GaEngine:
             number_of_wires=c.number_of_wires, size_of_individual=c.size_of_individual,
             population=c.population, mutation_rate=c.mutation_rate, mutation_range=c.mutation_range,
             structural_rate=c.structural_rate, max_generations=c.max_generations,
-            target_fitness=c.target_fitness, seed=self.seed, rank=self.rank, world=self.world)
+            target_fitness=c.target_fitness, seed=self.seed, rank=self.rank, world=self.world,
+            precision=_lib.PRECISIONS[self.precision], reserved=0)
         h = ctypes.c_void_p()
         _lib.check(lib.isq_ga_create(ctypes.byref(conf), _lib.ptr(self._tmat), self.device,
                                      self.max_batch, ctypes.byref(h)))

@@ -102,3 +102,36 @@ def test_compose_gates_api_matches_oracle():
     ref = O.compose([1, 9 + 1, 6, 5], [0.4, 2.2, 5.0, 1.0], 3)
     np.testing.assert_allclose(u, ref, atol=1e-13)
     np.testing.assert_allclose(compose_gates([], 3), np.eye(8), atol=0)
+
+
+FP32_RTOL, FP32_ATOL = 1e-4, 1e-6  # include/isq.h ISQ_PRECISION_FP32 bound
+
+
+def test_fp32_variant_matches_reference_goldens_within_stated_bound():
+    from paper_1809_11134_b200.fitness import fitness_batch
+
+    g, keys = _cases()
+    worst = 0.0
+    for k in keys:
+        n = int(k.split("_")[0][1:])
+        ref = g[k + "_fit"]
+        out = fitness_batch(g[k + "_codes"], g[k + "_thetas"], g[k + "_target"], n, precision="fp32")
+        err = np.abs(out - ref)
+        assert (err <= FP32_RTOL * np.abs(ref) + FP32_ATOL).all(), (k, out, ref)
+        worst = max(worst, float(err.max()))
+    assert worst > 0.0  # it really is a different arithmetic
+
+
+@pytest.mark.parametrize("n,L", [(3, 16), (4, 32), (5, 64)])
+def test_fp32_variant_matches_oracle_random(n, L):
+    from paper_1809_11134_b200.fitness import fitness_batch
+
+    rng = np.random.default_rng(500 + n)
+    count = 200
+    nc = 3 * n + n * (n - 1) // 2
+    codes = rng.integers(0, nc, size=(count, L)).astype(np.uint8)
+    thetas = rng.uniform(0, 2 * math.pi, size=(count, L))
+    T = random_unitary(2 ** n, rng)
+    out = fitness_batch(codes, thetas, T, n, precision="fp32")
+    ref = np.array([O.circuit_fitness(codes[c], thetas[c], T, n) for c in range(count)])
+    assert (np.abs(out - ref) <= FP32_RTOL * np.abs(ref) + FP32_ATOL).all()

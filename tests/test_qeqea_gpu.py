@@ -194,3 +194,26 @@ def test_c4_shape_sample_and_fitness_against_oracle():
         assert fit_close(fit[idx], ref).all()
         bests.append(eng.best_fitness)
     assert bests == sorted(bests)
+
+
+def test_fp32_engine_first_generation_within_bound():
+    """precision="fp32": same blueprints and gates as fp64 (they do not depend
+    on fitness in generation 0), fitness within the stated fp32 bound."""
+    from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
+    from paper_1809_11134_b200.fitness import TargetSpec
+
+    T = random_unitary(32, np.random.default_rng(9))
+    cfg = PopulationConfig(number_of_wires=5, size_of_individual=64, size_of_population=4096,
+                           target_fitness=1.0)
+    a = QeqeaEngine(cfg, TargetSpec("haar", 5, T), seed=4)
+    b = QeqeaEngine(cfg, TargetSpec("haar", 5, T), seed=4, precision="fp32")
+    fa, ca, ta = a.sample()
+    fb, cb, tb = b.sample()
+    assert np.array_equal(fa, fb) and np.array_equal(ca, cb) and np.array_equal(ta, tb)
+    a.step()
+    b.step()
+    x, y = a.last_fitness(), b.last_fitness()
+    assert (np.abs(x - y) <= 1e-4 * np.abs(x) + 1e-6).all()
+    assert not np.array_equal(x, y)
+    b.steps(5)  # keeps running on the fp32 path
+    assert b.generation == 6

@@ -28,33 +28,41 @@ def main():
         res["fp64_peak_tflops" if fp64 else "fp32_peak_tflops"] = v.value / 1e12
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream()
-    for n, L, count in [(3, 16, 1 << 20), (4, 32, 1 << 18), (5, 64, 1 << 16), (5, 64, 1 << 18)]:
-        if args_.only and f"n{n}" != args_.only:
-            continue
-        nc = 3 * n + n * (n - 1) // 2
-        g = torch.Generator(device=dev).manual_seed(1)
-        codes = torch.randint(0, nc, (count, L), device=dev, dtype=torch.uint8, generator=g)
-        thetas = torch.rand((count, L), device=dev, dtype=torch.float64, generator=g) * 2 * math.pi
-        T = torch.eye(2 ** n, dtype=torch.complex128, device=dev)
-        out = torch.empty(count, dtype=torch.float64, device=dev)
-        args = (n, L, count, codes.data_ptr(), thetas.data_ptr(), T.data_ptr(), out.data_ptr(), None,
-                stream.cuda_stream)
-        for _ in range(3):
-            _lib.check(lib.isq_fitness_batch_device(*args))
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = args_.reps
-        e0.record()
-        for _ in range(reps):
-            lib.isq_fitness_batch_device(*args)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        evals = count / (ms * 1e-3)
-        flop = (6 * L + 8) * 4 ** n
-        res[f"n{n}_L{L}_P{count}"] = {"ms": ms, "evals_per_s": evals,
-                                     "canon_tflops": evals * flop / 1e12,
-                                     "frac_fp64": evals * flop / 1e12 / res["fp64_peak_tflops"]}
+    for prec_name, prec in (("fp64", 0), ("fp32", 1)):
+        for mix in ("ga", "qeqea"):
+            for n, L, count in [(3, 16, 1 << 20), (4, 32, 1 << 18), (5, 64, 1 << 18)]:
+                if args_.only and f"n{n}" != args_.only:
+                    continue
+                nc = 3 * n + n * (n - 1) // 2
+                K = n + n * (n - 1) // 2
+                g = torch.Generator(device=dev).manual_seed(1)
+                if mix == "ga":  # uniform over the gate choices (ga.py:47-59)
+                    codes = torch.randint(0, nc, (count, L), device=dev, dtype=torch.uint8, generator=g)
+                else:  # QEQEA: slot kind uniform over K, measured axis uniform
+                    kinds = torch.randint(0, K, (count, L), device=dev, generator=g)
+                    axes = torch.randint(0, 3, (count, L), device=dev, generator=g)
+                    codes = torch.where(kinds < n, 3 * kinds + axes, 3 * n + (kinds - n)).to(torch.uint8)
+                thetas = torch.rand((count, L), device=dev, dtype=torch.float64, generator=g) * 2 * math.pi
+                T = torch.eye(2 ** n, dtype=torch.complex128, device=dev)
+                out = torch.empty(count, dtype=torch.float64, device=dev)
+                args = (n, L, count, codes.data_ptr(), thetas.data_ptr(), T.data_ptr(), out.data_ptr(), prec,
+                        stream.cuda_stream)
+                for _ in range(3):
+                    _lib.check(lib.isq_fitness_batch_device_ex(*args))
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = args_.reps
+                e0.record()
+                for _ in range(reps):
+                    lib.isq_fitness_batch_device_ex(*args)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                evals = count / (ms * 1e-3)
+                flop = (6 * L + 8) * 4 ** n
+                res[f"{prec_name}_{mix}_n{n}_L{L}_P{count}"] = {
+                    "ms": ms, "evals_per_s": evals, "canon_tflops": evals * flop / 1e12,
+                    "frac_fp64_peak": evals * flop / 1e12 / res["fp64_peak_tflops"]}
     print(json.dumps(res, indent=1))
 
 
