@@ -49,3 +49,46 @@ def test_product_package_does_not_import_oracle():
     pkg = ROOT / "paper_1809_11134_b200"
     for p in pkg.rglob("*.py"):
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", p.read_text(), flags=re.M), p
+
+
+@pytest.mark.parametrize("field,value", [("number_of_wires", 1), ("size_of_individual", 0),
+                                         ("probability_of_mutation", 1.5), ("n_meas", 0),
+                                         ("world", 9), ("rank", 3), ("precision", 7)])
+def test_qeqea_create_validates_before_touching_a_device(field, value):
+    """PopulationConfig validation (engine.py:45-63) and the sharding /
+    precision checks run in the C ABI before any CUDA call, so they hold on a
+    CPU-only host: ISQ_ERR_CONFIG and a message."""
+    from paper_1809_11134_b200 import _lib
+
+    lib = _lib.load()
+    kw = dict(number_of_wires=3, size_of_individual=8, size_of_population=5, probability_of_mutation=0.3,
+              mutation_range=0.78, n_meas=1, rank=0, max_generations=10, target_fitness=0.999, seed=1,
+              world=1, precision=0)
+    if field == "rank":
+        kw["world"] = 2
+    kw[field] = value
+    conf = _lib.QeqeaConfig(**kw)
+    T = np.eye(8, dtype=np.complex128)
+    h = ctypes.c_void_p()
+    st = lib.isq_qeqea_create(ctypes.byref(conf), T.ctypes.data_as(ctypes.c_void_p), 0, 4, ctypes.byref(h))
+    assert st == _lib.ISQ_ERR_CONFIG
+    assert h.value is None
+    assert lib.isq_last_error()
+
+
+def test_unsupported_shapes_are_reported_not_computed():
+    """n > 5 is a valid reference configuration the device build does not
+    implement: ISQ_ERR_UNSUPPORTED -> ConfigurationError, never a CPU fallback."""
+    from paper_1809_11134_b200 import _lib
+    from paper_1809_11134_b200.errors import ConfigurationError
+
+    lib = _lib.load()
+    conf = _lib.QeqeaConfig(number_of_wires=6, size_of_individual=8, size_of_population=5,
+                            probability_of_mutation=0.3, mutation_range=0.78, n_meas=1, rank=0,
+                            max_generations=10, target_fitness=0.999, seed=1, world=1, precision=0)
+    T = np.eye(64, dtype=np.complex128)
+    h = ctypes.c_void_p()
+    st = lib.isq_qeqea_create(ctypes.byref(conf), T.ctypes.data_as(ctypes.c_void_p), 0, 4, ctypes.byref(h))
+    assert st == _lib.ISQ_ERR_UNSUPPORTED
+    with pytest.raises(ConfigurationError):
+        _lib.check(st)
