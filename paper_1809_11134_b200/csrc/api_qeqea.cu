@@ -145,6 +145,10 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   const int64_t nc = a.S * a.L;                  // circuit-side touches
   const int64_t no = (int64_t)a.world * a.S * a.Lr;  // owner-side touches
   TRYA(cudaSetDevice(device));
+  if (qeqea_configure_device() != ISQ_OK) {
+    free_handle(h);
+    return ISQ_ERR_CUDA;
+  }
   TRYA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   TRYA(cudaMalloc((void**)&a.rot, a.Qtloc * sizeof(RotRec)));

@@ -130,6 +130,10 @@ constexpr double kHalfPiD = 1.5707963267948966;  // math.pi / 2
 
 // Python / numpy float remainder with the sign of the divisor (x % m, m > 0).
 __device__ __forceinline__ double py_mod(double x, double m) {
+  // |x| < 2m (an angle in [0, m) plus one bounded step): fmod is x, or x - m,
+  // which is exact there (Sterbenz); anything else takes the general path
+  if (x > 0.0 && x < m) return x;
+  if (x >= m && x < 2.0 * m) return __dsub_rn(x, m);
   double r = fmod(x, m);
   if (r != 0.0) {
     if (r < 0.0) r = __dadd_rn(r, m);
@@ -215,26 +219,40 @@ __device__ __forceinline__ void su3_one_param(int which, double v, double2 q[3])
 // mutated (masked and slot_max < 1) and applies the mutation to v.
 // Draw layout of the first block: w0 mask, w1 coin, w2 integers(8) (low
 // u32) or the angle sign, w3 the SU(3) parameter value.
-__device__ __forceinline__ bool mutate_slot(const QeqeaArgs& a, int64_t s, uint64_t mg, double f,
-                                            LiveSlot& v, bool* qutrit_path = nullptr) {
+enum : int { MUT_NONE = 0, MUT_ANGLE = 1, MUT_QUTRIT = 2 };
+
+// The draw-dependent part of the per-slot mutation: the angle step is applied
+// to v.theta; a qutrit mutation is returned as (which, value) for
+// su3_one_param, so a caller can run those (5 % of slots, costly and
+// divergent) compacted.
+__device__ __forceinline__ int mutate_decide(const QeqeaArgs& a, int64_t s, uint64_t mg, double f,
+                                             LiveSlot& v, int& which, double& value) {
   uint64_t w[4];
   stream_block(a.seed, DOM_MUTATE, mg, (uint64_t)s, 0, 1, w);
-  if (!(u64_to_double(w[0]) < a.p_mut)) return false;
-  if (!(f < 1.0)) return false;
+  if (!(u64_to_double(w[0]) < a.p_mut)) return MUT_NONE;
+  if (!(f < 1.0)) return MUT_NONE;
   const bool coin = u64_to_double(w[1]) < 0.5;
   const double omf = __dsub_rn(1.0, f);
-  if (qutrit_path) *qutrit_path = coin && s < a.Qt;
   if (coin && s < a.Qt) {
-    const int which = (int)((uint32_t)(w[2] & 0xffffffffULL) >> 29);  // Lemire, bound 8
-    const double range = which < 3 ? kHalfPiD : kTwoPiD;             // encoding.py:23
-    const double value = __dadd_rn(0.0, __dmul_rn(__dmul_rn(range, omf), u64_to_double(w[3])));
-    su3_one_param(which, value, v.q);
-  } else {
-    const double sign = u64_to_double(w[2]) < 0.5 ? 1.0 : -1.0;  // encoding.py:51
-    const double step = __dmul_rn(__dmul_rn(sign, omf), a.mutation_range);
-    v.theta = py_mod(__dadd_rn(v.theta, step), kTwoPiD);
+    which = (int)((uint32_t)(w[2] & 0xffffffffULL) >> 29);  // Lemire, bound 8
+    const double range = which < 3 ? kHalfPiD : kTwoPiD;     // encoding.py:23
+    value = __dadd_rn(0.0, __dmul_rn(__dmul_rn(range, omf), u64_to_double(w[3])));
+    return MUT_QUTRIT;
   }
-  return true;
+  const double sign = u64_to_double(w[2]) < 0.5 ? 1.0 : -1.0;  // encoding.py:51
+  const double step = __dmul_rn(__dmul_rn(sign, omf), a.mutation_range);
+  v.theta = py_mod(__dadd_rn(v.theta, step), kTwoPiD);
+  return MUT_ANGLE;
+}
+
+__device__ __forceinline__ bool mutate_slot(const QeqeaArgs& a, int64_t s, uint64_t mg, double f,
+                                            LiveSlot& v, bool* qutrit_path = nullptr) {
+  int which = 0;
+  double value = 0.0;
+  const int m = mutate_decide(a, s, mg, f, v, which, value);
+  if (qutrit_path) *qutrit_path = m == MUT_QUTRIT;
+  if (m == MUT_QUTRIT) su3_one_param(which, value, v.q);
+  return m != MUT_NONE;
 }
 
 // Live value of the (owned) slot s during generation g (committed value plus

@@ -84,19 +84,30 @@ __global__ void qeqea_unroute_kernel(QeqeaArgs a) {
 // carries a pending mutation (the commit consumes both).
 constexpr int kValThreads = 256;
 constexpr int kValPerThread = 3;  // touches per thread per tile: ~1 measurement task per thread
+constexpr int kValTile = kValThreads * kValPerThread;
 
-struct MeasureTask {  // 56 B: 768 tasks fit the 48 KB static shared limit
+struct MeasureTask {  // one rotation touch of the tile: its live qutrit, awaiting measurement
   double re[3], im[3];
+  double value;       // pending SU(3) parameter (qutrit mutation), see `which`
   uint32_t s;
-  uint32_t out;
+  uint16_t out;       // touch offset in the tile
+  int16_t which;      // pending su3_one_param parameter index, -1 none
+};
+
+struct ValuesShared {
+  MeasureTask tasks[kValTile];
+  uint16_t qq[kValTile];  // tasks with a pending qutrit mutation
+  int ntask, nq;
 };
 
 // Values phase of owned touch t up to the Born measurement: the live value
-// goes to v, the angle / starting slot_max / mutation flags to the touch
+// goes to v (angle mutations applied; a qutrit mutation is returned in
+// which / value), the angle / starting slot_max / mutation flags to the touch
 // arrays, and interaction slots get their gate code.  Returns true when the
 // touch is a rotation slot still to be measured (measure_code).
 __device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, uint64_t g, uint32_t& s,
-                                                 LiveSlot& v) {
+                                                 LiveSlot& v, int& which, double& value) {
+  which = -1;
   s = a.owner_flats[t];
   if (s == kNoSlot) {  // padding circuit: never commits (fitness <= 1 < 2)
     a.owner_codes[t] = 0;
@@ -106,11 +117,11 @@ __device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, 
     return false;
   }
   const double f = load_committed(a, slot_local(a, s), v);
-  bool qpath = false;
-  const bool mutated = g > 0 && mutate_slot(a, s, g - 1, f, v, &qpath);
+  const int m = g > 0 ? mutate_decide(a, s, g - 1, f, v, which, value) : MUT_NONE;
+  if (m != MUT_QUTRIT) which = -1;
   a.owner_thetas[t] = v.theta;
   a.touch_fbefore[t] = f;
-  a.touch_mutated[t] = (uint8_t)((mutated ? 1 : 0) | (mutated && qpath ? 2 : 0));
+  a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
   const int64_t kind = (int64_t)s / (a.L * a.P);
   if (kind < a.n) return true;
   a.owner_codes[t] = (uint8_t)(3 * a.n + (kind - a.n));
@@ -128,14 +139,17 @@ __device__ __forceinline__ uint8_t measure_code(const QeqeaArgs& a, uint32_t s, 
   return (uint8_t)(3 * ((int64_t)s / (a.L * a.P)) + axis);
 }
 
+// Per tile of kValTile owned touches: (1) record gathers + lazy angle
+// mutations, rotation touches queued in shared memory; (2) the queued qutrit
+// mutations (5 % of touches) on full warps; (3) the Born measurements of the
+// queued rotation touches on full warps.
 __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t1) {
-  __shared__ MeasureTask tasks[kValThreads * kValPerThread];
-  __shared__ int ntask;
+  extern __shared__ __align__(16) unsigned char val_smem[];
+  ValuesShared& sm = *reinterpret_cast<ValuesShared*>(val_smem);
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
-  constexpr int kTile = kValThreads * kValPerThread;
-  for (int64_t base = (int64_t)blockIdx.x * kTile; base < t1; base += (int64_t)gridDim.x * kTile) {
-    if (threadIdx.x == 0) ntask = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kValTile; base < t1; base += (int64_t)gridDim.x * kValTile) {
+    if (threadIdx.x == 0) sm.ntask = sm.nq = 0;
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kValPerThread; ++u) {
@@ -143,20 +157,39 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       if (t >= t1) break;
       uint32_t s;
       LiveSlot v;
-      if (value_touch_head(a, t, g, s, v)) {
-        const int k = atomicAdd(&ntask, 1);
+      int which;
+      double value;
+      if (value_touch_head(a, t, g, s, v, which, value)) {
+        const int k = atomicAdd(&sm.ntask, 1);
+        MeasureTask& mt = sm.tasks[k];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          tasks[k].re[c] = v.q[c].x;
-          tasks[k].im[c] = v.q[c].y;
+          mt.re[c] = v.q[c].x;
+          mt.im[c] = v.q[c].y;
         }
-        tasks[k].s = s;
-        tasks[k].out = (uint32_t)(t - base);
+        mt.value = value;
+        mt.s = s;
+        mt.out = (uint16_t)(t - base);
+        mt.which = (int16_t)which;
+        if (which >= 0) sm.qq[atomicAdd(&sm.nq, 1)] = (uint16_t)k;
       }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < ntask; k += kValThreads) {
-      const MeasureTask& mt = tasks[k];
+    for (int j = threadIdx.x; j < sm.nq; j += kValThreads) {
+      MeasureTask& mt = sm.tasks[sm.qq[j]];
+      double2 q[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) q[c] = make_double2(mt.re[c], mt.im[c]);
+      su3_one_param(mt.which, mt.value, q);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        mt.re[c] = q[c].x;
+        mt.im[c] = q[c].y;
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < sm.ntask; k += kValThreads) {
+      const MeasureTask& mt = sm.tasks[k];
       double re[3] = {mt.re[0], mt.re[1], mt.re[2]};
       double im[3] = {mt.im[0], mt.im[1], mt.im[2]};
       a.owner_codes[base + mt.out] = measure_code(a, mt.s, g, re, im);
@@ -522,7 +555,10 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
     for (int64_t t = threadIdx.x; t < touches; t += kRedThreads) {
       uint32_t s;
       LiveSlot v;
-      if (value_touch_head(a, t, g, s, v)) {
+      int which;
+      double value;
+      if (value_touch_head(a, t, g, s, v, which, value)) {
+        if (which >= 0) su3_one_param(which, value, v.q);
         double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
         double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
         a.owner_codes[t] = measure_code(a, s, g, re, im);
@@ -559,6 +595,18 @@ static int blocks_for(int64_t n, int threads) {
 
 
 
+isq_status qeqea_configure_device() {
+  // > 48 KB of dynamic shared memory needs the opt-in (per device)
+  ISQ_CUDA_TRY(cudaFuncSetAttribute((const void*)qeqea_values_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ValuesShared)));
+  return ISQ_OK;
+}
+
+static cudaError_t launch_values(const QeqeaArgs& a, int64_t t1, cudaStream_t s) {
+  qeqea_values_kernel<<<blocks_for(t1, kValThreads), kValThreads, sizeof(ValuesShared), s>>>(a, t1);
+  return cudaGetLastError();
+}
+
 isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s) {
   if (a.c0 < a.P) {
     const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, a.S);
@@ -567,7 +615,7 @@ isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s) {
   if (a.world > 1) {
     qeqea_route_kernel<<<blocks_for(a.S * a.L, 256), 256, 0, s>>>(a);
   } else {
-    qeqea_values_kernel<<<blocks_for(a.P * a.L, kValThreads), kValThreads, 0, s>>>(a, a.P * a.L);
+    ISQ_CUDA_TRY(launch_values(a, a.P * a.L, s));
   }
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
@@ -575,9 +623,7 @@ isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s) {
 
 isq_status qeqea_launch_values(const QeqeaArgs& a, cudaStream_t s) {
   if (a.world > 1) {
-    const int64_t t1 = a.world * a.S * a.Lr;
-    qeqea_values_kernel<<<blocks_for(t1, kValThreads), kValThreads, 0, s>>>(a, t1);
-    ISQ_CUDA_TRY(cudaGetLastError());
+    ISQ_CUDA_TRY(launch_values(a, a.world * a.S * a.Lr, s));
   }
   return ISQ_OK;
 }

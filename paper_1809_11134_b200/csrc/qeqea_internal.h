@@ -7,6 +7,7 @@ namespace isq {
 
 // world 1: prepare = sample + values; world > 1: prepare = sample + route,
 // values = values of the received owned touches, score = unroute + fitness + elite.
+isq_status qeqea_configure_device();  // kernel attributes, once per handle on its device
 isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_values(const QeqeaArgs& a, cudaStream_t s);
 isq_status qeqea_launch_score(const QeqeaArgs& a, cudaStream_t s);
