@@ -336,4 +336,68 @@ __device__ __forceinline__ void sample_circuit_warp(const QeqeaArgs& a, uint64_t
   }
 }
 
+// Lane-parallel sampling of several short circuits at once (2L u32 draws in
+// B = ceil(2L / 8) Philox blocks, B <= 32, i.e. L <= 128): every lane computes
+// one (circuit, block) pair, so 32 / B circuits share one round and all lanes
+// run Philox (sample_circuit_warp keeps 9 of 32 lanes busy).  Same draws, same
+// Lemire rejection replay, same flats as sample_circuit_warp.
+// blk: 32 x 4 words of shared memory per warp.
+__device__ __forceinline__ int sample_blocks_per_circuit(const QeqeaArgs& a) {
+  const int draws = (a.P > 1 ? a.L : 0) + a.L;
+  return (draws + 7) >> 3;
+}
+
+__device__ __forceinline__ void sample_circuits_batched(const QeqeaArgs& a, uint64_t g, int64_t c0, int64_t c1,
+                                                        uint32_t* flats, uint64_t* blk, int lane) {
+  const int L = a.L;
+  const int B = sample_blocks_per_circuit(a);
+  const int cpr = 32 / B;  // circuits per round
+  const uint32_t rngP = (uint32_t)(a.P - 1), rngK = (uint32_t)(a.K - 1);
+  const int offk = (a.P == 1) ? 0 : L;
+  for (int64_t cb = c0; cb < c1; cb += cpr) {
+    {
+      const int ci = lane / B, b = lane - ci * B;
+      const int64_t c = cb + ci;
+      if (ci < cpr && c < c1) {
+        uint64_t w[4];
+        stream_block(a.seed, DOM_SAMPLE, g, (uint64_t)c, 0, (uint64_t)b + 1, w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) blk[lane * 4 + k] = w[k];
+      }
+    }
+    __syncwarp();
+    const int nc = (int)min((int64_t)cpr, c1 - cb);
+    for (int ci = 0; ci < nc; ++ci) {
+      const uint64_t* cb_blk = blk + ci * B * 4;
+      bool reject = false;
+      for (int p = lane; p < L; p += 32) {
+        uint32_t ind = 0;
+        if (a.P > 1) {
+          const uint64_t word = cb_blk[(p >> 3) * 4 + ((p & 7) >> 1)];
+          const uint32_t u = (p & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+          reject |= lemire_rejects(u, rngP);
+          ind = lemire_value(u, rngP);
+        }
+        const int uk = offk + p;
+        const uint64_t word = cb_blk[(uk >> 3) * 4 + ((uk & 7) >> 1)];
+        const uint32_t u = (uk & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+        reject |= lemire_rejects(u, rngK);
+        const uint32_t kind = lemire_value(u, rngK);
+        flats[(cb + ci - c0) * L + p] = (uint32_t)((int64_t)kind * L * a.P + (int64_t)ind * L + p);
+      }
+      if (__any_sync(0xffffffffu, reject)) {  // numpy's Lemire rejected a draw: replay the stream
+        __syncwarp();
+        if (lane == 0) {
+          uint32_t* f = flats + (cb + ci - c0) * L;
+          NpStream st;
+          st.init(a.seed, DOM_SAMPLE, g, (uint64_t)(cb + ci), 0);
+          for (int p = 0; p < L; ++p) f[p] = (uint32_t)(st.integers(a.P) * L + p);
+          for (int p = 0; p < L; ++p) f[p] += (uint32_t)(st.integers(a.K) * L * a.P);
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 }  // namespace isq

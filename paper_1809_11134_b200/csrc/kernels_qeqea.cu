@@ -28,14 +28,23 @@ namespace isq {
 // keep each one's hot code inside the instruction cache and give the random
 // bank gathers thread-level memory parallelism.
 
+constexpr int kSampleRun = 64;  // circuits per warp task of the batched sampler
+
 __global__ void __launch_bounds__(kThreadsPerBlock) qeqea_sample_flats_kernel(QeqeaArgs a) {
-  __shared__ uint64_t blk[kWarpsPerBlock][36];
+  __shared__ uint64_t blk[kWarpsPerBlock][128];
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
   const int64_t c1 = min(a.P, a.c0 + a.S);
+  if (sample_blocks_per_circuit(a) <= 32) {
+    // short circuits (L <= 128): runs of kSampleRun circuits per warp, all lanes on Philox
+    for (int64_t r = a.c0 + ((int64_t)blockIdx.x * kWarpsPerBlock + wib) * kSampleRun; r < c1;
+         r += nwarps * kSampleRun)
+      sample_circuits_batched(a, g, r, min(c1, r + kSampleRun), a.flats + (r - a.c0) * a.L, blk[wib], lane);
+    return;
+  }
   for (int64_t c = a.c0 + (int64_t)blockIdx.x * kWarpsPerBlock + wib; c < c1; c += nwarps)
     sample_circuit_warp(a, g, c, a.flats + (c - a.c0) * a.L, blk[wib], lane);
 }
@@ -609,7 +618,7 @@ static cudaError_t launch_values(const QeqeaArgs& a, int64_t t1, cudaStream_t s)
 
 isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s) {
   if (a.c0 < a.P) {
-    const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, a.S);
+    const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, (a.S + kSampleRun - 1) / kSampleRun);
     qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a);
   }
   if (a.world > 1) {
