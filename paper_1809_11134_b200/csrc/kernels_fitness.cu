@@ -17,8 +17,13 @@ struct ChunkShared {
 // (<= 168 registers) gives 3 warps per scheduler for the n = 5
 // register-resident state (measured: 2 warps per scheduler at 244 registers
 // is 11 % slower).
+#ifdef ISQ_FIT_MAXNREG  // register-cap experiments (tools/): replaces the min-blocks bound
+#define ISQ_FIT_BOUNDS __maxnreg__(ISQ_FIT_MAXNREG)
+#else
+#define ISQ_FIT_BOUNDS __launch_bounds__(kFitThreads, MINB)
+#endif
 template <int NQ, int MINB, class R>
-__global__ void __launch_bounds__(kFitThreads, MINB)
+__global__ void ISQ_FIT_BOUNDS
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
                         double* __restrict__ fitness, const int32_t* __restrict__ stop) {
@@ -33,7 +38,10 @@ __global__ void __launch_bounds__(kFitThreads, MINB)
 
 // fp32 variant: the column of S in 64 float registers: 8 resident 2-warp
 // blocks per SM (<= 128 registers, 4 warps per scheduler).
-constexpr int kFitMinBlocks64 = 6;
+#ifndef ISQ_FIT64_MINB
+#define ISQ_FIT64_MINB 6
+#endif
+constexpr int kFitMinBlocks64 = ISQ_FIT64_MINB;
 constexpr int kFitMinBlocks32 = 8;
 
 // Composition with the exact global phase (compose_gates readout) + fitness.
