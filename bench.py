@@ -7,9 +7,11 @@ compose + score 2^20 circuits of 64 gates on 5 qubits, reductions, commit,
 table update) over a device-resident bank of 1.0e9 slots (36 GB, far above the
 126 MB L2), Haar-random target.  At N > 1 (torchrun) the 2^20 circuits are
 sharded over the ranks and the bank by slot position: per
-generation two NCCL all-to-alls (touches to their owners, gate codes / live
-angles back) and two all-gathers (fitness, shard elites); no O(P*L) pass is
-replicated.
+generation the touches go to their owners, gate codes / live angles come back
+and fitness / shard elites go to every rank — stored by the producing kernels
+straight into the peers' buffers over NVLink (`--transport p2p`, default,
+ordered by one-element all-reduces) or as NCCL all-to-alls / all-gathers
+(`--transport nccl`); no O(P*L) pass is replicated.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -181,7 +183,7 @@ def run_ours(args):
 
     stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
-        ops = DeviceQeqeaOps(eng)  # binds the handle to `stream`
+        ops = DeviceQeqeaOps(eng, args.transport)  # binds the handle to `stream`
         comm = Comm() if world > 1 else None
         shard = ops.S
         ops.begin_batch()
@@ -230,7 +232,9 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": "C5: QEQEA generation, n=5 qubits, depth L=64, population 2^20, "
                                "Haar-random 32x32 target; bank 1.0e9 slots (36 GB) resident in HBM",
-                   "n": N, "L": L, "P": P, "global_batch": P, "parallelism": f"dp{world} (circuit shards x position-owned bank shards)",
+                   "n": N, "L": L, "P": P, "global_batch": P,
+                   "parallelism": f"dp{world} (circuit shards x position-owned bank shards)"
+                                  + (f", {args.transport} transport" if world > 1 else ""),
                    "l2": "inputs larger than L2 (36 GB bank vs 126 MB)"},
         "gens_per_s": args.steps / (ms * 1e-3),
         "phase_ms": {"prepare (sample + route + lazy mutation + measure; world > 1: + 2 all-to-alls)":
@@ -247,7 +251,9 @@ def run_ours(args):
                               "phase updates here, not the canonical 6*4^n; the executed FP64 pipe "
                               "utilisation (ncu sm__pipe_fp64_cycles_active) is in profiles/ and DESIGN.md §6")},
         "clocks": clk,
-        "gpu_launches": (7 if world == 1 else 10) * args.steps,
+        # per generation: sample, values, fitness, 2 reductions, commit, advance;
+        # world > 1 adds route, unroute, elite (+ the fitness broadcast with p2p)
+        "gpu_launches": (7 if world == 1 else (11 if args.transport == "p2p" else 10)) * args.steps,
         "best_fitness": float(rec["best_fitness"][-1]),
     }
 
@@ -354,6 +360,8 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-fp32", action="store_true")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1: kernels store into peers over NVLink (p2p) or NCCL collectives between phases")
     ap.add_argument("--cpu-per-worker", type=int, default=400)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

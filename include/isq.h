@@ -207,6 +207,35 @@ typedef struct isq_qeqea_exchange_buffers {
   void* stream;       /* cudaStream_t of the handle                                    */
 } isq_qeqea_exchange_buffers;
 isq_status isq_qeqea_exchange(void* handle, isq_qeqea_exchange_buffers* out);
+
+/*
+ * NVLink peer transport (the fused alternative to the collectives above):
+ * once every rank's exchange buffers are mapped into every process, the
+ * producing kernels store straight into the consuming ranks' buffers at the
+ * places the collectives would put the data — prepare into the owners'
+ * recv_flats, values into the circuit ranks' recv_codes / recv_thetas, score
+ * into every rank's fitness and elite — so the data moves while the kernels
+ * compute, and the caller only orders the phases with a stream-ordered
+ * barrier (e.g. a one-element all-reduce) before prepare and after prepare,
+ * values and score.
+ *   isq_qeqea_ipc_export  this rank's 5 buffers (recv_flats, recv_codes,
+ *                         recv_thetas, fitness, elite) as cudaIpcMemHandle_t
+ *   isq_qeqea_ipc_open    all ranks' handles (world x 5, rank-major) -> maps the
+ *                         other ranks' buffers and enables the transport
+ *   isq_qeqea_set_peers   the same from device pointers already valid in this
+ *                         process (e.g. several ranks' handles on one device);
+ *                         NULL disables the transport (back to collectives)
+ */
+#define ISQ_PEER_BUFFERS 5
+typedef struct isq_ipc_handle {
+  char bytes[64];
+} isq_ipc_handle;
+typedef struct isq_qeqea_peer_buffers {
+  void *recv_flats, *recv_codes, *recv_thetas, *fitness, *elite;
+} isq_qeqea_peer_buffers;
+isq_status isq_qeqea_ipc_export(void* handle, isq_ipc_handle* out);
+isq_status isq_qeqea_ipc_open(void* handle, const isq_ipc_handle* all);
+isq_status isq_qeqea_set_peers(void* handle, const isq_qeqea_peer_buffers* peers);
 isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
                                 int32_t* stop_reason, uint64_t* generation, double* best_fitness);
 isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream);

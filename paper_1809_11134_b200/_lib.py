@@ -101,6 +101,17 @@ class QeqeaExchange(ctypes.Structure):
     ]
 
 
+PEER_BUFFERS = 5
+IPC_HANDLE_BYTES = 64
+
+
+class PeerBuffers(ctypes.Structure):
+    """isq_qeqea_peer_buffers (include/isq.h)."""
+
+    _fields_ = [("recv_flats", c_vp), ("recv_codes", c_vp), ("recv_thetas", c_vp), ("fitness", c_vp),
+                ("elite", c_vp)]
+
+
 GEN_RECORD = np.dtype([("gen_best", "f8"), ("gen_mean", "f8"), ("best_fitness", "f8"), ("reserved", "f8")])
 
 c_i32p = ctypes.POINTER(c_i32)
@@ -118,6 +129,9 @@ SIGNATURES: dict[str, tuple] = {
     "isq_qeqea_set_launch_mode": (c_i32, [c_vp, c_i32]),
     "isq_ga_set_launch_mode": (c_i32, [c_vp, c_i32]),
     "isq_qeqea_exchange": (c_i32, [c_vp, c_vp]),
+    "isq_qeqea_ipc_export": (c_i32, [c_vp, c_vp]),
+    "isq_qeqea_ipc_open": (c_i32, [c_vp, c_vp]),
+    "isq_qeqea_set_peers": (c_i32, [c_vp, c_vp]),
     "isq_qeqea_score": (c_i32, [c_vp]),
     "isq_qeqea_read_batch": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "isq_qeqea_buffers": (c_i32, [c_vp, c_vp, c_vp, c_vp]),

@@ -1,6 +1,7 @@
 // C ABI of the QEQEA engine handle (QeqeaEngine, engine.py:266-384).
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "qeqea_internal.h"
 
@@ -18,7 +19,17 @@ struct QeqeaHandle {
   QeqeaDevState* h_state = nullptr;  // pinned
   GenGraph graph;                    // isq_qeqea_step on small populations
   int launch_mode = ISQ_LAUNCH_AUTO;
+  PeerTable* d_peers = nullptr;      // peer transport table (device)
+  std::vector<void*> ipc_opened;     // peer buffers mapped by isq_qeqea_ipc_open
 };
+
+static void close_peers(QeqeaHandle* h) {
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  h->ipc_opened.clear();
+  cudaFree(h->d_peers);
+  h->d_peers = nullptr;
+  h->a.peers = nullptr;
+}
 
 static void free_handle(QeqeaHandle* h) {
   if (!h) return;
@@ -37,6 +48,7 @@ static void free_handle(QeqeaHandle* h) {
     cudaFree(a.owner_thetas);
   }
   h->graph.reset();
+  close_peers(h);
   if (h->h_records) cudaFreeHost(h->h_records);
   if (h->h_state) cudaFreeHost(h->h_state);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -264,6 +276,93 @@ isq_status isq_qeqea_finish(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   return qeqea_launch_finish(h->a, h->stream);
+}
+
+isq_status isq_qeqea_set_peers(void* handle, const isq_qeqea_peer_buffers* peers) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (peers == nullptr) {
+    close_peers(h);
+    return ISQ_OK;
+  }
+  if (h->world < 2) {
+    set_error("the peer transport needs world > 1");
+    return ISQ_ERR_CONFIG;
+  }
+  PeerTable t;
+  std::memset(&t, 0, sizeof(t));
+  for (int r = 0; r < h->world; ++r) {
+    const isq_qeqea_peer_buffers& b = peers[r];
+    if (!b.recv_flats || !b.recv_codes || !b.recv_thetas || !b.fitness || !b.elite) {
+      set_error("peer buffers of rank " + std::to_string(r) + " incomplete");
+      return ISQ_ERR_CONFIG;
+    }
+    t.recv_flats[r] = static_cast<uint32_t*>(b.recv_flats);
+    t.recv_codes[r] = static_cast<uint8_t*>(b.recv_codes);
+    t.recv_thetas[r] = static_cast<double*>(b.recv_thetas);
+    t.fitness[r] = static_cast<double*>(b.fitness);
+    t.elite[r] = static_cast<double*>(b.elite);
+  }
+  if (t.recv_flats[h->rank] != h->a.owner_flats || t.fitness[h->rank] != h->a.fitness) {
+    set_error("peers[rank] must be this handle's own exchange buffers");
+    return ISQ_ERR_CONFIG;
+  }
+  if (!h->d_peers) ISQ_CUDA_TRY(cudaMalloc((void**)&h->d_peers, sizeof(PeerTable)));
+  ISQ_CUDA_TRY(cudaMemcpy(h->d_peers, &t, sizeof(t), cudaMemcpyHostToDevice));
+  h->a.peers = h->d_peers;
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_ipc_export(void* handle, isq_ipc_handle* out) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  const QeqeaArgs& a = h->a;
+  if (h->world < 2) {
+    set_error("the peer transport needs world > 1");
+    return ISQ_ERR_CONFIG;
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(isq_ipc_handle), "IPC handle size");
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  void* bufs[ISQ_PEER_BUFFERS] = {a.owner_flats, a.recv_codes, a.recv_thetas, a.fitness, a.elite};
+  for (int k = 0; k < ISQ_PEER_BUFFERS; ++k) {
+    cudaIpcMemHandle_t m;
+    ISQ_CUDA_TRY(cudaIpcGetMemHandle(&m, bufs[k]));
+    std::memcpy(&out[k], &m, sizeof(m));
+  }
+  return ISQ_OK;
+}
+
+isq_status isq_qeqea_ipc_open(void* handle, const isq_ipc_handle* all) {
+  QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  const QeqeaArgs& a = h->a;
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  close_peers(h);
+  std::vector<isq_qeqea_peer_buffers> peers(h->world);
+  for (int r = 0; r < h->world; ++r) {
+    void* p[ISQ_PEER_BUFFERS];
+    if (r == h->rank) {
+      p[0] = a.owner_flats;
+      p[1] = a.recv_codes;
+      p[2] = a.recv_thetas;
+      p[3] = a.fitness;
+      p[4] = a.elite;
+    } else {
+      for (int k = 0; k < ISQ_PEER_BUFFERS; ++k) {
+        cudaIpcMemHandle_t m;
+        std::memcpy(&m, &all[r * ISQ_PEER_BUFFERS + k], sizeof(m));
+        cudaError_t e = cudaIpcOpenMemHandle(&p[k], m, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          set_error(std::string("cudaIpcOpenMemHandle (rank ") + std::to_string(r) + "): " +
+                    cudaGetErrorString(e));
+          close_peers(h);
+          return ISQ_ERR_CUDA;
+        }
+        h->ipc_opened.push_back(p[k]);
+      }
+    }
+    peers[r] = isq_qeqea_peer_buffers{p[0], p[1], p[2], p[3], p[4]};
+  }
+  return isq_qeqea_set_peers(handle, peers.data());
 }
 
 isq_status isq_qeqea_exchange(void* handle, isq_qeqea_exchange_buffers* x) {

@@ -59,6 +59,16 @@ struct alignas(16) IntRec {
 constexpr int kMaxWorld = 64;
 constexpr uint32_t kNoSlot = 0xffffffffu;  // padding touch of a padding circuit
 
+// NVLink peer-memory transport (world > 1, isq_qeqea_set_peers): the
+// exchange buffers of every rank, mapped into this process (own rank: local).
+struct PeerTable {
+  uint32_t* recv_flats[kMaxWorld];  // owner o: touches of its positions, from every circuit rank
+  uint8_t* recv_codes[kMaxWorld];   // circuit rank j: gate codes of its circuits, from every owner
+  double* recv_thetas[kMaxWorld];
+  double* fitness[kMaxWorld];       // every rank: the whole fitness vector
+  double* elite[kMaxWorld];         // every rank: all shard elites
+};
+
 // Device view of one engine handle.  Multi-GPU layout (population sharding,
 // DESIGN.md §8): rank r scores circuits [c0, c0 + S) and owns the bank slots
 // of positions [p_lo, p_lo + Lr) (every slot kind and individual); a slot's
@@ -102,6 +112,8 @@ struct QeqeaArgs {
   double* recv_thetas;
   double* elite;            // world * elite_len: per-rank shard best (fitness, circuit, L angles, L codes)
   int elite_len;
+  const PeerTable* peers;   // device table; non-null: the producing kernels store into the
+                            // consuming ranks' buffers directly (no all-to-all / all-gather)
   QeqeaDevState* st;
   GenRecord* records;
   uint8_t* best_codes;   // L

@@ -59,7 +59,10 @@ __device__ __forceinline__ int64_t routed_index(const QeqeaArgs& a, int64_t c_lo
   return a.S * lo + c_loc * lr + (p - lo);
 }
 
-// world > 1: this rank's touches grouped by owner (padding circuits send kNoSlot).
+// world > 1: this rank's touches grouped by owner (padding circuits send
+// kNoSlot).  Peer transport: stored straight into the owner's receive buffer
+// at the place the all-to-all would put them (block of source rank r at
+// r * S * Lr(o), row = circuit, column = owned position).
 __global__ void qeqea_route_kernel(QeqeaArgs a) {
   if (a.st->stop) return;
   const int64_t n = a.S * a.L;
@@ -67,8 +70,17 @@ __global__ void qeqea_route_kernel(QeqeaArgs a) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c_loc = i / a.L;
     const int p = (int)(i - c_loc * a.L);
-    a.send_flats[routed_index(a, c_loc, p)] = a.c0 + c_loc < a.P ? a.flats[i] : kNoSlot;
+    const uint32_t f = a.c0 + c_loc < a.P ? a.flats[i] : kNoSlot;
+    if (a.peers) {
+      int o = 0;
+      while (p >= a.p_bounds[o + 1]) ++o;
+      const int lo = a.p_bounds[o], lr = a.p_bounds[o + 1] - lo;
+      a.peers->recv_flats[o][(a.rank * a.S + c_loc) * lr + (p - lo)] = f;
+    } else {
+      a.send_flats[routed_index(a, c_loc, p)] = f;
+    }
   }
+  if (a.peers) __threadfence_system();
 }
 
 // world > 1: the owners' gate codes / live angles back into circuit order.
@@ -109,6 +121,32 @@ struct ValuesShared {
   int ntask, nq;
 };
 
+// Gate code / live angle of owned touch t, to the owner-side arrays and, with
+// the peer transport, straight into the receive buffers of the circuit's rank
+// (block of this owner at S * p_lo, row = circuit - j * S, column = q).
+__device__ __forceinline__ int64_t peer_recv_index(const QeqeaArgs& a, int64_t t, int64_t& j) {
+  const int64_t c = t / a.Lr;
+  j = c / a.S;
+  return a.S * a.p_lo + (c - j * a.S) * a.Lr + (t - c * a.Lr);
+}
+__device__ __forceinline__ void emit_code(const QeqeaArgs& a, int64_t t, uint8_t code) {
+  if (a.peers) {
+    int64_t j;
+    const int64_t idx = peer_recv_index(a, t, j);
+    a.peers->recv_codes[j][idx] = code;
+  } else {
+    a.owner_codes[t] = code;
+  }
+}
+__device__ __forceinline__ void emit_theta(const QeqeaArgs& a, int64_t t, double theta) {
+  a.owner_thetas[t] = theta;  // the commit reads it back
+  if (a.peers) {
+    int64_t j;
+    const int64_t idx = peer_recv_index(a, t, j);
+    a.peers->recv_thetas[j][idx] = theta;
+  }
+}
+
 // Values phase of owned touch t up to the Born measurement: the live value
 // goes to v (angle mutations applied; a qutrit mutation is returned in
 // which / value), the angle / starting slot_max / mutation flags to the touch
@@ -119,8 +157,8 @@ __device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, 
   which = -1;
   s = a.owner_flats[t];
   if (s == kNoSlot) {  // padding circuit: never commits (fitness <= 1 < 2)
-    a.owner_codes[t] = 0;
-    a.owner_thetas[t] = 0.0;
+    emit_code(a, t, 0);
+    emit_theta(a, t, 0.0);
     a.touch_fbefore[t] = 2.0;
     a.touch_mutated[t] = 0;
     return false;
@@ -128,12 +166,12 @@ __device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, 
   const double f = load_committed(a, slot_local(a, s), v);
   const int m = g > 0 ? mutate_decide(a, s, g - 1, f, v, which, value) : MUT_NONE;
   if (m != MUT_QUTRIT) which = -1;
-  a.owner_thetas[t] = v.theta;
+  emit_theta(a, t, v.theta);
   a.touch_fbefore[t] = f;
   a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
   const int64_t kind = (int64_t)s / (a.L * a.P);
   if (kind < a.n) return true;
-  a.owner_codes[t] = (uint8_t)(3 * a.n + (kind - a.n));
+  emit_code(a, t, (uint8_t)(3 * a.n + (kind - a.n)));
   return false;
 }
 
@@ -201,10 +239,11 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       const MeasureTask& mt = sm.tasks[k];
       double re[3] = {mt.re[0], mt.re[1], mt.re[2]};
       double im[3] = {mt.im[0], mt.im[1], mt.im[2]};
-      a.owner_codes[base + mt.out] = measure_code(a, mt.s, g, re, im);
+      emit_code(a, base + mt.out, measure_code(a, mt.s, g, re, im));
     }
     __syncthreads();
   }
+  if (a.peers) __threadfence_system();
 }
 
 // world > 1: best circuit of this rank's shard (first index on ties) and its
@@ -237,18 +276,36 @@ __global__ void __launch_bounds__(256) qeqea_elite_kernel(QeqeaArgs a) {
     }
     __syncthreads();
   }
-  double* e = a.elite + (int64_t)a.rank * a.elite_len;
   const int64_t best = sarg[0];
-  if (threadIdx.x == 0) {
-    e[0] = smax[0];
-    e[1] = (double)(best == INT64_MAX ? -1 : best);
+  // own slot of the elite buffer; peer transport: every rank's copy
+  for (int dst = a.peers ? 0 : a.rank; dst < (a.peers ? a.world : a.rank + 1); ++dst) {
+    double* e = (a.peers ? a.peers->elite[dst] : a.elite) + (int64_t)a.rank * a.elite_len;
+    if (threadIdx.x == 0) {
+      e[0] = smax[0];
+      e[1] = (double)(best == INT64_MAX ? -1 : best);
+    }
+    if (best == INT64_MAX) continue;
+    uint8_t* codes = reinterpret_cast<uint8_t*>(e + 2 + a.L);
+    for (int p = threadIdx.x; p < a.L; p += blockDim.x) {
+      e[2 + p] = a.gate_thetas[(best - a.c0) * a.L + p];
+      codes[p] = a.gate_codes[(best - a.c0) * a.L + p];
+    }
   }
-  if (best == INT64_MAX) return;
-  uint8_t* codes = reinterpret_cast<uint8_t*>(e + 2 + a.L);
-  for (int p = threadIdx.x; p < a.L; p += blockDim.x) {
-    e[2 + p] = a.gate_thetas[(best - a.c0) * a.L + p];
-    codes[p] = a.gate_codes[(best - a.c0) * a.L + p];
+  if (a.peers) __threadfence_system();
+}
+
+// Peer transport: this rank's fitness shard into every other rank's fitness
+// vector (the all-gather, as direct NVLink stores).
+__global__ void qeqea_fitness_broadcast_kernel(QeqeaArgs a) {
+  if (a.st->stop) return;
+  const int64_t n = a.S * (a.world - 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / a.S, c = a.c0 + (i - k * a.S);
+    const int dst = (int)(k < a.rank ? k : k + 1);
+    a.peers->fitness[dst][c] = a.fitness[c];
   }
+  __threadfence_system();
 }
 
 // -------------------------------------------------------------- reduce ---
@@ -570,7 +627,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
         if (which >= 0) su3_one_param(which, value, v.q);
         double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
         double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
-        a.owner_codes[t] = measure_code(a, s, g, re, im);
+        emit_code(a, t, measure_code(a, s, g, re, im));
       }
     }
     __syncthreads();
@@ -646,7 +703,10 @@ isq_status qeqea_launch_score(const QeqeaArgs& a, cudaStream_t s) {
                                                    a.fitness + a.c0, &a.st->stop, s, 0, a.precision);
     if (st != ISQ_OK) return st;
   }
-  if (a.world > 1) qeqea_elite_kernel<<<1, 256, 0, s>>>(a);
+  if (a.world > 1) {
+    if (a.peers) qeqea_fitness_broadcast_kernel<<<blocks_for(a.S * (a.world - 1), 256), 256, 0, s>>>(a);
+    qeqea_elite_kernel<<<1, 256, 0, s>>>(a);
+  }
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }

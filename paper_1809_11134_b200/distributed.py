@@ -20,7 +20,16 @@ Per QEQEA generation (include/isq.h split-phase protocol):
               the elite of the rank holding them, commit + table update of
               the owned touches only
 
-so every O(P*L) pass (sampling, bank gathers, commit) and the O(P*L*4^n)
+Two transports move the data, with identical results:
+
+* "p2p" (default of sharded_qeqea / bench.py): every rank's exchange buffers
+  are mapped into every process (CUDA IPC); route, values, the fitness
+  broadcast and elite kernels store straight into the consuming ranks'
+  buffers over NVLink while they compute, and four stream-ordered
+  one-element all-reduces order the phases;
+* "nccl": the a2a / gather steps are NCCL collectives between the phases.
+
+So every O(P*L) pass (sampling, bank gathers, commit) and the O(P*L*4^n)
 fitness are divided by `world`; only the O(P) reduction is replicated.
 GA (`ga.py`): genomes are replicated, rank r scores its genome shard, the
 fitness vector is all-gathered and every rank breeds identically from the
@@ -90,6 +99,29 @@ class Comm:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self._token = None
+
+    def barrier(self):
+        """Stream-ordered barrier of the peer transport: a one-element
+        all-reduce (NCCL: on the current stream, no host synchronisation)."""
+        import torch
+
+        if self.dist.get_backend(self.group) == "gloo":
+            # host barrier: this rank's kernels must have completed first
+            torch.cuda.current_stream().synchronize()
+            self.dist.barrier(group=self.group)
+            return
+        if self._token is None:
+            self._token = torch.zeros(1, dtype=torch.int32, device=torch.cuda.current_device())
+        self.dist.all_reduce(self._token, group=self.group)
+
+    def connect_peers(self, ops):
+        """Exchange the exchange-buffer IPC handles and map every rank's into
+        this process (isq_qeqea_ipc_export / _ipc_open)."""
+        mine = ops.ipc_handles()
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        ops.open_peers_ipc(allh)
 
     def all_to_all(self, out, inp, out_splits: List[int], in_splits: List[int]):
         self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
@@ -176,16 +208,27 @@ class _DeviceOps:
 
 
 class DeviceQeqeaOps(_DeviceOps):
+    """One rank's generation.  transport="nccl": the two all-to-alls and two
+    all-gathers are collectives between the phases; transport="p2p": the
+    producing kernels store straight into the other ranks' buffers over
+    NVLink (include/isq.h peer transport) and the phases are only ordered by
+    stream barriers.  Both give identical results."""
+
     _prefix = "qeqea"
 
-    def __init__(self, engine):
+    def __init__(self, engine, transport: str = "nccl"):
+        if transport not in ("nccl", "p2p"):
+            raise ValueError("transport must be 'nccl' or 'p2p'")
         super().__init__(engine)
+        self.transport = transport
+        self.connected = False
         x = _lib.QeqeaExchange()
         self._call("exchange", ctypes.byref(x))
         self.world, self.rank, self.S = x.world, x.rank, x.shard
         self.routing = Routing(engine.cfg.size_of_individual, self.S, self.world, self.rank)
         L, dev, no = engine.cfg.size_of_individual, engine.device, self.world * self.S * self.routing.Lr
         self.fitness = _device_view(x.fitness, self.world * self.S, "<f8", dev)
+        self._x = x
         if self.world > 1:
             self.elite_len = x.elite_len
             self.elite = _device_view(x.elite, self.world * x.elite_len, "<f8", dev)
@@ -197,10 +240,36 @@ class DeviceQeqeaOps(_DeviceOps):
             self.send_thetas = _device_view(x.send_thetas, no, "<f8", dev)
             self.recv_thetas = _device_view(x.recv_thetas, self.S * L, "<f8", dev)
 
+    # -- peer transport ---------------------------------------------------
+    def peer_buffers(self):
+        """This rank's exchange buffers (device pointers, include/isq.h order)."""
+        x = self._x
+        return (x.recv_flats, x.recv_codes, x.recv_thetas, x.fitness, x.elite)
+
+    def ipc_handles(self) -> bytes:
+        buf = (ctypes.c_char * (_lib.PEER_BUFFERS * _lib.IPC_HANDLE_BYTES))()
+        self._call("ipc_export", buf)
+        return bytes(buf)
+
+    def open_peers_ipc(self, all_handles):
+        raw = b"".join(all_handles)
+        buf = (ctypes.c_char * len(raw)).from_buffer_copy(raw)
+        self._call("ipc_open", buf)
+        self.connected = True
+
+    def set_peer_pointers(self, all_buffers):
+        """Peers already addressable in this process (several ranks' handles
+        on one device, tests/test_sharded_gpu.py)."""
+        arr = (_lib.PeerBuffers * self.world)(*[_lib.PeerBuffers(*b) for b in all_buffers])
+        self._call("set_peers", arr)
+        self.connected = True
+
     def generation(self, comm: Optional[Comm], marks=None):
         """One generation; `marks` (4 torch.cuda.Events, optional) are recorded
         on the handle's stream before prepare, before score, after score and
         after finish (bench.py phase timing)."""
+        if self.transport == "p2p" and self.world > 1:
+            return self._generation_p2p(comm, marks)
         r = self.routing
         if marks:
             marks[0].record(self.stream)
@@ -223,6 +292,26 @@ class DeviceQeqeaOps(_DeviceOps):
         if marks:
             marks[3].record(self.stream)
 
+    def _generation_p2p(self, comm, marks):
+        if not self.connected:
+            comm.connect_peers(self)
+        if marks:
+            marks[0].record(self.stream)
+        comm.barrier()           # every rank is done reading last generation's buffers
+        self._call("prepare")    # touches -> owners' recv_flats
+        comm.barrier()
+        self._call("values")     # codes / angles -> circuit ranks' recv buffers
+        comm.barrier()
+        if marks:
+            marks[1].record(self.stream)
+        self._call("score")      # fitness + elite -> every rank
+        if marks:
+            marks[2].record(self.stream)
+        comm.barrier()
+        self._call("finish")
+        if marks:
+            marks[3].record(self.stream)
+
 
 class DeviceGaOps(_DeviceOps):
     _prefix = "ga"
@@ -241,7 +330,7 @@ class DeviceGaOps(_DeviceOps):
         self._call("finish")
 
 
-def sharded_qeqea(cfg, target, seed: int, group=None, **kw) -> ShardedRunner:
+def sharded_qeqea(cfg, target, seed: int, group=None, transport: str = "p2p", **kw) -> ShardedRunner:
     """A QEQEA run sharded over the process group (one GPU per rank)."""
     import torch
     import torch.distributed as dist
@@ -251,7 +340,7 @@ def sharded_qeqea(cfg, target, seed: int, group=None, **kw) -> ShardedRunner:
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     dev = torch.cuda.current_device()
     eng = QeqeaEngine(cfg, target, seed, device=dev, rank=rank, world=world, **kw)
-    runner = ShardedRunner(DeviceQeqeaOps(eng), group)
+    runner = ShardedRunner(DeviceQeqeaOps(eng, transport), group)
     runner.engine = eng
     return runner
 

@@ -45,6 +45,18 @@ class LockstepComm:
                     pos += n
                 outer.barrier.wait()
 
+            def barrier(self):
+                import torch
+
+                torch.cuda.synchronize()
+                outer.barrier.wait()
+
+            def connect_peers(self, ops):
+                outer.slots[rank] = ops.peer_buffers()
+                outer.barrier.wait()
+                ops.set_peer_pointers(list(outer.slots))
+                outer.barrier.wait()
+
             def all_gather(self, full, chunk):
                 outer.slots[rank] = full
                 outer.barrier.wait()
@@ -56,7 +68,7 @@ class LockstepComm:
         return _View()
 
 
-def _run_sharded(cfg, target, seed, world, gens):
+def _run_sharded(cfg, target, seed, world, gens, transport="nccl"):
     import torch
 
     from paper_1809_11134_b200.distributed import DeviceQeqeaOps, ShardedRunner
@@ -67,7 +79,7 @@ def _run_sharded(cfg, target, seed, world, gens):
     out = [None] * world
 
     def worker(r):
-        ops = DeviceQeqeaOps(engines[r])
+        ops = DeviceQeqeaOps(engines[r], transport)
         runner = ShardedRunner(ops, comm=comm.rank_view(r))
         rec = runner.steps(gens)
         torch.cuda.synchronize()
@@ -81,9 +93,12 @@ def _run_sharded(cfg, target, seed, world, gens):
     return engines, out
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("n,L,P,gens,world", [(3, 16, 64, 30, 2), (3, 16, 61, 30, 3), (5, 64, 256, 8, 2),
                                               (4, 32, 100, 12, 4)])
-def test_sharded_matches_single_rank(n, L, P, gens, world):
+def test_sharded_matches_single_rank(n, L, P, gens, world, transport):
+    """transport="nccl": collectives between the phases (emulated by copies);
+    "p2p": the kernels store into the other ranks' buffers themselves."""
     from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
     from paper_1809_11134_b200.fitness import TargetSpec
 
@@ -93,7 +108,7 @@ def test_sharded_matches_single_rank(n, L, P, gens, world):
     spec = TargetSpec("haar", n, T)
     ref = QeqeaEngine(cfg, spec, seed=3)
     rrec = ref.steps(gens)
-    engines, out = _run_sharded(cfg, spec, 3, world, gens)
+    engines, out = _run_sharded(cfg, spec, 3, world, gens, transport)
     for r, (rec, stop, generation) in enumerate(out):
         assert generation == gens and stop == "generation-limit"
         assert np.array_equal(rec["gen_best"], rrec["gen_best"]), r
@@ -110,3 +125,60 @@ def test_sharded_matches_single_rank(n, L, P, gens, world):
         assert np.array_equal(pop.qutrits, full.qutrits[rot])
         seen[slots] = True
     assert seen.all()
+
+
+def _ipc_worker(rank, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    from paper_1809_11134_b200.distributed import sharded_qeqea
+    from paper_1809_11134_b200.engine import PopulationConfig
+    from paper_1809_11134_b200.fitness import TargetSpec
+
+    T = random_unitary(16, np.random.default_rng(77))
+    cfg = PopulationConfig(number_of_wires=4, size_of_individual=16, size_of_population=40,
+                           max_generations=20, target_fitness=1.0)
+    run = sharded_qeqea(cfg, TargetSpec("haar", 4, T), 5, transport="p2p")
+    rec = run.steps(20)
+    q.put((rank, rec["gen_best"].tolist(), rec["gen_mean"].tolist(), run.stop_reason))
+    run.engine.close()
+    dist.destroy_process_group()
+
+
+def test_p2p_transport_over_cuda_ipc_two_processes():
+    """Two processes on the one GPU map each other's exchange buffers with
+    CUDA IPC (isq_qeqea_ipc_export / _ipc_open) and run the peer transport,
+    ordered by host barriers (gloo): the trajectory equals one rank's."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
+    from paper_1809_11134_b200.fitness import TargetSpec
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get() for _ in range(2)])
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    T = random_unitary(16, np.random.default_rng(77))
+    cfg = PopulationConfig(number_of_wires=4, size_of_individual=16, size_of_population=40,
+                           max_generations=20, target_fitness=1.0)
+    ref = QeqeaEngine(cfg, TargetSpec("haar", 4, T), 5).steps(20)
+    for rank, gb, gm, stop in res:
+        assert gb == list(ref["gen_best"]) and gm == list(ref["gen_mean"]), rank
+        assert stop == "generation-limit"
