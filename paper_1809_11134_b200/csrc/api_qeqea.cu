@@ -109,6 +109,11 @@ static isq_status validate(const isq_qeqea_config* c) {
     }                                                                \
   } while (0)
 
+static isq_status null_handle() {
+  set_error("null engine handle");
+  return ISQ_ERR_CONFIG;
+}
+
 }  // namespace isq
 
 using namespace isq;
@@ -223,6 +228,7 @@ isq_status isq_qeqea_destroy(void* handle) {
 
 isq_status isq_qeqea_set_stream(void* handle, void* stream) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -233,6 +239,7 @@ isq_status isq_qeqea_set_stream(void* handle, void* stream) {
 
 isq_status isq_qeqea_begin_batch(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   // rec_base := generation (device-side copy, stream ordered)
   ISQ_CUDA_TRY(cudaMemcpyAsync(&h->a.st->rec_base, &h->a.st->generation, 8,
@@ -248,6 +255,7 @@ static isq_status need_world1(const QeqeaHandle* h, const char* what) {
 
 isq_status isq_qeqea_eval(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   isq_status st = need_world1(h, "isq_qeqea_eval");
   if (st != ISQ_OK) return st;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
@@ -256,30 +264,35 @@ isq_status isq_qeqea_eval(void* handle) {
 
 isq_status isq_qeqea_prepare(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   return qeqea_launch_prepare(h->a, h->stream);
 }
 
 isq_status isq_qeqea_values(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   return qeqea_launch_values(h->a, h->stream);
 }
 
 isq_status isq_qeqea_score(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   return qeqea_launch_score(h->a, h->stream);
 }
 
 isq_status isq_qeqea_finish(void* handle) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   return qeqea_launch_finish(h->a, h->stream);
 }
 
 isq_status isq_qeqea_set_peers(void* handle, const isq_qeqea_peer_buffers* peers) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   if (peers == nullptr) {
@@ -316,6 +329,7 @@ isq_status isq_qeqea_set_peers(void* handle, const isq_qeqea_peer_buffers* peers
 
 isq_status isq_qeqea_ipc_export(void* handle, isq_ipc_handle* out) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   const QeqeaArgs& a = h->a;
   if (h->world < 2) {
     set_error("the peer transport needs world > 1");
@@ -334,6 +348,7 @@ isq_status isq_qeqea_ipc_export(void* handle, isq_ipc_handle* out) {
 
 isq_status isq_qeqea_ipc_open(void* handle, const isq_ipc_handle* all) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   const QeqeaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   close_peers(h);
@@ -367,6 +382,7 @@ isq_status isq_qeqea_ipc_open(void* handle, const isq_ipc_handle* all) {
 
 isq_status isq_qeqea_exchange(void* handle, isq_qeqea_exchange_buffers* x) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   const QeqeaArgs& a = h->a;
   std::memset(x, 0, sizeof(*x));
   x->world = a.world;
@@ -389,6 +405,7 @@ isq_status isq_qeqea_exchange(void* handle, isq_qeqea_exchange_buffers* x) {
 isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
                                 int32_t* stop_reason, uint64_t* generation, double* best_fitness) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaMemcpyAsync(h->h_state, h->a.st, sizeof(QeqeaDevState), cudaMemcpyDeviceToHost,
                                h->stream));
@@ -411,6 +428,7 @@ isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, in
 isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_record* records,
                           int32_t* n_done, int32_t* stop_reason) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   isq_status st0 = need_world1(h, "isq_qeqea_step");
   if (st0 != ISQ_OK) return st0;
   if (n_generations > h->max_batch) {
@@ -440,6 +458,7 @@ isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_re
 
 isq_status isq_qeqea_set_launch_mode(void* handle, int32_t mode) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   if (mode < ISQ_LAUNCH_AUTO || mode > ISQ_LAUNCH_FUSED) {
     set_error("unknown launch mode");
     return ISQ_ERR_CONFIG;
@@ -451,6 +470,7 @@ isq_status isq_qeqea_set_launch_mode(void* handle, int32_t mode) {
 isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len,
                              void** stream) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   if (fitness_dev) *fitness_dev = h->a.fitness;
   if (shard_len) *shard_len = h->shard;
   if (stream) *stream = h->stream;
@@ -459,6 +479,7 @@ isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_le
 
 isq_status isq_qeqea_best(void* handle, uint8_t* codes, double* thetas, double* fitness) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   ISQ_CUDA_TRY(cudaMemcpy(codes, h->a.best_codes, h->a.L, cudaMemcpyDeviceToHost));
@@ -488,6 +509,7 @@ struct SoaTemps {
 isq_status isq_qeqea_get_state(void* handle, double* theta, double* qamp, double* slot_max,
                                uint64_t* generation, double* best_fitness, int32_t* stop) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   const QeqeaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -513,6 +535,7 @@ isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* 
                                const double* slot_max, uint64_t generation, double best_fitness,
                                int32_t stop, const uint8_t* best_codes, const double* best_thetas) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   const QeqeaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -545,6 +568,7 @@ isq_status isq_qeqea_set_state(void* handle, const double* theta, const double* 
 
 isq_status isq_qeqea_live_population(void* handle, double* theta, double* qutrits) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   const QeqeaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   double *d_t = nullptr, *d_q = nullptr;
@@ -573,6 +597,7 @@ isq_status isq_qeqea_live_population(void* handle, double* theta, double* qutrit
 isq_status isq_qeqea_sample(void* handle, int64_t c0, int64_t c1, int64_t* flats, uint8_t* codes,
                             double* thetas) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   const QeqeaArgs& a = h->a;
   isq_status st0 = need_world1(h, "isq_qeqea_sample");
   if (st0 != ISQ_OK) return st0;
@@ -608,6 +633,7 @@ isq_status isq_qeqea_sample(void* handle, int64_t c0, int64_t c1, int64_t* flats
 
 isq_status isq_qeqea_fitness(void* handle, double* out) {
   QeqeaHandle* h = static_cast<QeqeaHandle*>(handle);
+  if (!h) return null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   ISQ_CUDA_TRY(cudaMemcpy(out, h->a.fitness, h->a.P * 8, cudaMemcpyDeviceToHost));

@@ -446,6 +446,11 @@ using namespace isq;
     }                                                                \
   } while (0)
 
+static isq_status ga_null_handle() {
+  set_error("null engine handle");
+  return ISQ_ERR_CONFIG;
+}
+
 extern "C" {
 
 isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t device,
@@ -534,6 +539,7 @@ isq_status isq_ga_destroy(void* handle) {
 
 isq_status isq_ga_set_stream(void* handle, void* stream) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -544,6 +550,7 @@ isq_status isq_ga_set_stream(void* handle, void* stream) {
 
 isq_status isq_ga_begin_batch(void* handle) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaMemcpyAsync(&h->a.st->rec_base, &h->a.st->generation, 8,
                                cudaMemcpyDeviceToDevice, h->stream));
@@ -552,6 +559,7 @@ isq_status isq_ga_begin_batch(void* handle) {
 
 isq_status isq_ga_eval(void* handle) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   const int64_t c0 = h->rank * h->shard;
   const int64_t c1 = c0 + h->shard < h->a.P ? c0 + h->shard : h->a.P;
@@ -560,6 +568,7 @@ isq_status isq_ga_eval(void* handle) {
 
 isq_status isq_ga_finish(void* handle) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   return ga_launch_finish(h->a, h->stream);
 }
@@ -567,6 +576,7 @@ isq_status isq_ga_finish(void* handle) {
 isq_status isq_ga_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
                              int32_t* stop_reason, uint64_t* generation, double* best_fitness) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   GaDevState s;
@@ -585,6 +595,7 @@ isq_status isq_ga_read_batch(void* handle, isq_generation_record* records, int32
 isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, int32_t* n_done,
                        int32_t* stop_reason) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   if (h->world != 1) {
     set_error("isq_ga_step drives a single rank; use eval / all-gather / finish for world > 1");
     return ISQ_ERR_CONFIG;
@@ -620,6 +631,7 @@ isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, 
 
 isq_status isq_ga_set_launch_mode(void* handle, int32_t mode) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   if (mode < ISQ_LAUNCH_AUTO || mode > ISQ_LAUNCH_FUSED) {
     set_error("unknown launch mode");
     return ISQ_ERR_CONFIG;
@@ -630,6 +642,7 @@ isq_status isq_ga_set_launch_mode(void* handle, int32_t mode) {
 
 isq_status isq_ga_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   if (fitness_dev) *fitness_dev = h->a.fitness;
   if (shard_len) *shard_len = h->shard;
   if (stream) *stream = h->stream;
@@ -638,6 +651,7 @@ isq_status isq_ga_buffers(void* handle, void** fitness_dev, int64_t* shard_len, 
 
 isq_status isq_ga_best(void* handle, uint8_t* codes, double* thetas, double* fitness) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   ISQ_CUDA_TRY(cudaMemcpy(codes, h->a.best_codes, h->a.L, cudaMemcpyDeviceToHost));
@@ -651,6 +665,7 @@ isq_status isq_ga_best(void* handle, uint8_t* codes, double* thetas, double* fit
 isq_status isq_ga_get_state(void* handle, uint8_t* codes, double* thetas, uint64_t* generation,
                             double* best_fitness, int32_t* stop) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   const GaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -669,6 +684,7 @@ isq_status isq_ga_set_state(void* handle, const uint8_t* codes, const double* th
                             uint64_t generation, double best_fitness, int32_t stop,
                             const uint8_t* best_codes, const double* best_thetas) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   const GaArgs& a = h->a;
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -695,6 +711,7 @@ isq_status isq_ga_set_state(void* handle, const uint8_t* codes, const double* th
 
 isq_status isq_ga_fitness(void* handle, double* out) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   ISQ_CUDA_TRY(cudaMemcpy(out, h->a.fitness, h->a.P * 8, cudaMemcpyDeviceToHost));
@@ -703,6 +720,7 @@ isq_status isq_ga_fitness(void* handle, double* out) {
 
 isq_status isq_ga_parents(void* handle, int32_t* out) {
   GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
   ISQ_CUDA_TRY(cudaSetDevice(h->device));
   ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
   ISQ_CUDA_TRY(cudaMemcpy(out, h->a.parents, h->a.P * 4, cudaMemcpyDeviceToHost));

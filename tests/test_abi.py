@@ -92,3 +92,13 @@ def test_unsupported_shapes_are_reported_not_computed():
     assert st == _lib.ISQ_ERR_UNSUPPORTED
     with pytest.raises(ConfigurationError):
         _lib.check(st)
+
+
+def test_null_handles_are_rejected():
+    from paper_1809_11134_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.isq_qeqea_begin_batch(None) == _lib.ISQ_ERR_CONFIG
+    assert lib.isq_ga_begin_batch(None) == _lib.ISQ_ERR_CONFIG
+    assert b"null" in lib.isq_last_error()
+    assert lib.isq_qeqea_destroy(None) == _lib.ISQ_OK
