@@ -334,8 +334,14 @@ def run_ours(args):
             torch.cuda.synchronize()
         fms = start.elapsed_time(end)
         fit_ms = sum(e[1].elapsed_time(e[2]) for e in fev) / args.steps
+        p32 = ctypes.c_double()
+        _lib.check(lib.isq_fma_peak(0, local, ctypes.cast(ctypes.pointer(p32), ctypes.c_void_p)))
+        a32 = canonical_flops(N, L) * P / (fit_ms * 1e-3) / 1e12
         var = {"value": P * args.steps / (fms * 1e-3), "unit": "evals/s", "ms_per_step": fms / args.steps,
                "fitness_kernel_ms": fit_ms,
+               "roofline": {"bound": "fp32", "achieved": a32, "peak": p32.value / 1e12, "unit": "TFLOP/s",
+                            "frac": a32 / (p32.value / 1e12),
+                            "peak_source": "FP32 CUDA-core FMA peak measured live by isq_fma_peak"},
                "bound": "|fit32 - fit64| <= 1e-4 |fit64| + 1e-6 (tests/test_fitness_gpu.py)"}
         fe.close()
         if not args.skip_e2e:
