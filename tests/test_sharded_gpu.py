@@ -182,3 +182,39 @@ def test_p2p_transport_over_cuda_ipc_two_processes():
     for rank, gb, gm, stop in res:
         assert gb == list(ref["gen_best"]) and gm == list(ref["gen_mean"]), rank
         assert stop == "generation-limit"
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_ga_matches_single_rank(world):
+    """GA sharding (replicated genomes, genome shards scored per rank, fitness
+    all-gathered) reproduces the single-rank GA bit for bit."""
+    import torch
+
+    from paper_1809_11134_b200.distributed import DeviceGaOps, ShardedRunner
+    from paper_1809_11134_b200.fitness import target_matrix
+    from paper_1809_11134_b200.ga import GaConfig, GaEngine
+
+    cfg = GaConfig(number_of_wires=3, size_of_individual=16, population=61, max_generations=25)
+    t = target_matrix("Toffoli")
+    ref = GaEngine(cfg, t, seed=8)
+    rrec = ref.steps(25)
+    comm = LockstepComm(world)
+    engines = [GaEngine(cfg, t, seed=8, rank=r, world=world, max_batch=8) for r in range(world)]
+    out = [None] * world
+
+    def worker(r):
+        runner = ShardedRunner(DeviceGaOps(engines[r]), comm=comm.rank_view(r))
+        out[r] = runner.steps(25)
+        torch.cuda.synchronize()
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    for r in range(world):
+        assert np.array_equal(out[r]["gen_best"], rrec["gen_best"]), r
+        assert np.array_equal(out[r]["gen_mean"], rrec["gen_mean"]), r
+        c, th_ = engines[r].genome_arrays()
+        rc, rt = ref.genome_arrays()
+        assert np.array_equal(c, rc) and np.array_equal(th_, rt)
