@@ -102,3 +102,18 @@ def test_null_handles_are_rejected():
     assert lib.isq_ga_begin_batch(None) == _lib.ISQ_ERR_CONFIG
     assert b"null" in lib.isq_last_error()
     assert lib.isq_qeqea_destroy(None) == _lib.ISQ_OK
+
+
+def test_c_host_example_compiles_against_the_header(tmp_path):
+    """examples/qeqea_host.c builds against include/isq.h + libisq.so with a
+    plain C compiler (no CUDA or torch headers in the ABI)."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc") or shutil.which("cc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    lib = ROOT / "paper_1809_11134_b200"
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+                    str(ROOT / "examples" / "qeqea_host.c"), "-L", str(lib), "-lisq", f"-Wl,-rpath,{lib}",
+                    "-o", str(tmp_path / "qeqea_host")], check=True)
