@@ -1,0 +1,49 @@
+"""The reference's acceptance criteria on the device engines
+(pkg/tests/test_acceptance.py criteria 1-3; recorded outcomes in
+pkg/test_output.txt:12-18).  Counter-based streams make the individual runs
+differ from the reference's PCG64 runs; the outcomes must not."""
+import math
+import statistics
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SEEDS = (1, 2, 3, 4, 5)
+CNOT_L3_CAP = 1 - math.sqrt(1 - math.sqrt(2) / 2)  # 0.4588..., test_output.txt:12
+
+
+def _run(engine):
+    while not engine.done:
+        engine.steps(4096)
+    return engine.best_fitness, engine.generation
+
+
+def test_criterion_1_qeqea_cnot_reaches_the_length3_cap():
+    from paper_1809_11134_b200 import PopulationConfig, QeqeaEngine, target_matrix
+
+    for s in SEEDS:
+        best, gen = _run(QeqeaEngine(PopulationConfig(2, 3, 5, max_generations=50_000, target_fitness=0.999),
+                                     target_matrix("CNOT"), s))
+        assert CNOT_L3_CAP - 1e-3 < best <= CNOT_L3_CAP + 1e-12, (s, best)
+        assert gen == 50_000
+
+
+def test_criterion_2_ga_synthesizes_cnot_in_every_seed():
+    from paper_1809_11134_b200 import GaConfig, GaEngine, target_matrix
+
+    for s in SEEDS:
+        best, gen = _run(GaEngine(GaConfig(2, 6, 50, mutation_rate=0.2, mutation_range=math.pi / 8,
+                                           structural_rate=0.2, max_generations=10_000, target_fitness=0.999),
+                                  target_matrix("CNOT"), s))
+        assert best >= 0.999 and gen < 10_000, (s, best, gen)
+
+
+def test_criterion_3_ga_beats_qeqea_on_toffoli():
+    from paper_1809_11134_b200 import GaConfig, GaEngine, PopulationConfig, QeqeaEngine, target_matrix
+
+    t = target_matrix("Toffoli")
+    ga = [_run(GaEngine(GaConfig(3, 16, 50, max_generations=20_000), t, s))[0] for s in SEEDS]
+    qe = [_run(QeqeaEngine(PopulationConfig(3, 16, 5, max_generations=20_000), t, s))[0] for s in SEEDS]
+    assert statistics.median(ga) >= statistics.median(qe)
+    assert 0.40 < statistics.median(qe) < 0.55  # the reference's plateau (README: 0.45-0.52)
