@@ -31,6 +31,20 @@ __global__ void gather(const uint4* __restrict__ tab, uint64_t nrec, int64_t n, 
   if (acc == 1.2345) out[0] = acc;
 }
 
+// 64 B records read with two 256-bit loads (sm_100 LDG.256) instead of four 128-bit ones
+__global__ void gather64_v256(const double* __restrict__ tab, uint64_t nrec, int64_t n, double* out) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix(i * 0x9E3779B97F4A7C15ULL) % nrec;
+    const double* p = tab + r * 16;
+    double a, b, c, d, e, f, g, h;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(e), "=d"(f), "=d"(g), "=d"(h) : "l"(p + 4));
+    acc += a + b + c + d + e + f + g + h;
+  }
+  if (acc == 1.2345) out[0] = acc;
+}
+
 __global__ void rmw(unsigned long long* tab, uint64_t nrec, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t r = mix(i * 0x9E3779B97F4A7C15ULL) % nrec;
@@ -68,6 +82,7 @@ int main() {
   run("gather32", [&] { gather<32><<<grid, blk>>>(tab, nrec, n, out); });
   run("gather64", [&] { gather<64><<<grid, blk>>>(tab, nrec, n, out); });
   run("gather128", [&] { gather<128><<<grid, blk>>>(tab, nrec, n, out); });
+  run("gather64v256", [&] { gather64_v256<<<grid, blk>>>((const double*)tab, nrec, n, out); });
   run("atomicmax8", [&] { rmw<<<grid, blk>>>((unsigned long long*)tab, nrec, n); });
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
