@@ -60,7 +60,10 @@ isq_status isq_fitness_batch(int32_t n, int32_t length, int64_t count, const uin
                              const double* thetas, const double* target, double* fitness_out,
                              double* unitary_out, int32_t device);
 
-/* Same on device pointers, enqueued on `stream` (cudaStream_t, may be NULL). */
+/* Same on device pointers, enqueued on `stream` (cudaStream_t, may be NULL).
+ * Asynchronous: a circuit holding a code that is not a gate of this wire
+ * count gets a NaN fitness (the host-buffer entry points return
+ * ISQ_ERR_CONFIG instead). */
 isq_status isq_fitness_batch_device(int32_t n, int32_t length, int64_t count,
                                     const uint8_t* codes_dev, const double* thetas_dev,
                                     const double* target_dev, double* fitness_dev,

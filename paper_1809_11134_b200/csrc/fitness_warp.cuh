@@ -92,7 +92,7 @@ struct FastEval {
         b = rb;
         type = axis == 0 ? GT_RX : GT_RY;
       }
-    } else {
+    } else if (code < G::NCODES) {
       int i = 1, tt = code - 3 * NQ;
       while (tt >= NQ - i) {
         tt -= NQ - i;
@@ -100,6 +100,8 @@ struct FastEval {
       }
       const int j = i + 1 + tt;
       mask = (1 << (NQ - i)) | (1 << (NQ - j));
+    } else {
+      mask = 0;  // not a gate of this wire count: the chunk reports it (NaN fitness)
     }
     double x = theta;
     if (b >= 0) {
@@ -192,10 +194,12 @@ struct FastEval {
   // The rotation positions are found with one ballot; the diagonal runs
   // between them touch only the pending phase (diag_run), the rotations
   // flush the non-commuting part of it and rotate the register state.
-  __device__ __forceinline__ void chunk(int code, double theta, int nq, Chunk& sm, int lane) {
+  // Returns true (warp-uniform) when a lane's code is not a valid gate code.
+  __device__ __forceinline__ bool chunk(int code, double theta, int nq, Chunk& sm, int lane) {
     int info = GT_DIAG, dmask = 0;  // lanes past the end: neutral diagonal, empty mask
     R2 e0 = Cplx<R>::make(R(1), R(0)), e1 = e0;
     if (lane < nq) prepare(code, theta, info, dmask, e0, e1);
+    const bool bad = __any_sync(0xffffffffu, lane < nq && (code < 0 || code >= G::NCODES));
     sm.info[lane] = info;
     sm.dmask[lane] = dmask;
     sm.cs2[lane][0] = e0;
@@ -243,6 +247,7 @@ struct FastEval {
       }
     }
     __syncwarp();
+    return bad;
   }
 
   // Fitness from the final state (fitness.py:36-49).
@@ -307,7 +312,8 @@ template <int NQ, class R = double>
 __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t* __restrict__ codes,
                                              const double* __restrict__ thetas,
                                              const double2* __restrict__ Ts, FastChunkT<R>* sh,
-                                             double* __restrict__ fitness, int warps_per_block) {
+                                             double* __restrict__ fitness, int warps_per_block,
+                                             int* bad_code = nullptr) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   FastChunkT<R>& cs = sh[wib];
@@ -317,6 +323,7 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
   for (; c < count; c += nwarps) {
     FastEval<NQ, R> ev;
     ev.begin(lane);
+    bool bad = false;
     for (int base = 0; base < L; base += 32) {
       const int nq = min(32, L - base);
       asm volatile("cp.async.wait_all;\n" ::);
@@ -335,10 +342,13 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
         nb = 0;
       }
       stage_chunk(cs, count, L, codes, thetas, nc, nb, lane);
-      ev.chunk(code, th, nq, cs, lane);
+      bad |= ev.chunk(code, th, nq, cs, lane);
     }
     const double f = ev.finish(Ts, cs, lane);
-    if (lane == 0) fitness[c] = f;
+    if (lane == 0) {
+      fitness[c] = bad ? __longlong_as_double(0x7ff8000000000000LL) : f;  // NaN: invalid gate code
+      if (bad && bad_code) atomicOr(bad_code, 1);
+    }
   }
 }
 

@@ -76,6 +76,7 @@ struct BatchContext {
   double* thetas[2] = {nullptr, nullptr};
   double* fit[2] = {nullptr, nullptr};
   double* target = nullptr;
+  int* bad = nullptr;             // device flag: an invalid gate code was seen
   unsigned char* unit = nullptr;  // compose output (not pipelined)
   size_t cap_rows = 0, cap_len = 0, cap_unit = 0;
   cudaEvent_t loaded[2], done[2];
@@ -109,8 +110,10 @@ static isq_status fitness_batch_host(int32_t n, int32_t length, int64_t count, c
   isq_status st = check_shape(n, length, count);
   if (st != ISQ_OK) return st;
   const int64_t total = count * (int64_t)length;
-  st = check_codes(n, codes, total);
-  if (st != ISQ_OK) return st;
+  if (unitary_out) {  // readout path: codes checked on the host
+    st = check_codes(n, codes, total);
+    if (st != ISQ_OK) return st;
+  }
   if (count == 0) return ISQ_OK;
   ISQ_CUDA_TRY(cudaSetDevice(device));
   BatchContext* c = batch_context(device);
@@ -164,7 +167,10 @@ static isq_status fitness_batch_host(int32_t n, int32_t length, int64_t count, c
     }
     return ISQ_OK;
   }
-  // pipelined: copy stream loads chunk i into buffer i%2 while comp scores chunk i-1
+  // pipelined: copy stream loads chunk i into buffer i%2 while comp scores chunk i-1;
+  // gate codes are validated by the fitness kernel itself (device flag)
+  if (!c->bad) ISQ_CUDA_TRY(cudaMalloc((void**)&c->bad, sizeof(int)));
+  ISQ_CUDA_TRY(cudaMemsetAsync(c->bad, 0, sizeof(int), c->comp));
   int64_t i = 0;
   for (int64_t off = 0; off < count; off += chunk, ++i) {
     const int b = (int)(i & 1);
@@ -179,12 +185,15 @@ static isq_status fitness_batch_host(int32_t n, int32_t length, int64_t count, c
     ISQ_CUDA_TRY(cudaEventRecord(c->loaded[b], c->copy));
     ISQ_CUDA_TRY(cudaStreamWaitEvent(c->comp, c->loaded[b], 0));
     st = launch_fitness_batch(n, length, m, c->codes[b], c->thetas[b], c->target, c->fit[b],
-                              nullptr, c->comp, precision);
+                              nullptr, c->comp, precision, c->bad);
     if (st != ISQ_OK) return st;
     ISQ_CUDA_TRY(cudaMemcpyAsync(fitness_out + off, c->fit[b], m * 8, cudaMemcpyDeviceToHost, c->comp));
     ISQ_CUDA_TRY(cudaEventRecord(c->done[b], c->comp));
   }
+  int bad = 0;
+  ISQ_CUDA_TRY(cudaMemcpyAsync(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->comp));
   ISQ_CUDA_TRY(cudaStreamSynchronize(c->comp));
+  if (bad) return check_codes(n, codes, total);  // locate it for the message
   return ISQ_OK;
 }
 

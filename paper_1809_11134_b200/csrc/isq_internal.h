@@ -38,14 +38,17 @@ int persistent_grid(const void* kernel, size_t dyn_smem, int64_t work_warps,
 isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* codes,
                                 const double* thetas, const double* target_dev,
                                 double* fitness_dev, double* unitary_dev, cudaStream_t stream,
-                                int precision = ISQ_PRECISION_FP64);
+                                int precision = ISQ_PRECISION_FP64, int* bad_code = nullptr);
 
 // fitness-only batch that skips all work once *stop != 0 (engine generations).
 isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
                                           const double* thetas, const double* target_dev,
                                           double* fitness_dev, const int32_t* stop,
                                           cudaStream_t stream, int blocks_per_sm = 0,
-                                          int precision = ISQ_PRECISION_FP64);
+                                          int precision = ISQ_PRECISION_FP64,
+                                          int* bad_code = nullptr);
+// Circuits holding a code that is not a gate of the wire count get a NaN
+// fitness, and *bad_code (device int, nullable) is set to 1.
 
 // Launch-bound small populations: `per_graph` generations captured once into
 // a CUDA graph (on a private capture stream, so the caller's stream may be the

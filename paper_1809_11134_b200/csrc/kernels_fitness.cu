@@ -26,14 +26,14 @@ template <int NQ, int MINB, class R>
 __global__ void ISQ_FIT_BOUNDS
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
-                        double* __restrict__ fitness, const int32_t* __restrict__ stop) {
+                        double* __restrict__ fitness, const int32_t* __restrict__ stop, int* bad_code) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
   __shared__ FastChunkT<R> sh[kFitWarps];
   if (stop != nullptr && *stop) return;
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
   __syncthreads();
-  fitness_rows<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps);
+  fitness_rows<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps, bad_code);
 }
 
 // fp32 variant: the column of S in 64 float registers: 8 resident 2-warp
@@ -190,12 +190,12 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
 template <int NQ, int MINB, class R>
 static isq_status launch_fast(int L, int64_t count, const uint8_t* codes, const double* thetas,
                               const double* target, double* fitness, const int32_t* stop,
-                              int blocks_per_sm, cudaStream_t stream) {
+                              int blocks_per_sm, cudaStream_t stream, int* bad_code) {
   const void* k = (const void*)fitness_fast_kernel<NQ, MINB, R>;
   int grid = persistent_grid(k, 0, count, kFitWarps);
   if (blocks_per_sm > 0 && grid > num_sms() * blocks_per_sm) grid = num_sms() * blocks_per_sm;
   fitness_fast_kernel<NQ, MINB, R><<<grid, kFitThreads, 0, stream>>>(
-      count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop);
+      count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop, bad_code);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
@@ -203,25 +203,27 @@ static isq_status launch_fast(int L, int64_t count, const uint8_t* codes, const 
 template <int NQ>
 static isq_status launch_fast_prec(int L, int64_t count, const uint8_t* codes, const double* thetas,
                                    const double* target, double* fitness, const int32_t* stop,
-                                   int blocks_per_sm, int precision, cudaStream_t stream) {
+                                   int blocks_per_sm, int precision, cudaStream_t stream, int* bad) {
   if (precision == ISQ_PRECISION_FP32)
     return launch_fast<NQ, kFitMinBlocks32, float>(L, count, codes, thetas, target, fitness, stop,
-                                                    blocks_per_sm, stream);
+                                                    blocks_per_sm, stream, bad);
   return launch_fast<NQ, kFitMinBlocks64, double>(L, count, codes, thetas, target, fitness, stop,
-                                                  blocks_per_sm, stream);
+                                                  blocks_per_sm, stream, bad);
 }
 
 isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
                                           const double* thetas, const double* target,
                                           double* fitness, const int32_t* stop,
-                                          cudaStream_t stream, int blocks_per_sm, int precision) {
+                                          cudaStream_t stream, int blocks_per_sm, int precision,
+                                          int* bad_code) {
   if (count <= 0) return ISQ_OK;
   const int b = blocks_per_sm, p = precision;
+  int* bc = bad_code;
   switch (n) {
-    case 2: return launch_fast_prec<2>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
-    case 3: return launch_fast_prec<3>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
-    case 4: return launch_fast_prec<4>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
-    case 5: return launch_fast_prec<5>(L, count, codes, thetas, target, fitness, stop, b, p, stream);
+    case 2: return launch_fast_prec<2>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
+    case 3: return launch_fast_prec<3>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
+    case 4: return launch_fast_prec<4>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
+    case 5: return launch_fast_prec<5>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
     default:
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;
@@ -230,11 +232,11 @@ isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uin
 
 isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* codes,
                                 const double* thetas, const double* target, double* fitness,
-                                double* unitary, cudaStream_t stream, int precision) {
+                                double* unitary, cudaStream_t stream, int precision, int* bad_code) {
   if (count <= 0) return ISQ_OK;
   if (unitary == nullptr)
     return launch_fitness_batch_stoppable(n, L, count, codes, thetas, target, fitness, nullptr, stream,
-                                          0, precision);
+                                          0, precision, bad_code);
   switch (n) {  // composition readout: always fp64
     case 2: return launch_nq<2>(L, count, codes, thetas, target, fitness, unitary, stream);
     case 3: return launch_nq<3>(L, count, codes, thetas, target, fitness, unitary, stream);

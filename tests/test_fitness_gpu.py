@@ -135,3 +135,35 @@ def test_fp32_variant_matches_oracle_random(n, L):
     out = fitness_batch(codes, thetas, T, n, precision="fp32")
     ref = np.array([O.circuit_fitness(codes[c], thetas[c], T, n) for c in range(count)])
     assert (np.abs(out - ref) <= FP32_RTOL * np.abs(ref) + FP32_ATOL).all()
+
+
+def test_invalid_gate_codes_fail_loudly():
+    """A code outside the wire count's gate set: ConfigurationError from the
+    host-buffer API (validated on the device, not by a host scan), NaN for
+    exactly that circuit from the device API."""
+    import torch
+
+    from paper_1809_11134_b200 import _lib
+    from paper_1809_11134_b200.errors import ConfigurationError
+    from paper_1809_11134_b200.fitness import fitness_batch
+
+    rng = np.random.default_rng(3)
+    codes = rng.integers(0, 12, size=(40, 16)).astype(np.uint8)
+    thetas = rng.uniform(0, 2 * math.pi, size=(40, 16))
+    T = random_unitary(8, rng)
+    good = fitness_batch(codes, thetas, T, 3)
+    bad = codes.copy()
+    bad[17, 5] = 12  # n = 3 has 12 gate choices (ga.py:47-59)
+    with pytest.raises(ConfigurationError):
+        fitness_batch(bad, thetas, T, 3)
+    dev = torch.device("cuda:0")
+    c = torch.from_numpy(bad).to(dev)
+    t = torch.from_numpy(thetas).to(dev)
+    tt = torch.from_numpy(np.ascontiguousarray(T)).to(dev)
+    out = torch.empty(40, dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.isq_fitness_batch_device_ex(3, 16, 40, c.data_ptr(), t.data_ptr(), tt.data_ptr(),
+                                               out.data_ptr(), 0, None))
+    got = out.cpu().numpy()
+    assert np.isnan(got[17]) and not np.isnan(np.delete(got, 17)).any()
+    assert np.array_equal(np.delete(got, 17), np.delete(good, 17))
