@@ -112,7 +112,8 @@ def emit(obj):
 
 def cpu_reference_sample(steps: int, warmup: int, per_worker: int):
     """The reference algorithm's CPU path on all host cores (oracle port)."""
-    from oracle.cpu_baseline import CpuPool, haar_target, qeqea_like_circuits
+    from oracle.cpu_baseline import CpuPool
+    from paper_1809_11134_b200.synthetic import haar_target, qeqea_like_circuits
 
     pool = CpuPool()
     T = haar_target(N)
@@ -164,7 +165,7 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    from oracle.cpu_baseline import haar_target
+    from paper_1809_11134_b200.synthetic import haar_target
     from paper_1809_11134_b200 import _lib
     from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
     from paper_1809_11134_b200.fitness import TargetSpec
@@ -266,7 +267,7 @@ def run_ours(args):
             _, codes, thetas = eng.sample(0, P)  # this generation's C5 circuits
             src = "this generation's C5 circuits"
         else:
-            from oracle.cpu_baseline import qeqea_like_circuits
+            from paper_1809_11134_b200.synthetic import qeqea_like_circuits
 
             codes, thetas = qeqea_like_circuits(N, L, n_mine, seed=77 + rank)
             src = "QEQEA-mix C5-shaped circuits, P/N per rank"

@@ -9,7 +9,6 @@ product-side caller, for its `cpu_baseline` leg and the `--impl reference` arm.
 """
 from __future__ import annotations
 
-import math
 import os
 import time
 from concurrent.futures import ProcessPoolExecutor
@@ -17,26 +16,9 @@ from concurrent.futures import ProcessPoolExecutor
 import numpy as np
 
 
-def qeqea_like_circuits(n: int, L: int, count: int, seed: int = 0):
-    """Random circuits with the QEQEA gate mix: slot kind uniform over the
-    n + C(n,2) kinds (engine.py:180), measured axis uniform, theta uniform."""
-    rng = np.random.default_rng(seed)
-    K = n + n * (n - 1) // 2
-    kinds = rng.integers(0, K, size=(count, L))
-    axes = rng.integers(0, 3, size=(count, L))
-    codes = np.where(kinds < n, 3 * kinds + axes, 3 * n + (kinds - n)).astype(np.uint8)
-    thetas = rng.uniform(0.0, 2 * math.pi, size=(count, L))
-    return codes, thetas
-
-
-def haar_target(n: int) -> np.ndarray:
-    """The C5 synthetic target: QR-Haar unitary from default_rng(12345)
-    (pkg/tests/conftest.py:10-14), identical bits on every host."""
-    rng = np.random.default_rng(12345)
-    d = 2 ** n
-    z = rng.normal(size=(d, d)) + 1j * rng.normal(size=(d, d))
-    q, r = np.linalg.qr(z)
-    return q * (np.diag(r) / np.abs(np.diag(r)))
+# the synthetic workload generators live with the product (inputs, not the
+# computation); re-exported here for the CPU baseline's callers
+from paper_1809_11134_b200.synthetic import haar_target, qeqea_like_circuits  # noqa: E402,F401
 
 
 def _worker(args):

@@ -8,7 +8,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 import numpy as np
 
-from oracle.cpu_baseline import haar_target
+from paper_1809_11134_b200.synthetic import haar_target
 from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
 from paper_1809_11134_b200.fitness import TargetSpec, target_matrix
 

@@ -4,7 +4,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np, torch
 from paper_1809_11134_b200 import _lib
-from oracle.cpu_baseline import haar_target, qeqea_like_circuits
+from paper_1809_11134_b200.synthetic import haar_target, qeqea_like_circuits
 
 for mb in (75, 603):
     h = torch.empty(mb << 20, dtype=torch.uint8, pin_memory=True)
