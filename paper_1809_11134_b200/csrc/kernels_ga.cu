@@ -149,11 +149,20 @@ __device__ double np_pairwise_sum(const double* a, int64_t n) {
 // Final reduction + best-so-far update (ga.py:171-174) + SUS (ga.py:95-116).
 // SUS is inherently sequential (cumulative sums compared against pointer +=
 // spacing): thread 0 replays it exactly; warp 0 copies the elite genome.
+constexpr int kSusCache = 2048;  // fitness values staged in shared memory for the sequential walk
+
 __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_improved_p, int64_t* s_elite_p) {
+  __shared__ double sfit[kSusCache];
   int& s_improved = *s_improved_p;
   int64_t& s_elite = *s_elite_p;
   GaDevState* st = a.st;
   const int cur = ga_cur(a);
+  // the walk below is one thread's dependent loads: serve them from shared memory
+  const bool cached = a.P <= kSusCache;
+  if (cached)
+    for (int64_t i = threadIdx.x; i < a.P; i += blockDim.x) sfit[i] = a.fitness[i];
+  __syncthreads();
+  const double* fit = cached ? sfit : a.fitness;
   if (threadIdx.x == 0) {
     double m = -1.0, sum = 0.0;
     int64_t arg = INT64_MAX;
@@ -182,7 +191,7 @@ __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_impro
     // ---- sus_select(fitnesses, P, stream) ----
     NpStream rs;
     rs.init(a.seed, DOM_GA_SUS, st->generation, 0, 0);
-    const double total = np_pairwise_sum(a.fitness, a.P);
+    const double total = np_pairwise_sum(fit, a.P);
     if (total <= 0.0) {
       for (int64_t k = 0; k < a.P; ++k) a.parents[k] = (int32_t)rs.integers(a.P);
     } else {
@@ -191,8 +200,8 @@ __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_impro
       double cumulative = 0.0;
       int64_t index = 0;
       for (int64_t k = 0; k < a.P; ++k) {
-        while (index < a.P - 1 && __dadd_rn(cumulative, a.fitness[index]) <= pointer) {
-          cumulative = __dadd_rn(cumulative, a.fitness[index]);
+        while (index < a.P - 1 && __dadd_rn(cumulative, fit[index]) <= pointer) {
+          cumulative = __dadd_rn(cumulative, fit[index]);
           ++index;
         }
         a.parents[k] = (int32_t)index;
@@ -423,7 +432,36 @@ static isq_status ga_launch_small(const GaArgs& a, int n_gens, cudaStream_t s) {
   return ISQ_OK;
 }
 
+// Small populations: reductions, SUS, breeding and advance of one generation
+// in a single block (same device bodies as the four-kernel finish).
+constexpr int64_t kGaTailGenes = 1 << 14;
+
+__global__ void __launch_bounds__(kGaRed) ga_tail_kernel(GaArgs a) {
+  __shared__ double smax[kGaRed], ssum[kGaRed];
+  __shared__ int64_t sarg[kGaRed];
+  __shared__ int s_improved;
+  __shared__ int64_t s_elite;
+  if (a.st->stop) return;
+  const uint64_t g = a.st->generation;
+  const int cur = ga_cur(a);
+  for (int part = 0; part < a.n_parts; ++part) {
+    ga_reduce_partial_body(a, part, smax, ssum, sarg);
+    __syncthreads();
+  }
+  ga_reduce_sus_body(a, &s_improved, &s_elite);
+  __syncthreads();
+  const int64_t elite = a.st->elite;
+  for (int64_t t = threadIdx.x; t < a.P * a.L; t += kGaRed) ga_breed_gene(a, t, g, cur, elite);
+  __syncthreads();
+  if (threadIdx.x == 0) ga_advance_body(a);
+}
+
 static isq_status ga_launch_finish(const GaArgs& a, cudaStream_t s) {
+  if (a.P * a.L <= kGaTailGenes) {
+    ga_tail_kernel<<<1, kGaRed, 0, s>>>(a);
+    ISQ_CUDA_TRY(cudaGetLastError());
+    return ISQ_OK;
+  }
   ga_reduce_partials<<<a.n_parts, kGaRed, 0, s>>>(a);
   ga_reduce_sus_kernel<<<1, kGaRed, 0, s>>>(a);
   ga_breed_kernel<<<ga_blocks(a.P * a.L), 256, 0, s>>>(a);
