@@ -217,3 +217,32 @@ def test_fp32_engine_first_generation_within_bound():
     assert not np.array_equal(x, y)
     b.steps(5)  # keeps running on the fp32 path
     assert b.generation == 6
+
+
+def test_handles_release_their_device_memory():
+    """Create / run / close engines repeatedly (QEQEA on the fused path, CUDA
+    graphs and plain kernels; GA): device memory returns to where it started."""
+    import torch
+
+    from paper_1809_11134_b200 import GaConfig, GaEngine, PopulationConfig, QeqeaEngine, target_matrix
+
+    t = target_matrix("Toffoli")
+
+    def cycle():
+        for P in (5, 4096, 1 << 16):
+            e = QeqeaEngine(PopulationConfig(3, 16, P, max_generations=40), t, 1)
+            e.steps(20)
+            _ = e.best_gates
+            e.close()
+        g = GaEngine(GaConfig(3, 16, 50, max_generations=40), t, 1)
+        g.steps(20)
+        g.close()
+
+    cycle()  # first use allocates the runtime's own pools
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(3):
+        cycle()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert abs(free1 - free0) < 64 << 20, (free0, free1)
