@@ -159,11 +159,20 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_env()
+    # ISQ_BENCH_SHARE_GPU=1: functional check of the N > 1 code path with every
+    # rank on GPU 0 (gloo, host barriers); its timings mean nothing
+    share = world > 1 and os.environ.get("ISQ_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
+    red_dev = "cpu" if share else f"cuda:{local}"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_1809_11134_b200.synthetic import haar_target
     from paper_1809_11134_b200 import _lib
     from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
@@ -210,7 +219,7 @@ def run_ours(args):
     eval_ms = [e[1].elapsed_time(e[2]) for e in ev]
     fin_ms = [e[2].elapsed_time(e[3]) for e in ev]
     if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}")
+        t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     rec, _ = ops.read_batch()
@@ -251,6 +260,7 @@ def run_ours(args):
                               "phase updates here, not the canonical 6*4^n; the executed FP64 pipe "
                               "utilisation (ncu sm__pipe_fp64_cycles_active) is in profiles/ and DESIGN.md §6")},
         "clocks": clk,
+        **({"shared_gpu_functional_check": True} if share else {}),
         # per generation: sample, values, fitness, 2 reductions, commit, advance;
         # world > 1 adds route, unroute, elite (+ the fitness broadcast with p2p)
         "gpu_launches": (7 if world == 1 else (11 if args.transport == "p2p" else 10)) * args.steps,
@@ -290,7 +300,7 @@ def run_ours(args):
             batch()
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device=f"cuda:{local}", dtype=torch.float64)
+            t = torch.tensor([dt], device=red_dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         out["e2e"] = {"value": P * args.steps / dt, "unit": "evals/s",
