@@ -17,6 +17,8 @@
 #include <cstring>
 #include <string>
 
+#include <cooperative_groups.h>
+
 #include "engine_common.cuh"
 #include "fitness_warp.cuh"
 #include "isq_internal.h"
@@ -149,7 +151,7 @@ __device__ double np_pairwise_sum(const double* a, int64_t n) {
 // Final reduction + best-so-far update (ga.py:171-174) + SUS (ga.py:95-116).
 // SUS is inherently sequential (cumulative sums compared against pointer +=
 // spacing): thread 0 replays it exactly; warp 0 copies the elite genome.
-constexpr int kSusCache = 2048;  // fitness values staged in shared memory for the sequential walk
+constexpr int kSusCache = 512;   // fitness values staged in shared memory for the sequential walk
 
 __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_improved_p, int64_t* s_elite_p) {
   __shared__ double sfit[kSusCache];
@@ -415,6 +417,78 @@ static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaSt
 // Single-block path: one fitness round (P <= 8 warps) and few genes; larger
 // launch-bound populations (C2, P = 50) run faster as a CUDA graph of the
 // multi-kernel generation, whose fitness kernel spreads the circuits over SMs.
+// Launch-bound populations beyond one block's fitness round (C2: 50
+// genomes): n generations in one cooperative launch of up to one block per
+// SM, the phases separated by grid-wide barriers — fitness (all blocks),
+// reductions + SUS (block 0), breeding (all blocks), advance (block 0).
+template <int NQ>
+__global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  using G = Geo<NQ>;
+  constexpr int kWarps = kGaRed / 32;
+  __shared__ double2 Ts[G::D * G::D];
+  __shared__ FastChunk sh[kWarps];
+  __shared__ double smax[kGaRed], ssum[kGaRed];
+  __shared__ int64_t sarg[kGaRed];
+  __shared__ int s_improved;
+  __shared__ int64_t s_elite;
+  for (int i = threadIdx.x; i < G::D * G::D; i += kGaRed) Ts[i] = a.target[i];
+  __syncthreads();
+  const int64_t genes = a.P * a.L;
+  for (int it = 0; it < n_gens; ++it) {
+    if (a.st->stop) return;  // uniform across the grid: written before the last grid barrier
+    const uint64_t g = a.st->generation;
+    const int cur = ga_cur(a);
+    fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
+    grid.sync();
+    if (blockIdx.x == 0) {
+      for (int part = 0; part < a.n_parts; ++part) {
+        ga_reduce_partial_body(a, part, smax, ssum, sarg);
+        __syncthreads();
+      }
+      ga_reduce_sus_body(a, &s_improved, &s_elite);
+    }
+    grid.sync();
+    const int64_t elite = a.st->elite;
+    for (int64_t t = (int64_t)blockIdx.x * kGaRed + threadIdx.x; t < genes; t += (int64_t)gridDim.x * kGaRed)
+      ga_breed_gene(a, t, g, cur, elite);
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) ga_advance_body(a);
+    grid.sync();
+  }
+}
+
+template <int NQ>
+static isq_status ga_launch_coop_nq(const GaArgs& a, int n_gens, cudaStream_t s) {
+  int per_sm = 0;
+  ISQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ga_coop_kernel<NQ>, kGaRed, 0));
+  const int64_t want = (a.P + kGaRed / 32 - 1) / (kGaRed / 32);  // one circuit per warp
+  int64_t grid = (int64_t)num_sms() * (per_sm > 0 ? 1 : 0);
+  if (grid > want) grid = want;
+  if (grid < 1) {
+    set_error("cooperative GA kernel does not fit on an SM");
+    return ISQ_ERR_CUDA;
+  }
+  GaArgs args = a;
+  void* params[] = {(void*)&args, (void*)&n_gens};
+  ISQ_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)ga_coop_kernel<NQ>, dim3((unsigned)grid), dim3(kGaRed),
+                                           params, 0, s));
+  return ISQ_OK;
+}
+
+static isq_status ga_launch_coop(const GaArgs& a, int n_gens, cudaStream_t s) {
+  switch (a.n) {
+    case 2: return ga_launch_coop_nq<2>(a, n_gens, s);
+    case 3: return ga_launch_coop_nq<3>(a, n_gens, s);
+    case 4: return ga_launch_coop_nq<4>(a, n_gens, s);
+    case 5: return ga_launch_coop_nq<5>(a, n_gens, s);
+    default:
+      set_error("numberOfWires outside the compiled range 2..5");
+      return ISQ_ERR_UNSUPPORTED;
+  }
+}
+
 constexpr int64_t kGaSmallGenes = 1 << 12;
 constexpr int64_t kGaSmallPop = kGaRed / 32;
 
@@ -650,9 +724,12 @@ isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, 
     set_error("the fused single-block generation is fp64 only");
     return ISQ_ERR_CONFIG;
   }
-  if (mode == ISQ_LAUNCH_FUSED || (mode == ISQ_LAUNCH_AUTO && a.precision == ISQ_PRECISION_FP64 &&
-                                   a.P <= kGaSmallPop && a.P * a.L <= kGaSmallGenes)) {
-    st = n > 0 ? ga_launch_small(a, n, h->stream) : ISQ_OK;
+  const bool fp64 = a.precision == ISQ_PRECISION_FP64;
+  if (mode == ISQ_LAUNCH_FUSED || (mode == ISQ_LAUNCH_AUTO && fp64 && a.P * a.L <= kGaTailGenes)) {
+    // one launch for n generations: one block when the population is one
+    // fitness round, a cooperative grid otherwise
+    const bool one_block = a.P <= kGaSmallPop && a.P * a.L <= kGaSmallGenes;
+    st = n <= 0 ? ISQ_OK : one_block ? ga_launch_small(a, n, h->stream) : ga_launch_coop(a, n, h->stream);
     if (st != ISQ_OK) return st;
     return isq_ga_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
   }
