@@ -633,9 +633,39 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
     __syncthreads();
     fitness_rows<NQ>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, a.fitness, kWarps);
     __syncthreads();
-    for (int part = 0; part < a.n_parts; ++part) {
-      reduce_partial_body(a, part, smax, ssum, sarg);
+    if (a.P <= 32 && a.n_parts == 1) {
+      // one warp: the same pairwise tree as reduce_partial_body (its upper
+      // levels only add zeros), as shuffles instead of 8 block barriers
+      if (wib == 0) {
+        double m = -1.0, sum = 0.0;
+        int64_t arg = INT64_MAX;
+        if (lane < a.P) {
+          m = sum = a.fitness[lane];
+          arg = lane;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          const double m2 = __shfl_down_sync(0xffffffffu, m, off);
+          const int64_t a2 = __shfl_down_sync(0xffffffffu, arg, off);
+          const double s2 = __shfl_down_sync(0xffffffffu, sum, off);
+          if (m2 > m || (m2 == m && a2 < arg)) {
+            m = m2;
+            arg = a2;
+          }
+          sum += s2;
+        }
+        if (lane == 0) {
+          a.part_max[0] = m;
+          a.part_sum[0] = sum;
+          a.part_arg[0] = arg;
+        }
+      }
       __syncthreads();
+    } else {
+      for (int part = 0; part < a.n_parts; ++part) {
+        reduce_partial_body(a, part, smax, ssum, sarg);
+        __syncthreads();
+      }
     }
     reduce_final_body(a, &s_improved, &s_best);
     __syncthreads();
