@@ -152,10 +152,9 @@ __device__ __forceinline__ void emit_theta(const QeqeaArgs& a, int64_t t, double
 // which / value), the angle / starting slot_max / mutation flags to the touch
 // arrays, and interaction slots get their gate code.  Returns true when the
 // touch is a rotation slot still to be measured (measure_code).
-__device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, uint64_t g, uint32_t& s,
+__device__ __forceinline__ bool value_touch_from(const QeqeaArgs& a, int64_t t, uint64_t g, uint32_t s,
                                                  LiveSlot& v, int& which, double& value) {
   which = -1;
-  s = a.owner_flats[t];
   if (s == kNoSlot) {  // padding circuit: never commits (fitness <= 1 < 2)
     emit_code(a, t, 0);
     emit_theta(a, t, 0.0);
@@ -175,15 +174,25 @@ __device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, 
   return false;
 }
 
+__device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, uint64_t g, uint32_t& s,
+                                                 LiveSlot& v, int& which, double& value) {
+  s = a.owner_flats[t];
+  return value_touch_from(a, t, g, s, v, which, value);
+}
+
 // construct_segments for one rotation slot (engine.py:167-170): Born
 // measurement on the slot's (generation, slot) stream -> gate code.
+__device__ __forceinline__ uint8_t measure_code_on(const QeqeaArgs& a, uint32_t s, NpStream& st, double re[3],
+                                                   double im[3]) {
+  bool ok = true;
+  const int axis = measure_axis(re, im, a.n_meas, st, &ok);
+  return (uint8_t)(3 * ((int64_t)s / (a.L * a.P)) + axis);
+}
 __device__ __forceinline__ uint8_t measure_code(const QeqeaArgs& a, uint32_t s, uint64_t g, double re[3],
                                                 double im[3]) {
   NpStream st;
   st.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);
-  bool ok = true;
-  const int axis = measure_axis(re, im, a.n_meas, st, &ok);
-  return (uint8_t)(3 * ((int64_t)s / (a.L * a.P)) + axis);
+  return measure_code_on(a, s, st, re, im);
 }
 
 // Per tile of kValTile owned touches: (1) record gathers + lazy angle
@@ -619,15 +628,20 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
     for (int64_t c = wib; c < a.P; c += kWarps) sample_circuit_warp(a, g, c, a.flats + c * a.L, blk[wib], lane);
     __syncthreads();
     for (int64_t t = threadIdx.x; t < touches; t += kRedThreads) {
-      uint32_t s;
+      const uint32_t s = a.owner_flats[t];
+      // the measurement stream's first block depends only on (g, s): start it
+      // before the record load and the mutation (latency-bound tiny populations)
+      NpStream ms;
+      ms.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);
+      if ((int64_t)s / (a.L * a.P) < a.n) ms.prime();
       LiveSlot v;
       int which;
       double value;
-      if (value_touch_head(a, t, g, s, v, which, value)) {
+      if (value_touch_from(a, t, g, s, v, which, value)) {
         if (which >= 0) su3_one_param(which, value, v.q);
         double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
         double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
-        emit_code(a, t, measure_code(a, s, g, re, im));
+        emit_code(a, t, measure_code_on(a, s, ms, re, im));
       }
     }
     __syncthreads();

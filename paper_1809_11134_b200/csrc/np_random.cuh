@@ -128,6 +128,20 @@ struct NpStream {
     has32 = false;
     u32buf = 0;
   }
+  // Generate the first block now (it depends only on the stream key), so its
+  // latency can overlap independent work before the first draw.
+  __host__ __device__ __forceinline__ void prime() {
+    if (ctr == 0) {
+      ctr = 1;
+      uint64_t w[4];
+      stream_block(seed, dom, gen, idx, sub, 1, w);
+      b0 = w[0];
+      b1 = w[1];
+      b2 = w[2];
+      b3 = w[3];
+      pos = 0;
+    }
+  }
   __host__ __device__ __forceinline__ uint64_t next64() {
     if (pos >= 4) {
       ++ctr;
