@@ -11,9 +11,10 @@
 //   phi    : pending per-row phases, carried as the unit complex factor
 //            e^{i phi_r} on lane r (r < D), so flushes need no sincos
 //
-// * Rz and ZZ are diagonal: e^{-i th/2} diag(1 | e^{i th}) over the rows whose
-//   wire bit (Rz) or bit parity (ZZ) is 1.  They commute with phi, so each
-//   costs one predicated complex multiply per lane (w_r *= e^{i th g(r)}).
+// * Rz and ZZ are diagonal: e^{-i th/2} on the rows whose wire bit (Rz) or
+//   bit parity (ZZ) is 0, e^{+i th/2} on the others.  They commute with phi,
+//   so each costs one complex multiply per lane (w_r *= e^{-+i th/2}, the
+//   conjugate picked by a sign flip).
 //   The rotation positions of a 32-gate chunk come from one ballot; the
 //   diagonal runs between them are branch-free loops over the pending phase.
 // * Ry = S Rx S^dagger with S = diag(1, i) on the wire, and both S factors are
@@ -26,7 +27,10 @@
 //   sign), with the in-place 3-shear lifting x += p y; y += q x; x += p y.
 //   In-place updates keep every switch case free of register moves, so the
 //   hot code is n rotation cases + n flush cases and fits the instruction cache.
-// * At the end |tr(S_true^dagger T)| = |sum_kj conj(S_phys[k][j]) e^{-i phi_k} T[k][j]|.
+// * The warp starts from M = T and applies the adjoint gates in reverse order
+//   (G^dagger: the negated angle), so it ends with M = S^dagger T and
+//   |tr(S^dagger T)| = |sum_j e^{i phi_j} M_phys[j][j]|: one entry per column
+//   instead of a dense 2^n x 2^n overlap.
 #pragma once
 #include "unitary_warp.cuh"
 
@@ -50,10 +54,10 @@ struct Cplx<float> {
 template <class R>
 struct FastChunkT {
   using R2 = typename Cplx<R>::T;
-  R2 cs2[32][2];       // diag: {(1, 0), (cos th, sin th)}; rotation: {(C = cos a, 0), (p, q)}
+  R2 cs2[32][2];       // diag: {unused, e^{-i th/2}}; rotation: {(C = cos a, 0), (p, q)}
   int dmask[32];       // diag: row mask whose parity picks up e^{i th}; 0 for rotations
   int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit
-  R2 fac[32];          // flush factors / final row weights, indexed by physical row
+  R2 fac[32];          // flush factors, indexed by physical row
   double nth[32];      // next chunk's angles / codes, staged by cp.async (no registers held)
   uint32_t ncode[8];
 };
@@ -64,6 +68,47 @@ enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
 
+// sin / cos on |x| <= pi/4 (no range reduction; fdlibm kernel polynomials,
+// <= 1 ulp against the correctly rounded values on that interval).
+__device__ __forceinline__ void sincos_pi4(double x, double& s, double& c) {
+  const double z = x * x;
+  double ps = 1.58969099521155010221e-10;
+  ps = fma(ps, z, -2.50507602534068634195e-08);
+  ps = fma(ps, z, 2.75573137070700676789e-06);
+  ps = fma(ps, z, -1.98412698298579493134e-04);
+  ps = fma(ps, z, 8.33333333332248946124e-03);
+  ps = fma(ps, z, -1.66666666666666324348e-01);
+  s = fma(x * z, ps, x);
+  double pc = -1.13596475577881948265e-11;
+  pc = fma(pc, z, 2.08757232129817482790e-09);
+  pc = fma(pc, z, -2.75573143513906633035e-07);
+  pc = fma(pc, z, 2.48015872894767294178e-05);
+  pc = fma(pc, z, -1.38888888888741095749e-03);
+  pc = fma(pc, z, 4.16666666666666019037e-02);
+  c = 1.0 - fma(-z * z, pc, 0.5 * z);
+}
+
+// c ? a : b as an opaque selp (a select tree over a register array written
+// as C++ selects is turned back into a dynamically indexed local array).
+__device__ __forceinline__ double sel(int c, double a, double b) {
+  double o;
+  asm("{.reg .pred p; setp.ne.b32 p, %3, 0; selp.f64 %0, %1, %2, p;}" : "=d"(o) : "d"(a), "d"(b), "r"(c));
+  return o;
+}
+__device__ __forceinline__ float sel(int c, float a, float b) {
+  float o;
+  asm("{.reg .pred p; setp.ne.b32 p, %3, 0; selp.f32 %0, %1, %2, p;}" : "=f"(o) : "f"(a), "f"(b), "r"(c));
+  return o;
+}
+
+// v with its sign flipped when bit 0 of `par` is set.
+__device__ __forceinline__ double flip_sign(double v, int par) {
+  return __hiloint2double(__double2hiint(v) ^ (par << 31), __double2loint(v));
+}
+__device__ __forceinline__ float flip_sign(float v, int par) {
+  return __int_as_float(__float_as_int(v) ^ (par << 31));
+}
+
 template <int NQ, class R = double>
 struct FastEval {
   using G = Geo<NQ>;
@@ -72,14 +117,29 @@ struct FastEval {
   WarpUnitary<NQ, R> st;
   R wr, wi;  // pending phase factor e^{i phi} of physical row `lane` (lane < D)
 
-  __device__ __forceinline__ void begin(int lane) {
-    st.set_identity(lane);
+  // M = T (column j of the target on lane j); the gates are then applied as
+  // their adjoints in reverse order, M = S^dagger T, so the overlap is a trace.
+  __device__ __forceinline__ void begin(const double2* __restrict__ T, int lane) {
+    const int j = lane & (G::D - 1);
+    const int h = (lane >> NQ) & (G::LPC - 1);
+#pragma unroll
+    for (int r = 0; r < G::E; ++r) {
+      double tx, ty;  // volatile: the column is loop-invariant, and hoisting it
+                      // out of the circuit loop would pin 2 D registers
+      asm volatile("ld.v2.f64 {%0, %1}, [%2];" : "=d"(tx), "=d"(ty) : "l"(T + (h * G::E + r) * G::D + j));
+      st.re[r] = R(tx);
+      st.im[r] = R(ty);
+    }
     wr = R(1);
     wi = R(0);
   }
 
-  // Lane-parallel gate preparation for one position (one sincos call site
-  // for every gate type, so a chunk pays for it once).
+  // Lane-parallel gate preparation for one position (one sincos site for
+  // every gate type, so a chunk pays for it once).  With r = remainder(th, 2 pi)
+  // (|r| <= pi) and x = -r/4 (|x| <= pi/4, no range reduction):
+  //   rotation: plane angle a = -r/2 -> (C, p, q) = (cos a, -tan(a/2), sin a)
+  //   diagonal: e = e^{-i r/2}; rows whose mask parity is 0 take e, parity 1
+  //             take conj(e) (Rz / ZZ up to a global phase)
   // Gate parameters are computed in fp64 for both arithmetic types.
   __device__ __forceinline__ static void prepare(int code, double theta, int& info, int& dmask,
                                                  R2& e0, R2& e1) {
@@ -103,26 +163,26 @@ struct FastEval {
     } else {
       mask = 0;  // not a gate of this wire count: the chunk reports it (NaN fitness)
     }
-    double x = theta;
-    if (b >= 0) {
-      // plane angle, reduced to [-pi/2, pi/2] up to a global sign
-      double a = -0.5 * remainder(theta, kTwoPi);
-      if (a > 0.5 * kPi) a -= kPi;
-      if (a < -0.5 * kPi) a += kPi;
-      x = 0.5 * a;
-    }
+    // remainder(theta, 2 pi), exact (up to the sign of a zero); the engines'
+    // angles all lie in [-2 pi, 2 pi]
+    double r;
+    if (fabs(theta) <= kTwoPi)
+      r = theta > kPi ? theta - kTwoPi : (theta < -kPi ? theta + kTwoPi : theta);
+    else
+      r = remainder(theta, kTwoPi);
     double sn, cs;
-    sincos(x, &sn, &cs);
+    sincos_pi4(-0.25 * r, sn, cs);
+    const double C = fma(cs, cs, -sn * sn), S = 2.0 * sn * cs;
     if (b >= 0) {
       info = type | (b << 8);
       dmask = 0;
-      e0 = Cplx<R>::make(R(fma(cs, cs, -sn * sn)), R(0));
-      e1 = Cplx<R>::make(R(-sn / cs), R(2.0 * sn * cs));
+      e0 = Cplx<R>::make(R(C), R(0));
+      e1 = Cplx<R>::make(R(-sn / cs), R(S));
     } else {
       info = GT_DIAG;
       dmask = mask;
       e0 = Cplx<R>::make(R(1), R(0));
-      e1 = Cplx<R>::make(R(cs), R(sn));
+      e1 = Cplx<R>::make(R(C), R(S));
     }
   }
 
@@ -183,7 +243,8 @@ struct FastEval {
   __device__ __forceinline__ void diag_run(int q, int qe, const Chunk& sm, int row) {
 #pragma unroll 2
     for (; q < qe; ++q) {
-      const R2 e = sm.cs2[q][__popc(row & sm.dmask[q]) & 1];
+      R2 e = sm.cs2[q][1];
+      e.y = flip_sign(e.y, __popc(row & sm.dmask[q]));  // parity 1: conj
       const R t = wr * e.y;
       wr = fma(wr, e.x, -wi * e.y);
       wi = fma(wi, e.x, t);
@@ -218,64 +279,75 @@ struct FastEval {
       const int b = inf >> 8;
       const int m = 1 << b;
       const bool ry = (inf & 3) == GT_RY;
-      if (ry && (row & m)) {  // S^dagger: rows with the wire bit set pick up -i
-        const R t = wr;
-        wr = wi;
-        wi = -t;
-      }
-      // flush factor of the rows with bit b set: w_r * conj(w_{r^m}) (1 elsewhere);
-      // those rows then carry the phase of their partner, so it commutes with Rx
+      const bool hib = (row & m) != 0;
+      // flush factor of the rows with bit b set: w_r * conj(w_{r^m}), times -i
+      // for Ry (S^dagger); those rows then carry their partner's phase (times
+      // +i for Ry: S), which commutes with the Rx.  Rows with the bit clear
+      // keep their phase; their factor is only read for lane-bit rotations
+      // (n < 5), where it must be 1.
       const R orr = __shfl_xor_sync(0xffffffffu, wr, m);
       const R ori = __shfl_xor_sync(0xffffffffu, wi, m);
-      R fr = R(1), fi = R(0);
-      if (row & m) {
-        fr = fma(wr, orr, wi * ori);
-        fi = fma(wi, orr, -wr * ori);
-        wr = orr;
-        wi = ori;
+      R fr = fma(wr, orr, wi * ori), fi = fma(wi, orr, -wr * ori);
+      if (ry) {
+        const R t = fr;
+        fr = fi;
+        fi = -t;
+      }
+      if constexpr (G::LB > 0) {
+        fr = hib ? fr : R(1);
+        fi = hib ? fi : R(0);
       }
       sm.fac[lane] = Cplx<R>::make(fr, fi);
+      if (hib) {
+        wr = ry ? -ori : orr;
+        wi = ry ? orr : ori;
+      }
       const R2 pq = sm.cs2[qr][1];
       const R C = sm.cs2[qr][0].x;
       __syncwarp();
       flush_rotate(b, sm.fac, pq.x, pq.y, C, lane);
       __syncwarp();
-      if (ry && (row & m)) {  // S: rows with the wire bit set pick up +i
-        const R t = wr;
-        wr = -wi;
-        wi = t;
-      }
     }
     __syncwarp();
     return bad;
   }
 
-  // Fitness from the final state (fitness.py:36-49).
-  // The overlap is accumulated in fp64 for both arithmetic types.
-  __device__ __forceinline__ double finish(const double2* __restrict__ T, Chunk& sm, int lane) {
-    if (lane < G::D) sm.fac[lane] = Cplx<R>::make(wr, -wi);  // e^{-i phi}
-    __syncwarp();
+  // Registers [0, HALF) <- [HALF, 2 HALF) where bit HALF of idx is set, down
+  // to HALF = 1: register 0 ends up holding register idx.
+  template <int HALF>
+  __device__ __forceinline__ void select_level(int idx) {
+    if constexpr (HALF >= 1) {
+      const int up = idx & HALF;
+#pragma unroll
+      for (int i = 0; i < HALF; ++i) {
+        st.re[i] = sel(up, st.re[i + HALF], st.re[i]);
+        st.im[i] = sel(up, st.im[i + HALF], st.im[i]);
+      }
+      select_level<HALF / 2>(idx);
+    }
+  }
+
+  // Fitness from the final state (fitness.py:36-49): |tr(M_true)| with
+  // M_true = diag(e^{i phi}) M_phys, i.e. sum_j e^{i phi_j} M_phys[j][j].
+  // The diagonal entry of column j is picked out of the registers with a
+  // select tree over the register index; the trace is summed in fp64.
+  __device__ __forceinline__ double finish(int lane) {
     const int j = lane & (G::D - 1);
     const int h = (lane >> NQ) & (G::LPC - 1);
-    double ar = 0.0, ai = 0.0;
-#pragma unroll
-    for (int r = 0; r < G::E; ++r) {
-      const int k = h * G::E + r;
-      const double2 t = T[k * G::D + j];
-      const R2 wf = sm.fac[k];
-      const double wx = wf.x, wy = wf.y, xr = st.re[r], xi = st.im[r];
-      // p = conj(x) * t ; acc += w * p
-      const double pr = fma(xr, t.x, xi * t.y);
-      const double pi = fma(xr, t.y, -xi * t.x);
-      ar = fma(wx, pr, fma(-wy, pi, ar));
-      ai = fma(wx, pi, fma(wy, pr, ai));
+    R pr = wr, pi = wi;
+    if constexpr (G::LB > 0) {  // the phase of row j is carried by lane j
+      pr = __shfl_sync(0xffffffffu, wr, j);
+      pi = __shfl_sync(0xffffffffu, wi, j);
     }
+    select_level<G::E / 2>(j & (G::E - 1));
+    const double xr = st.re[0], xi = st.im[0], wx = pr, wy = pi;
+    double ar = fma(wx, xr, -wy * xi), ai = fma(wx, xi, wy * xr);
+    if (h != (j >> G::EB)) ar = ai = 0.0;  // row j lives on another lane of the column
 #pragma unroll
     for (int off = G::ACTIVE / 2; off >= 1; off >>= 1) {
       ar += __shfl_xor_sync(0xffffffffu, ar, off);
       ai += __shfl_xor_sync(0xffffffffu, ai, off);
     }
-    __syncwarp();
     return fitness_from_overlap(hypot(ar, ai), G::D);
   }
 };
@@ -288,20 +360,22 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
 }
 
-// Stage the (code, theta) row slice [nb, nb + 32) of circuit nc in shared
-// memory with cp.async, so the prefetch holds no registers (a register
-// prefetch was spilled and its store waited on the load right away).
+// Stage chunk `nb` of circuit nc in shared memory with cp.async, so the
+// prefetch holds no registers (a register prefetch was spilled and its store
+// waited on the load right away).  Chunks run backwards through the circuit:
+// chunk nb holds positions [L - nb - nq, L - nb), nq = min(32, L - nb).
 template <class Chunk>
 __device__ __forceinline__ void stage_chunk(Chunk& sm, int64_t count, int L, const uint8_t* codes,
                                             const double* thetas, int64_t nc, int nb, int lane) {
   if (nc >= count) return;
-  const int64_t row = nc * (int64_t)L + nb;
-  if (nb + lane < L) cp_async(&sm.nth[lane], thetas + row + lane, 8);
+  const int nq = min(32, L - nb);
+  const int64_t row = nc * (int64_t)L + (L - nb - nq);
+  if (lane < nq) cp_async(&sm.nth[lane], thetas + row + lane, 8);
   const uint8_t* src = codes + row;
-  if (nb + 32 <= L && ((reinterpret_cast<uintptr_t>(src) & 3) == 0)) {
+  if (nq == 32 && ((reinterpret_cast<uintptr_t>(src) & 3) == 0)) {
     if (lane < 8) cp_async(&sm.ncode[lane], src + 4 * lane, 4);
   } else {
-    if (nb + lane < L) reinterpret_cast<uint8_t*>(sm.ncode)[lane] = src[lane];
+    if (lane < nq) reinterpret_cast<uint8_t*>(sm.ncode)[lane] = src[lane];
   }
   asm volatile("cp.async.commit_group;\n" ::);
 }
@@ -322,7 +396,7 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
   stage_chunk(cs, count, L, codes, thetas, c, 0, lane);
   for (; c < count; c += nwarps) {
     FastEval<NQ, R> ev;
-    ev.begin(lane);
+    ev.begin(Ts, lane);
     bool bad = false;
     for (int base = 0; base < L; base += 32) {
       const int nq = min(32, L - base);
@@ -330,9 +404,9 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
       __syncwarp();
       int code = 0;
       double th = 0.0;
-      if (lane < nq) {
-        code = reinterpret_cast<const uint8_t*>(cs.ncode)[lane];
-        th = cs.nth[lane];
+      if (lane < nq) {  // position L - 1 - base - lane, as its adjoint
+        code = reinterpret_cast<const uint8_t*>(cs.ncode)[nq - 1 - lane];
+        th = -cs.nth[nq - 1 - lane];
       }
       __syncwarp();
       int64_t nc = c;
@@ -344,7 +418,7 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
       stage_chunk(cs, count, L, codes, thetas, nc, nb, lane);
       bad |= ev.chunk(code, th, nq, cs, lane);
     }
-    const double f = ev.finish(Ts, cs, lane);
+    const double f = ev.finish(lane);
     if (lane == 0) {
       fitness[c] = bad ? __longlong_as_double(0x7ff8000000000000LL) : f;  // NaN: invalid gate code
       if (bad && bad_code) atomicOr(bad_code, 1);

@@ -77,6 +77,11 @@ int main() {
     printf("%-12s %8.3f ms  %6.2f Gacc/s\n", name, ms, n / (ms * 1e6));
   };
   const int grid = 148 * 8, blk = 256;
+  for (int gran : {-1, 32, 64, 128}) {
+  if (gran > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitMaxL2FetchGranularity);
+  printf("-- L2 fetch granularity %zu B%s\n", cur, gran < 0 ? " (default)" : "");
   run("gather8", [&] { gather<8><<<grid, blk>>>(tab, nrec, n, out); });
   run("gather16", [&] { gather<16><<<grid, blk>>>(tab, nrec, n, out); });
   run("gather32", [&] { gather<32><<<grid, blk>>>(tab, nrec, n, out); });
@@ -84,6 +89,7 @@ int main() {
   run("gather128", [&] { gather<128><<<grid, blk>>>(tab, nrec, n, out); });
   run("gather64v256", [&] { gather64_v256<<<grid, blk>>>((const double*)tab, nrec, n, out); });
   run("atomicmax8", [&] { rmw<<<grid, blk>>>((unsigned long long*)tab, nrec, n); });
+  }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
