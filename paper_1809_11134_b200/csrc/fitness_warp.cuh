@@ -55,7 +55,7 @@ template <class R>
 struct FastChunkT {
   using R2 = typename Cplx<R>::T;
   R2 cs2[32][2];       // diag: {unused, e^{-i th/2}}; rotation: {(C = cos a, 0), (p, q)}
-  int dmask[32];       // diag: row mask whose parity picks up e^{i th}; 0 for rotations
+  uint32_t rpar[32];   // diag: bit r = parity of row r under the gate's wire mask; 0 for rotations
   int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit
   R2 fac[32];          // flush factors, indexed by physical row
   double nth[32];      // next chunk's angles / codes, staged by cp.async (no registers held)
@@ -101,12 +101,22 @@ __device__ __forceinline__ float sel(int c, float a, float b) {
   return o;
 }
 
-// v with its sign flipped when bit 0 of `par` is set.
-__device__ __forceinline__ double flip_sign(double v, int par) {
-  return __hiloint2double(__double2hiint(v) ^ (par << 31), __double2loint(v));
+// v with its sign flipped when bit 31 of `bits` is set.
+__device__ __forceinline__ double flip_sign_bit(double v, uint32_t bits) {
+  return __hiloint2double(__double2hiint(v) ^ (int)(bits & 0x80000000u), __double2loint(v));
 }
-__device__ __forceinline__ float flip_sign(float v, int par) {
-  return __int_as_float(__float_as_int(v) ^ (par << 31));
+__device__ __forceinline__ float flip_sign_bit(float v, uint32_t bits) {
+  return __int_as_float(__float_as_int(v) ^ (int)(bits & 0x80000000u));
+}
+
+// Bit r set for the rows r < 32 whose bits under `mask` have odd parity.
+__device__ __forceinline__ uint32_t row_parity(int mask) {
+  constexpr uint32_t kBitRows[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
+  uint32_t p = 0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    if (mask & (1 << k)) p ^= kBitRows[k];
+  return p;
 }
 
 template <int NQ, class R = double>
@@ -141,7 +151,7 @@ struct FastEval {
   //   diagonal: e = e^{-i r/2}; rows whose mask parity is 0 take e, parity 1
   //             take conj(e) (Rz / ZZ up to a global phase)
   // Gate parameters are computed in fp64 for both arithmetic types.
-  __device__ __forceinline__ static void prepare(int code, double theta, int& info, int& dmask,
+  __device__ __forceinline__ static void prepare(int code, double theta, int& info, uint32_t& rpar,
                                                  R2& e0, R2& e1) {
     int b = -1, type = GT_DIAG, mask;
     if (code < 3 * NQ) {
@@ -175,12 +185,12 @@ struct FastEval {
     const double C = fma(cs, cs, -sn * sn), S = 2.0 * sn * cs;
     if (b >= 0) {
       info = type | (b << 8);
-      dmask = 0;
+      rpar = 0;
       e0 = Cplx<R>::make(R(C), R(0));
       e1 = Cplx<R>::make(R(-sn / cs), R(S));
     } else {
       info = GT_DIAG;
-      dmask = mask;
+      rpar = row_parity(mask);
       e0 = Cplx<R>::make(R(1), R(0));
       e1 = Cplx<R>::make(R(C), R(S));
     }
@@ -240,11 +250,11 @@ struct FastEval {
   // Pending phase of this lane's row times the diagonal gates [q, qe) of the
   // chunk (all of them diagonal): branch-free, one predicated complex
   // multiply per gate.
-  __device__ __forceinline__ void diag_run(int q, int qe, const Chunk& sm, int row) {
+  __device__ __forceinline__ void diag_run(int q, int qe, const Chunk& sm, int sh) {
 #pragma unroll 2
     for (; q < qe; ++q) {
       R2 e = sm.cs2[q][1];
-      e.y = flip_sign(e.y, __popc(row & sm.dmask[q]));  // parity 1: conj
+      e.y = flip_sign_bit(e.y, sm.rpar[q] << sh);  // parity 1: conj
       const R t = wr * e.y;
       wr = fma(wr, e.x, -wi * e.y);
       wi = fma(wi, e.x, t);
@@ -257,22 +267,23 @@ struct FastEval {
   // flush the non-commuting part of it and rotate the register state.
   // Returns true (warp-uniform) when a lane's code is not a valid gate code.
   __device__ __forceinline__ bool chunk(int code, double theta, int nq, Chunk& sm, int lane) {
-    int info = GT_DIAG, dmask = 0;  // lanes past the end: neutral diagonal, empty mask
+    int info = GT_DIAG;  // lanes past the end: neutral diagonal, no parity
+    uint32_t rpar = 0;
     R2 e0 = Cplx<R>::make(R(1), R(0)), e1 = e0;
-    if (lane < nq) prepare(code, theta, info, dmask, e0, e1);
+    if (lane < nq) prepare(code, theta, info, rpar, e0, e1);
     const bool bad = __any_sync(0xffffffffu, lane < nq && (code < 0 || code >= G::NCODES));
     sm.info[lane] = info;
-    sm.dmask[lane] = dmask;
+    sm.rpar[lane] = rpar;
     sm.cs2[lane][0] = e0;
     sm.cs2[lane][1] = e1;
     unsigned rot = __ballot_sync(0xffffffffu, info != GT_DIAG);
     __syncwarp();
     const int row = lane;  // physical row whose phase this lane carries
+    const int sh = 31 - row;
     int q = 0;
-    for (;;) {
-      const int qr = rot ? __ffs(rot) - 1 : nq;
-      diag_run(q, qr, sm, row);
-      if (qr >= nq) break;
+    while (rot) {
+      const int qr = __ffs(rot) - 1;
+      diag_run(q, qr, sm, sh);
       rot &= rot - 1;
       q = qr + 1;
       const int inf = sm.info[qr];
@@ -285,22 +296,19 @@ struct FastEval {
       // +i for Ry: S), which commutes with the Rx.  Rows with the bit clear
       // keep their phase; their factor is only read for lane-bit rotations
       // (n < 5), where it must be 1.
-      const R orr = __shfl_xor_sync(0xffffffffu, wr, m);
-      const R ori = __shfl_xor_sync(0xffffffffu, wi, m);
+      // (the partner's phase comes over times i for Ry: o' = i o, so that
+      // w conj(o') = -i w conj(o) and the new phase is o')
+      const R orr = __shfl_xor_sync(0xffffffffu, ry ? -wi : wr, m);
+      const R ori = __shfl_xor_sync(0xffffffffu, ry ? wr : wi, m);
       R fr = fma(wr, orr, wi * ori), fi = fma(wi, orr, -wr * ori);
-      if (ry) {
-        const R t = fr;
-        fr = fi;
-        fi = -t;
-      }
       if constexpr (G::LB > 0) {
         fr = hib ? fr : R(1);
         fi = hib ? fi : R(0);
       }
       sm.fac[lane] = Cplx<R>::make(fr, fi);
       if (hib) {
-        wr = ry ? -ori : orr;
-        wi = ry ? orr : ori;
+        wr = orr;
+        wi = ori;
       }
       const R2 pq = sm.cs2[qr][1];
       const R C = sm.cs2[qr][0].x;
@@ -308,6 +316,7 @@ struct FastEval {
       flush_rotate(b, sm.fac, pq.x, pq.y, C, lane);
       __syncwarp();
     }
+    diag_run(q, nq, sm, sh);
     __syncwarp();
     return bad;
   }

@@ -39,6 +39,13 @@ def main():
                                max_generations=10_000, target_fitness=0.999), target_matrix("CNOT"), s))
          for s in SEEDS]
     out["c2_ga_cnot"] = [f"{b:.4f}@{g}" for b, g, _ in r]
+    # success rate over 40 seeds beside the reference's (tests/golden/ga_cnot_outcomes_reference.json)
+    r = [run(GaEngine(GaConfig(2, 6, 50, mutation_rate=0.2, mutation_range=math.pi / 8, structural_rate=0.2,
+                               max_generations=10_000, target_fitness=0.999), target_matrix("CNOT"), s))
+         for s in range(1, 41)]
+    ref = json.loads((Path(__file__).resolve().parent.parent / "tests" / "golden" /
+                      "ga_cnot_outcomes_reference.json").read_text())
+    out["c2_ga_cnot_rate_40_seeds"] = {"device": sum(b >= 0.999 for b, _, _ in r), "reference": ref["successes"]}
     ga = [run(GaEngine(GaConfig(3, 16, 50, max_generations=20_000), target_matrix("Toffoli"), s))[0] for s in SEEDS]
     qe = [run(QeqeaEngine(PopulationConfig(3, 16, 5, max_generations=20_000), target_matrix("Toffoli"), s))[0]
           for s in SEEDS]

@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--no-peak", action="store_true")
+    ap.add_argument("--mix", default="", help="ga | qeqea (default both)")
+    ap.add_argument("--prec", default="", help="fp64 | fp32 (default both)")
     args_ = ap.parse_args()
     lib = _lib.load()
     res = {"fp64_peak_tflops": 36.5}
@@ -29,7 +31,11 @@ def main():
     dev = torch.device("cuda:0")
     stream = torch.cuda.current_stream()
     for prec_name, prec in (("fp64", 0), ("fp32", 1)):
+        if args_.prec and prec_name != args_.prec:
+            continue
         for mix in ("ga", "qeqea"):
+            if args_.mix and mix != args_.mix:
+                continue
             for n, L, count in [(3, 16, 1 << 20), (4, 32, 1 << 18), (5, 64, 1 << 18)]:
                 if args_.only and f"n{n}" != args_.only:
                     continue
