@@ -107,17 +107,15 @@ constexpr int kValThreads = 256;
 constexpr int kValPerThread = 3;  // touches per thread per tile: ~1 measurement task per thread
 constexpr int kValTile = kValThreads * kValPerThread;
 
-struct MeasureTask {  // one rotation touch of the tile: its live qutrit, awaiting measurement
-  double re[3], im[3];
-  double value;       // pending SU(3) parameter (qutrit mutation), see `which`
-  uint32_t s;
-  uint16_t out;       // touch offset in the tile
-  int16_t which;      // pending su3_one_param parameter index, -1 none
-};
-
+// Per tile: the touches' committed records, staged by cp.async (no registers
+// held while the random gathers are in flight), then updated in place.
 struct ValuesShared {
-  MeasureTask tasks[kValTile];
-  uint16_t qq[kValTile];  // tasks with a pending qutrit mutation
+  RotRec rec[kValTile];     // committed record (an IntRec in the first 16 B); qutrit updated in place
+  uint32_t s[kValTile];     // slot of each touch
+  double value[kValTile];   // pending SU(3) parameter (qutrit mutation)
+  int8_t which[kValTile];   // its parameter index
+  uint16_t task[kValTile];  // rotation touches to measure
+  uint16_t qq[kValTile];    // of which with a pending qutrit mutation
   int ntask, nq;
 };
 
@@ -195,60 +193,90 @@ __device__ __forceinline__ uint8_t measure_code(const QeqeaArgs& a, uint32_t s, 
   return measure_code_on(a, s, st, re, im);
 }
 
-// Per tile of kValTile owned touches: (1) record gathers + lazy angle
-// mutations, rotation touches queued in shared memory; (2) the queued qutrit
-// mutations (5 % of touches) on full warps; (3) the Born measurements of the
-// queued rotation touches on full warps.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Per tile of kValTile owned touches: (0) the records of all the tile's
+// touches gathered into shared memory with cp.async; (1) lazy angle
+// mutations, rotation touches queued; (2) the queued qutrit mutations (5 % of
+// touches) on full warps; (3) the Born measurements of the queued rotation
+// touches on full warps.
 __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t1) {
-  extern __shared__ __align__(16) unsigned char val_smem[];
+  extern __shared__ __align__(64) unsigned char val_smem[];
   ValuesShared& sm = *reinterpret_cast<ValuesShared*>(val_smem);
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   for (int64_t base = (int64_t)blockIdx.x * kValTile; base < t1; base += (int64_t)gridDim.x * kValTile) {
     if (threadIdx.x == 0) sm.ntask = sm.nq = 0;
+#pragma unroll
+    for (int u = 0; u < kValPerThread; ++u) {
+      const int i = u * kValThreads + threadIdx.x;
+      if (base + i >= t1) break;
+      const uint32_t s = a.owner_flats[base + i];
+      sm.s[i] = s;
+      if (s == kNoSlot) continue;
+      const int64_t loc = slot_local(a, s);
+      if (loc < a.Qtloc) {
+        const char* src = reinterpret_cast<const char*>(a.rot + loc);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cp_async16(reinterpret_cast<char*>(&sm.rec[i]) + 16 * k, src + 16 * k);
+      } else {
+        cp_async16(&sm.rec[i], a.inter + (loc - a.Qtloc));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kValPerThread; ++u) {
-      const int64_t t = base + u * kValThreads + threadIdx.x;
+      const int i = u * kValThreads + threadIdx.x;
+      const int64_t t = base + i;
       if (t >= t1) break;
-      uint32_t s;
+      const uint32_t s = sm.s[i];
+      if (s == kNoSlot) {  // padding circuit: never commits (fitness <= 1 < 2)
+        emit_code(a, t, 0);
+        emit_theta(a, t, 0.0);
+        a.touch_fbefore[t] = 2.0;
+        a.touch_mutated[t] = 0;
+        continue;
+      }
+      const int64_t kind = (int64_t)s / (a.L * a.P);
+      const double2 ts = reinterpret_cast<const double2*>(&sm.rec[i])[kind < a.n ? 3 : 0];
       LiveSlot v;
-      int which;
-      double value;
-      if (value_touch_head(a, t, g, s, v, which, value)) {
-        const int k = atomicAdd(&sm.ntask, 1);
-        MeasureTask& mt = sm.tasks[k];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          mt.re[c] = v.q[c].x;
-          mt.im[c] = v.q[c].y;
+      v.theta = ts.x;
+      const double f = ts.y;
+      int which = -1;
+      double value = 0.0;
+      // the qutrit stays in shared memory: a qutrit mutation only needs which / value here
+      const int m = g > 0 ? mutate_decide(a, s, g - 1, f, v, which, value) : MUT_NONE;
+      emit_theta(a, t, v.theta);
+      a.touch_fbefore[t] = f;
+      a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
+      if (kind < a.n) {
+        sm.task[atomicAdd(&sm.ntask, 1)] = (uint16_t)i;
+        if (m == MUT_QUTRIT) {
+          sm.which[i] = (int8_t)which;
+          sm.value[i] = value;
+          sm.qq[atomicAdd(&sm.nq, 1)] = (uint16_t)i;
         }
-        mt.value = value;
-        mt.s = s;
-        mt.out = (uint16_t)(t - base);
-        mt.which = (int16_t)which;
-        if (which >= 0) sm.qq[atomicAdd(&sm.nq, 1)] = (uint16_t)k;
+      } else {
+        emit_code(a, t, (uint8_t)(3 * a.n + (kind - a.n)));
       }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < sm.nq; j += kValThreads) {
-      MeasureTask& mt = sm.tasks[sm.qq[j]];
-      double2 q[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) q[c] = make_double2(mt.re[c], mt.im[c]);
-      su3_one_param(mt.which, mt.value, q);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        mt.re[c] = q[c].x;
-        mt.im[c] = q[c].y;
-      }
+      const int i = sm.qq[j];
+      su3_one_param(sm.which[i], sm.value[i], sm.rec[i].q);
     }
     __syncthreads();
     for (int k = threadIdx.x; k < sm.ntask; k += kValThreads) {
-      const MeasureTask& mt = sm.tasks[k];
-      double re[3] = {mt.re[0], mt.re[1], mt.re[2]};
-      double im[3] = {mt.im[0], mt.im[1], mt.im[2]};
-      emit_code(a, base + mt.out, measure_code(a, mt.s, g, re, im));
+      const int i = sm.task[k];
+      const double2* q = sm.rec[i].q;
+      double re[3] = {q[0].x, q[1].x, q[2].x};
+      double im[3] = {q[0].y, q[1].y, q[2].y};
+      emit_code(a, base + i, measure_code(a, sm.s[i], g, re, im));
     }
     __syncthreads();
   }
