@@ -9,11 +9,15 @@ timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "p
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
-timeout 600 python tools/kbench.py --no-peak > $OUT/kbench.json 2>&1
+timeout 600 python tools/kbench.py > $OUT/kbench.json 2>&1
+timeout 600 python tools/small_bench.py > $OUT/small_bench.txt 2>&1
+timeout 300 python tools/acceptance.py > $OUT/acceptance.json 2> $OUT/acceptance.err
 if [ "${PROFILE:-1}" = "1" ]; then
   timeout 300 python tools/engine_bench.py --P 1048576 --gens 2 > $OUT/plain.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $OUT/launches_c5.csv python tools/engine_bench.py --P 1048576 --gens 2 > $OUT/ncu_launch.log 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/bench_launches.csv python bench.py --steps 2 --warmup 3 --skip-e2e --skip-fp32 > $OUT/bench_ncu.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fitness_fast|qeqea_values|qeqea_commit" -s 9 -c 3 \
       -o $OUT/prof_c5 python tools/engine_bench.py --P 1048576 --gens 2 > $OUT/ncu_full.log 2>&1
   echo "ncu rc=$?" >> $OUT/ncu_full.log
