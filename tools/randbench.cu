@@ -52,6 +52,21 @@ __global__ void rmw(unsigned long long* tab, uint64_t nrec, int64_t n) {
   }
 }
 
+__global__ void scatter_store(unsigned long long* tab, uint64_t nrec, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix(i * 0x9E3779B97F4A7C15ULL) % nrec;
+    tab[r * 16] = (unsigned long long)i;
+  }
+}
+
+// load, compare, RED only when larger (most touches of a converged bank do not improve)
+__global__ void rmw_cond(unsigned long long* tab, uint64_t nrec, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix(i * 0x9E3779B97F4A7C15ULL) % nrec;
+    if (tab[r * 16] < (unsigned long long)i) atomicMax(tab + r * 16, (unsigned long long)i);
+  }
+}
+
 int main() {
   const size_t bytes = 16ULL << 30;  // 16 GB table of 128 B records
   const uint64_t nrec = bytes / 128;
@@ -77,7 +92,7 @@ int main() {
     printf("%-12s %8.3f ms  %6.2f Gacc/s\n", name, ms, n / (ms * 1e6));
   };
   const int grid = 148 * 8, blk = 256;
-  for (int gran : {-1, 32, 64, 128}) {
+  for (int gran : {-1}) {
   if (gran > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
   size_t cur = 0;
   cudaDeviceGetLimit(&cur, cudaLimitMaxL2FetchGranularity);
@@ -89,6 +104,7 @@ int main() {
   run("gather128", [&] { gather<128><<<grid, blk>>>(tab, nrec, n, out); });
   run("gather64v256", [&] { gather64_v256<<<grid, blk>>>((const double*)tab, nrec, n, out); });
   run("atomicmax8", [&] { rmw<<<grid, blk>>>((unsigned long long*)tab, nrec, n); });
+  run("store8", [&] { scatter_store<<<grid, blk>>>((unsigned long long*)tab, nrec, n); });
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
