@@ -155,6 +155,10 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   for (int o = 0; o <= a.world; ++o) a.p_bounds[o] = (int)((int64_t)o * a.L / a.world);
   a.p_lo = a.p_bounds[a.rank];
   a.Lr = a.p_bounds[a.rank + 1] - a.p_lo;
+  a.div_L.init((uint32_t)a.L);
+  a.div_LP.init((uint32_t)(a.L * a.P));
+  a.div_Lr.init((uint32_t)(a.Lr > 0 ? a.Lr : 1));
+  a.div_S.init((uint32_t)a.S);
   a.Qloc = a.K * a.P * a.Lr;
   a.Qtloc = (int64_t)a.n * a.P * a.Lr;
   a.elite_len = 2 + a.L + (a.L + 7) / 8;

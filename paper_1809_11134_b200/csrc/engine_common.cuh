@@ -75,6 +75,24 @@ struct PeerTable {
 // position is fixed by Eq. 9, so the touches of position p always go to the
 // same owner.  World 1: c0 = 0, S = P, p_lo = 0, Lr = L, and the owner-side
 // touch arrays alias the circuit-side ones.
+// Division of 32-bit unsigned values by a runtime-invariant divisor d >= 1:
+// q = (mulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1
+// (Granlund & Montgomery), exact for every n < 2^32.  Slot, touch and
+// circuit indices are all below 2^32 (slots are uint32).
+struct FastDiv {
+  uint32_t d, m;
+  int l;
+  __host__ void init(uint32_t dd) {
+    d = dd;
+    l = 0;
+    while ((1ull << l) < dd) ++l;
+    m = (uint32_t)((((1ull << l) - dd) << 32) / dd + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> l);
+  }
+};
+
 struct QeqeaArgs {
   // configuration (engine.py:33-43)
   int n, L;
@@ -90,6 +108,7 @@ struct QeqeaArgs {
   int64_t c0;      // first circuit of this rank
   int p_lo, Lr;    // owned positions
   int p_bounds[kMaxWorld + 1];  // owner o holds positions [p_bounds[o], p_bounds[o + 1])
+  FastDiv div_L, div_LP, div_Lr, div_S;  // by L, L * P (slot -> kind), Lr, S
   int64_t Qloc, Qtloc;  // owned slots / owned rotation-region slots
   // bank (owned slots, local index, see slot_local)
   RotRec* rot;     // Qtloc records
@@ -129,9 +148,15 @@ struct QeqeaArgs {
 
 // Eq. 9 flat index s = (kind P + i) L + p  <->  owned local index (kind P + i) Lr + (p - p_lo).
 __host__ __device__ __forceinline__ int64_t slot_local(const QeqeaArgs& a, int64_t s) {
+#ifdef __CUDA_ARCH__
+  const int64_t ki = a.div_L.div((uint32_t)s);
+#else
   const int64_t ki = s / a.L;
+#endif
   return ki * a.Lr + (s - ki * a.L - a.p_lo);
 }
+// Slot kind (rotation wire k < n, else interaction pair k - n) of slot s.
+__device__ __forceinline__ int64_t slot_kind(const QeqeaArgs& a, uint32_t s) { return a.div_LP.div(s); }
 __host__ __device__ __forceinline__ int64_t slot_global(const QeqeaArgs& a, int64_t loc) {
   const int64_t ki = loc / a.Lr;
   return ki * a.L + a.p_lo + (loc - ki * a.Lr);
@@ -281,7 +306,7 @@ __device__ __forceinline__ void live_slot(const QeqeaArgs& a, int64_t s, uint64_
 // construct_segments, engine.py:167-170).
 __device__ __forceinline__ int slot_gate_code(const QeqeaArgs& a, int64_t s, uint64_t g,
                                               const LiveSlot& v) {
-  const int64_t kind = s / (a.L * a.P);
+  const int64_t kind = slot_kind(a, (uint32_t)s);
   if (kind < a.n) {
     NpStream st;
     st.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);

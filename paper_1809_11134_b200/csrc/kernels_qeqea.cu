@@ -68,7 +68,7 @@ __global__ void qeqea_route_kernel(QeqeaArgs a) {
   const int64_t n = a.S * a.L;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c_loc = i / a.L;
+    const int64_t c_loc = a.div_L.div((uint32_t)i);
     const int p = (int)(i - c_loc * a.L);
     const uint32_t f = a.c0 + c_loc < a.P ? a.flats[i] : kNoSlot;
     if (a.peers) {
@@ -89,7 +89,7 @@ __global__ void qeqea_unroute_kernel(QeqeaArgs a) {
   const int64_t n = a.S * a.L;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c_loc = i / a.L;
+    const int64_t c_loc = a.div_L.div((uint32_t)i);
     const int64_t src = routed_index(a, c_loc, (int)(i - c_loc * a.L));
     a.gate_codes[i] = a.recv_codes[src];
     a.gate_thetas[i] = a.recv_thetas[src];
@@ -123,8 +123,8 @@ struct ValuesShared {
 // the peer transport, straight into the receive buffers of the circuit's rank
 // (block of this owner at S * p_lo, row = circuit - j * S, column = q).
 __device__ __forceinline__ int64_t peer_recv_index(const QeqeaArgs& a, int64_t t, int64_t& j) {
-  const int64_t c = t / a.Lr;
-  j = c / a.S;
+  const int64_t c = a.div_Lr.div((uint32_t)t);
+  j = a.div_S.div((uint32_t)c);
   return a.S * a.p_lo + (c - j * a.S) * a.Lr + (t - c * a.Lr);
 }
 __device__ __forceinline__ void emit_code(const QeqeaArgs& a, int64_t t, uint8_t code) {
@@ -166,7 +166,7 @@ __device__ __forceinline__ bool value_touch_from(const QeqeaArgs& a, int64_t t, 
   emit_theta(a, t, v.theta);
   a.touch_fbefore[t] = f;
   a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
-  const int64_t kind = (int64_t)s / (a.L * a.P);
+  const int64_t kind = slot_kind(a, s);
   if (kind < a.n) return true;
   emit_code(a, t, (uint8_t)(3 * a.n + (kind - a.n)));
   return false;
@@ -184,7 +184,7 @@ __device__ __forceinline__ uint8_t measure_code_on(const QeqeaArgs& a, uint32_t 
                                                    double im[3]) {
   bool ok = true;
   const int axis = measure_axis(re, im, a.n_meas, st, &ok);
-  return (uint8_t)(3 * ((int64_t)s / (a.L * a.P)) + axis);
+  return (uint8_t)(3 * (slot_kind(a, s)) + axis);
 }
 __device__ __forceinline__ uint8_t measure_code(const QeqeaArgs& a, uint32_t s, uint64_t g, double re[3],
                                                 double im[3]) {
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
         a.touch_mutated[t] = 0;
         continue;
       }
-      const int64_t kind = (int64_t)s / (a.L * a.P);
+      const int64_t kind = slot_kind(a, s);
       const double2 ts = reinterpret_cast<const double2*>(&sm.rec[i])[kind < a.n ? 3 : 0];
       LiveSlot v;
       v.theta = ts.x;
@@ -468,7 +468,7 @@ constexpr int kCommitThreads = 256;
 // double order).  The values kernel recorded each touch's starting slot_max
 // and pending-mutation flag, so only improving touches do random bank traffic.
 __device__ __forceinline__ void commit_touch(const QeqeaArgs& a, int64_t t, uint64_t g) {
-  const double fit = a.fitness[t / a.Lr];
+  const double fit = a.fitness[a.div_Lr.div((uint32_t)t)];
   const double fb = a.touch_fbefore[t];
   if (!(fit > fb)) return;
   const uint32_t s = a.owner_flats[t];
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
       // before the record load and the mutation (latency-bound tiny populations)
       NpStream ms;
       ms.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);
-      if ((int64_t)s / (a.L * a.P) < a.n) ms.prime();
+      if (slot_kind(a, s) < a.n) ms.prime();
       LiveSlot v;
       int which;
       double value;
