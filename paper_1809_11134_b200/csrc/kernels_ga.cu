@@ -54,6 +54,7 @@ struct GaArgs {
   int64_t* part_arg;
   int n_parts;
   int precision;  // fitness arithmetic: ISQ_PRECISION_FP64 / _FP32
+  FastDiv div_L, div_P;  // gene index -> genome; pair index mod P (P * L < 2^32)
 };
 
 __device__ __forceinline__ int ga_cur(const GaArgs& a) { return (int)(a.st->generation & 1); }
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
 // (parents[2k % P], parents[(2k+1) % P]) (ga.py:177-187); slot 0 is the elite.
 __device__ __forceinline__ void ga_breed_gene(const GaArgs& a, int64_t t, uint64_t g, int cur, int64_t elite) {
   const int nxt = cur ^ 1;
-  const int64_t i = t / a.L;
+  const int64_t i = a.div_L.div((uint32_t)t);
   const int j = (int)(t - i * a.L);
   if (i == 0) {
     a.codes[nxt][j] = a.codes[cur][elite * a.L + j];
@@ -241,7 +242,9 @@ __device__ __forceinline__ void ga_breed_gene(const GaArgs& a, int64_t t, uint64
   }
   const int64_t k = (i - 1) >> 1;
   const bool first = ((i - 1) & 1) == 0;
-  const int64_t pa = a.parents[(2 * k) % a.P], pb = a.parents[(2 * k + 1) % a.P];
+  const uint32_t k0 = (uint32_t)(2 * k), k1 = k0 + 1u;
+  const int64_t pa = a.parents[k0 - a.div_P.div(k0) * (uint32_t)a.P],
+                pb = a.parents[k1 - a.div_P.div(k1) * (uint32_t)a.P];
   // two_point_crossover: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
   int p = 0, q = 0;
   if (a.L >= 2) {
@@ -586,6 +589,8 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
     return bad("numberOfWires exceeds the device kernels (compiled for 2..5 wires)",
                ISQ_ERR_UNSUPPORTED);
   if (cfg->population >= (1LL << 31)) return bad("population must be < 2^31", ISQ_ERR_UNSUPPORTED);
+  if ((int64_t)cfg->population * cfg->size_of_individual >= (1LL << 32))
+    return bad("population * sizeOfIndividual must be < 2^32", ISQ_ERR_UNSUPPORTED);
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return bad("invalid rank/world");
   if (cfg->precision != ISQ_PRECISION_FP64 && cfg->precision != ISQ_PRECISION_FP32)
     return bad("precision must be ISQ_PRECISION_FP64 or ISQ_PRECISION_FP32");
@@ -599,6 +604,8 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
   a.n = cfg->number_of_wires;
   a.L = cfg->size_of_individual;
   a.P = cfg->population;
+  a.div_L.init((uint32_t)a.L);
+  a.div_P.init((uint32_t)a.P);
   a.ncodes = 3 * a.n + a.n * (a.n - 1) / 2;
   a.rate = cfg->mutation_rate;
   a.mrange = cfg->mutation_range;
