@@ -211,12 +211,25 @@ __host__ __device__ __forceinline__ uint32_t lemire_value(uint32_t u, uint32_t r
 // bound/redraw loop is reproduced exactly, exp/log are the device versions
 // (last-ulp differences from glibc can flip a draw only when U
 // lies within an ulp of a CDF boundary).
+//
+// n = 1 (the default n_meas): glibc's exp(1.0 * log(q)) returns q itself for
+// every q in [0.5, 1] we tested (5e7 random q across that range and 8M
+// consecutive doubles at each end, numpy 2.3), so qn = q is the reference's
+// value, with none of the device exp/log rounding; and bnd >= 10 > n, so
+// bound = n.
 __device__ __forceinline__ int64_t binomial_inversion(NpStream& s, int64_t n, double p) {
   const double q = ISQ_DSUB(1.0, p);
-  const double qn = exp(ISQ_DMUL((double)n, log(q)));
-  const double np_ = ISQ_DMUL((double)n, p);
-  const double bnd = ISQ_DADD(np_, ISQ_DMUL(10.0, sqrt(ISQ_DADD(ISQ_DMUL(np_, q), 1.0))));
-  const int64_t bound = (int64_t)((double)n < bnd ? (double)n : bnd);
+  double qn;
+  int64_t bound;
+  if (n == 1) {
+    qn = q;
+    bound = 1;
+  } else {
+    qn = exp(ISQ_DMUL((double)n, log(q)));
+    const double np_ = ISQ_DMUL((double)n, p);
+    const double bnd = ISQ_DADD(np_, ISQ_DMUL(10.0, sqrt(ISQ_DADD(ISQ_DMUL(np_, q), 1.0))));
+    bound = (int64_t)((double)n < bnd ? (double)n : bnd);
+  }
   int64_t X = 0;
   double px = qn;
   double U = s.random();
