@@ -212,11 +212,12 @@ __host__ __device__ __forceinline__ uint32_t lemire_value(uint32_t u, uint32_t r
 // (last-ulp differences from glibc can flip a draw only when U
 // lies within an ulp of a CDF boundary).
 //
-// n = 1 (the default n_meas): glibc's exp(1.0 * log(q)) returns q itself for
-// every q in [0.5, 1] we tested (5e7 random q across that range and 8M
-// consecutive doubles at each end, numpy 2.3), so qn = q is the reference's
-// value, with none of the device exp/log rounding; and bnd >= 10 > n, so
-// bound = n.
+// n = 1 (the default n_meas): the C library's exp(1.0 * log(q)), which
+// numpy's distributions.c calls, returns q itself for every q in [0.5, 1]
+// tested (3M random q and 1M consecutive doubles at each end through glibc,
+// tests/test_oracle.py::test_exp_log_identity_on_binomial_q), so qn = q is
+// the reference's value, without the device exp/log rounding; and
+// bnd >= 10 > n, so bound = n.
 __device__ __forceinline__ int64_t binomial_inversion(NpStream& s, int64_t n, double p) {
   const double q = ISQ_DSUB(1.0, p);
   double qn;

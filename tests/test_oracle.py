@@ -157,3 +157,21 @@ def test_sampling_stream_layout():
     b = g.integers(15, size=2)
     assert list(a) == [(u * 1024) >> 32 for u in u32[:3]]
     assert list(b) == [(u * 15) >> 32 for u in u32[3:5]]
+
+
+def test_exp_log_identity_on_binomial_q():
+    """numpy's random_binomial_inversion computes qn = exp(n * log(q)) with the
+    C library; for n = 1 (the default n_meas) the device takes qn = q
+    (csrc/np_random.cuh binomial_inversion).  That is exact iff the C
+    library's exp(log(q)) returns q for every q = 1 - p, p in [0, 0.5]."""
+    import math
+    import random
+    import struct
+
+    def step(x, k):
+        return struct.unpack("<d", struct.pack("<q", struct.unpack("<q", struct.pack("<d", x))[0] + k))[0]
+
+    rng = random.Random(5)
+    qs = [1.0 - 0.5 * rng.random() for _ in range(200_000)]
+    qs += [step(0.5, k) for k in range(50_000)] + [step(1.0, -k) for k in range(50_000)] + [0.5, 1.0]
+    assert all(math.exp(1.0 * math.log(q)) == q for q in qs)
