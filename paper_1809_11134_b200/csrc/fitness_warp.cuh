@@ -65,6 +65,34 @@ using FastChunk = FastChunkT<double>;
 
 enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
 
+// Resident 2-warp blocks per SM the explicit-gate fitness kernels are bounded
+// for (__launch_bounds__ min blocks): n = 5 holds a 32-row column in
+// registers (fp64: 6 blocks = 168 registers, 3 warps per scheduler); n = 4
+// (16 rows over 2 lanes) runs 10 blocks (measured 6 % faster than 6; 8 and
+// 12 are no better); n = 3 is bound by per-gate overhead, not occupancy.
+#ifndef ISQ_FIT64_MINB
+#define ISQ_FIT64_MINB 6
+#endif
+#ifndef ISQ_FIT64_MINB4
+#define ISQ_FIT64_MINB4 10
+#endif
+#ifndef ISQ_FIT64_MINB3
+#define ISQ_FIT64_MINB3 6
+#endif
+#ifndef ISQ_FIT32_MINB4
+#define ISQ_FIT32_MINB4 8
+#endif
+#ifndef ISQ_FIT32_MINB3
+#define ISQ_FIT32_MINB3 8
+#endif
+template <int NQ, class R>
+constexpr int fit_min_blocks() {
+  if constexpr (sizeof(R) == 8)
+    return NQ >= 5 ? ISQ_FIT64_MINB : (NQ == 4 ? ISQ_FIT64_MINB4 : ISQ_FIT64_MINB3);
+  else
+    return NQ >= 5 ? 8 : (NQ == 4 ? ISQ_FIT32_MINB4 : ISQ_FIT32_MINB3);
+}
+
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
 

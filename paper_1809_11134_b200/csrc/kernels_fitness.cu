@@ -38,11 +38,6 @@ __global__ void ISQ_FIT_BOUNDS
 
 // fp32 variant: the column of S in 64 float registers: 8 resident 2-warp
 // blocks per SM (<= 128 registers, 4 warps per scheduler).
-#ifndef ISQ_FIT64_MINB
-#define ISQ_FIT64_MINB 6
-#endif
-constexpr int kFitMinBlocks64 = ISQ_FIT64_MINB;
-constexpr int kFitMinBlocks32 = 8;
 
 // Composition with the exact global phase (compose_gates readout) + fitness.
 template <int NQ>
@@ -205,9 +200,9 @@ static isq_status launch_fast_prec(int L, int64_t count, const uint8_t* codes, c
                                    const double* target, double* fitness, const int32_t* stop,
                                    int blocks_per_sm, int precision, cudaStream_t stream, int* bad) {
   if (precision == ISQ_PRECISION_FP32)
-    return launch_fast<NQ, kFitMinBlocks32, float>(L, count, codes, thetas, target, fitness, stop,
+    return launch_fast<NQ, fit_min_blocks<NQ, float>(), float>(L, count, codes, thetas, target, fitness, stop,
                                                     blocks_per_sm, stream, bad);
-  return launch_fast<NQ, kFitMinBlocks64, double>(L, count, codes, thetas, target, fitness, stop,
+  return launch_fast<NQ, fit_min_blocks<NQ, double>(), double>(L, count, codes, thetas, target, fitness, stop,
                                                   blocks_per_sm, stream, bad);
 }
 

@@ -400,8 +400,8 @@ static isq_status ga_launch_eval_nq(const GaArgs& a, int64_t c0, int64_t c1, cud
 
 template <int NQ>
 static isq_status ga_launch_eval_prec(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
-  if (a.precision == ISQ_PRECISION_FP32) return ga_launch_eval_nq<NQ, 8, float>(a, c0, c1, s);
-  return ga_launch_eval_nq<NQ, 6, double>(a, c0, c1, s);
+  if (a.precision == ISQ_PRECISION_FP32) return ga_launch_eval_nq<NQ, fit_min_blocks<NQ, float>(), float>(a, c0, c1, s);
+  return ga_launch_eval_nq<NQ, fit_min_blocks<NQ, double>(), double>(a, c0, c1, s);
 }
 
 static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
