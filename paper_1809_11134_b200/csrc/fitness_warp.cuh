@@ -67,11 +67,13 @@ enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
 
 // Resident 2-warp blocks per SM the explicit-gate fitness kernels are bounded
 // for (__launch_bounds__ min blocks): n = 5 holds a 32-row column in
-// registers (fp64: 6 blocks = 168 registers, 3 warps per scheduler); n = 4
+// registers; with a bound of 5 blocks ptxas still allocates 168 registers
+// (6 resident blocks, 3 warps per scheduler) and schedules 1.6 % faster code
+// than with the bound of 6 (7 blocks spill 1.4 KB per thread); n = 4
 // (16 rows over 2 lanes) runs 10 blocks (measured 6 % faster than 6; 8 and
 // 12 are no better); n = 3 is bound by per-gate overhead, not occupancy.
 #ifndef ISQ_FIT64_MINB
-#define ISQ_FIT64_MINB 6
+#define ISQ_FIT64_MINB 5
 #endif
 #ifndef ISQ_FIT64_MINB4
 #define ISQ_FIT64_MINB4 10
