@@ -324,6 +324,19 @@ def run_ours(args):
                            f"OPENBLAS_NUM_THREADS=1"),
                 "parity_max_rel_err_vs_gpu": float(rel.max()),
             }
+    # the reference's own call: QeqeaEngine.step() (engine.py:318-361), one
+    # generation per call with its (max, mean) read back to the host, wall
+    # clock around K calls (ctypes + launch + the synchronising record read)
+    if world == 1 and not args.skip_e2e:
+        eng.step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            eng.step()
+        dt = time.perf_counter() - t0
+        out["api_step"] = {"value": P * args.steps / dt, "unit": "evals/s", "ms_per_step": dt * 1e3 / args.steps,
+                           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(_lib.GEN_RECORD.itemsize),
+                           "path": "QeqeaEngine.step() through the C ABI (isq_qeqea_step), host wall clock"}
     eng.close()
     # the fp32 variant of the fitness kernel (include/isq.h ISQ_PRECISION_FP32):
     # a full C5 generation with fp32 fitness, and its error on the e2e circuits
