@@ -151,7 +151,7 @@ isq_status isq_qeqea_step(void* handle, int32_t n, isq_generation_record* record
 /* How isq_qeqea_step / isq_ga_step launch their generations (results are
  * identical in every mode):
  *   AUTO     FUSED for <= 8 candidates and <= 4096 gate slots, GRAPH for
- *            <= 2^18 gate slots, else KERNELS
+ *            <= 2^22 gate slots, else KERNELS
  *   KERNELS  one launch per kernel per generation
  *   GRAPH    16-generation CUDA graphs replayed on the handle's stream
  *   FUSED    n generations in one single-block launch */
