@@ -56,7 +56,7 @@ struct FastChunkT {
   using R2 = typename Cplx<R>::T;
   R2 cs2[32][2];       // diag: {unused, e^{-i th/2}}; rotation: {(C = cos a, 0), (p, q)}
   uint32_t rpar[32];   // diag: bit r = parity of row r under the gate's wire mask; 0 for rotations
-  int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit
+  int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit (n = 5)
   R2 fac[32];          // flush factors, indexed by physical row
   double nth[32];      // next chunk's angles / codes, staged by cp.async (no registers held)
   uint32_t ncode[8];
@@ -326,11 +326,23 @@ struct FastEval {
     R2 e0 = Cplx<R>::make(R(1), R(0)), e1 = e0;
     if (lane < nq) prepare(code, theta, info, rpar, e0, e1);
     const bool bad = __any_sync(0xffffffffu, lane < nq && (code < 0 || code >= G::NCODES));
-    sm.info[lane] = info;
+    // n <= 4: each rotation's type and row bit as warp-uniform bit planes (no
+    // shared-memory round trip on the rotation's critical path: -3 % at n = 3,
+    // 4); n = 5 reads them back from shared memory (the bit planes cost it
+    // spills: +1.5 %)
+    constexpr bool kPlanes = NQ < 5;
+    if constexpr (!kPlanes) sm.info[lane] = info;
     sm.rpar[lane] = rpar;
     sm.cs2[lane][0] = e0;
     sm.cs2[lane][1] = e1;
     unsigned rot = __ballot_sync(0xffffffffu, info != GT_DIAG);
+    unsigned ryb = 0, bp0 = 0, bp1 = 0, bp2 = 0;
+    if constexpr (kPlanes) {
+      ryb = __ballot_sync(0xffffffffu, (info & 3) == GT_RY);
+      bp0 = __ballot_sync(0xffffffffu, info & 0x100);
+      bp1 = __ballot_sync(0xffffffffu, info & 0x200);
+      bp2 = __ballot_sync(0xffffffffu, info & 0x400);
+    }
     __syncwarp();
     const int row = lane;  // physical row whose phase this lane carries
     const int sh = 31 - row;
@@ -340,7 +352,12 @@ struct FastEval {
       diag_run(q, qr, sm, sh);
       rot &= rot - 1;
       q = qr + 1;
-      const int inf = sm.info[qr];
+      int inf;
+      if constexpr (kPlanes)
+        inf = (((bp0 >> qr) & 1) << 8) | (((bp1 >> qr) & 1) << 9) | (((bp2 >> qr) & 1) << 10) |
+              (((ryb >> qr) & 1) ? GT_RY : GT_RX);
+      else
+        inf = sm.info[qr];
       const int b = inf >> 8;
       const int m = 1 << b;
       const bool ry = (inf & 3) == GT_RY;
