@@ -123,7 +123,11 @@ static isq_status fitness_batch_host(int32_t n, int32_t length, int64_t count, c
   }
   std::lock_guard<std::mutex> lk(c->mu);
   const int64_t D = 1LL << n;
-  const int64_t chunk = count < (1 << 17) ? count : (1 << 17);  // circuits per pipeline stage
+  // circuits per pipeline stage: ~1/32 of the batch (2^14..2^17), so the
+  // last stage's score, which nothing overlaps, stays short
+  int64_t chunk = count / 32;
+  chunk = chunk < (1 << 14) ? (1 << 14) : (chunk > (1 << 17) ? (1 << 17) : chunk);
+  if (chunk > count) chunk = count;
   const size_t len = (size_t)(length > 0 ? length : 1);
   if ((size_t)chunk > c->cap_rows || len > c->cap_len) {
     for (int b = 0; b < 2; ++b) {
