@@ -59,6 +59,41 @@ __global__ void scatter_store(unsigned long long* tab, uint64_t nrec, int64_t n)
   }
 }
 
+// random stores of W bytes (16: one 128-bit store; 32 / 64: 256-bit stores): a
+// full 32 B sector written needs no DRAM read for the merge
+template <int W>
+__global__ void scatter_wide(double* tab, uint64_t nrec, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix(i * 0x9E3779B97F4A7C15ULL) % nrec;
+    double* p = tab + r * 16;
+    const double v = (double)i;
+    if constexpr (W == 16) {
+      asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v), "d"(v));
+    } else {
+#pragma unroll
+      for (int k = 0; k < W / 32; ++k)
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4 * k), "d"(v), "d"(v), "d"(v), "d"(v));
+    }
+  }
+}
+
+// duplicate detection in an L2-resident bitmap (seen / dup bit per key):
+// `n` random keys below `nkeys`, one ATOM (OR, old value used) per key and a
+// RED into the dup bitmap for repeats
+__global__ void dedup_bits(uint32_t* seen, uint32_t* dup, uint64_t nkeys, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(i * 0x9E3779B97F4A7C15ULL) % nkeys;
+    const uint32_t bit = 1u << (k & 31);
+    if (atomicOr(seen + (k >> 5), bit) & bit) atomicOr(dup + (k >> 5), bit);
+  }
+}
+__global__ void dedup_read(const uint32_t* dup, uint64_t nkeys, int64_t n, uint8_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = mix(i * 0x9E3779B97F4A7C15ULL) % nkeys;
+    flag[i] = (dup[k >> 5] >> (k & 31)) & 1;
+  }
+}
+
 // load, compare, RED only when larger (most touches of a converged bank do not improve)
 __global__ void rmw_cond(unsigned long long* tab, uint64_t nrec, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -105,6 +140,22 @@ int main() {
   run("gather64v256", [&] { gather64_v256<<<grid, blk>>>((const double*)tab, nrec, n, out); });
   run("atomicmax8", [&] { rmw<<<grid, blk>>>((unsigned long long*)tab, nrec, n); });
   run("store8", [&] { scatter_store<<<grid, blk>>>((unsigned long long*)tab, nrec, n); });
+  run("store16", [&] { scatter_wide<16><<<grid, blk>>>((double*)tab, nrec, n); });
+  run("store32", [&] { scatter_wide<32><<<grid, blk>>>((double*)tab, nrec, n); });
+  run("store64", [&] { scatter_wide<64><<<grid, blk>>>((double*)tab, nrec, n); });
+  {
+    // one position group: 16 positions x P = 2^20 touches into 16 x 15 x 2^20 keys
+    const int64_t ng = 16LL << 20;
+    const uint64_t nkeys = 16ULL * 15 * (1 << 20);
+    uint32_t* seen = reinterpret_cast<uint32_t*>(tab);
+    uint32_t* dup = seen + nkeys / 32 + 1024;
+    uint8_t* flag = reinterpret_cast<uint8_t*>(dup + nkeys / 32 + 1024);
+    const size_t bm = nkeys / 8 + 4096;
+    printf("-- dedup group: %lld keys-touches, bitmaps 2 x %.1f MB\n", (long long)ng, bm / 1e6);
+    run("dedup_memset", [&] { cudaMemsetAsync(seen, 0, 2 * bm); });
+    run("dedup_bits", [&] { dedup_bits<<<grid, blk>>>(seen, dup, nkeys, ng); });
+    run("dedup_read", [&] { dedup_read<<<grid, blk>>>(dup, nkeys, ng, flag); });
+  }
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
