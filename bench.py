@@ -279,6 +279,15 @@ def run_ours(args):
     tf = ROOT / "profiles" / "traffic_eval_c5.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    # executed FP64 pipe utilisation of the same kernel from the committed
+    # `ncu --set full` capture (profiles/, not measured by this run)
+    pipe_ncu = None
+    nf = ROOT / "profiles" / "r01_c5_ncu_full.json"
+    if nf.exists():
+        for k in json.loads(nf.read_text()):
+            if "fitness_fast_kernel<5" in k.get("kernel", ""):
+                v = k.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "")
+                pipe_ncu = float(v.split()[0]) / 100 if v else None
 
     out = {
         "metric": METRIC, "value": evals_per_s, "unit": "evals/s", "n_gpus": world,
@@ -298,13 +307,15 @@ def run_ours(args):
                      "finish (world > 1: all-gathers; reduce + commit + table)": sum(fin_ms) / len(fin_ms)},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
+                     "fp64_pipe_active_ncu": pipe_ncu,
                      "kernel": "fitness_fast_kernel<5> (score phase, one launch per generation)",
                      "peak_source": "FP64 CUDA-core FMA peak measured live by isq_fma_peak "
                                     "(MEASURED_PEAKS.json carries no FP64 figure)",
                      "work": "canonical F(n,L) = (6L+8) 4^n flop/eval (SURVEY.md §8d) x circuits per launch",
                      "note": ("frac > 1 is possible: diagonal gates (Rz, ZZ; 78% of QEQEA gates) cost O(2^n) "
                               "phase updates here, not the canonical 6*4^n; the executed FP64 pipe "
-                              "utilisation (ncu sm__pipe_fp64_cycles_active) is in profiles/ and DESIGN.md §6")},
+                              "utilisation is fp64_pipe_active_ncu (ncu sm__pipe_fp64_cycles_active of the "
+                              "committed capture, profiles/r01_c5_ncu_full.json; DESIGN.md §6)")},
         "clocks": clk,
         **({"shared_gpu_functional_check": True} if share else {}),
         # per generation: sample, values, fitness, 2 reductions, commit, advance;
