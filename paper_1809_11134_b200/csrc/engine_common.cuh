@@ -262,24 +262,44 @@ enum : int { MUT_NONE = 0, MUT_ANGLE = 1, MUT_QUTRIT = 2 };
 // to v.theta; a qutrit mutation is returned as (which, value) for
 // su3_one_param, so a caller can run those (5 % of slots, costly and
 // divergent) compacted.
-__device__ __forceinline__ int mutate_decide(const QeqeaArgs& a, int64_t s, uint64_t mg, double f,
-                                             LiveSlot& v, int& which, double& value) {
+// The draws of slot s's mutation stream (generation mg), which depend on
+// nothing but the stream key, so a caller can compute them while the slot's
+// record is still in flight: bit 0 masked (random() < p_mut), bit 1 coin,
+// bit 2 angle sign (random() < 0.5), bits 8..10 integers(8); d3 the uniform's
+// double.
+struct MutDraw {
+  uint32_t bits;
+  double d3;
+};
+__device__ __forceinline__ MutDraw mutate_draw(const QeqeaArgs& a, int64_t s, uint64_t mg) {
   uint64_t w[4];
   stream_block(a.seed, DOM_MUTATE, mg, (uint64_t)s, 0, 1, w);
-  if (!(u64_to_double(w[0]) < a.p_mut)) return MUT_NONE;
+  MutDraw d;
+  d.bits = (u64_to_double(w[0]) < a.p_mut ? 1u : 0u) | (u64_to_double(w[1]) < 0.5 ? 2u : 0u) |
+           (u64_to_double(w[2]) < 0.5 ? 4u : 0u) | (((uint32_t)(w[2] & 0xffffffffULL) >> 29) << 8);
+  d.d3 = u64_to_double(w[3]);
+  return d;
+}
+__device__ __forceinline__ int mutate_apply(const QeqeaArgs& a, int64_t s, const MutDraw& d, double f,
+                                            LiveSlot& v, int& which, double& value) {
+  if (!(d.bits & 1u)) return MUT_NONE;  // random() >= p_mut
   if (!(f < 1.0)) return MUT_NONE;
-  const bool coin = u64_to_double(w[1]) < 0.5;
+  const bool coin = (d.bits & 2u) != 0;
   const double omf = __dsub_rn(1.0, f);
   if (coin && s < a.Qt) {
-    which = (int)((uint32_t)(w[2] & 0xffffffffULL) >> 29);  // Lemire, bound 8
-    const double range = which < 3 ? kHalfPiD : kTwoPiD;     // encoding.py:23
-    value = __dadd_rn(0.0, __dmul_rn(__dmul_rn(range, omf), u64_to_double(w[3])));
+    which = (int)((d.bits >> 8) & 7u);                     // Lemire, bound 8
+    const double range = which < 3 ? kHalfPiD : kTwoPiD;  // encoding.py:23
+    value = __dadd_rn(0.0, __dmul_rn(__dmul_rn(range, omf), d.d3));
     return MUT_QUTRIT;
   }
-  const double sign = u64_to_double(w[2]) < 0.5 ? 1.0 : -1.0;  // encoding.py:51
+  const double sign = (d.bits & 4u) ? 1.0 : -1.0;  // encoding.py:51
   const double step = __dmul_rn(__dmul_rn(sign, omf), a.mutation_range);
   v.theta = py_mod(__dadd_rn(v.theta, step), kTwoPiD);
   return MUT_ANGLE;
+}
+__device__ __forceinline__ int mutate_decide(const QeqeaArgs& a, int64_t s, uint64_t mg, double f,
+                                             LiveSlot& v, int& which, double& value) {
+  return mutate_apply(a, s, mutate_draw(a, s, mg), f, v, which, value);
 }
 
 __device__ __forceinline__ bool mutate_slot(const QeqeaArgs& a, int64_t s, uint64_t mg, double f,

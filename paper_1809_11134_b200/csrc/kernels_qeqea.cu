@@ -103,6 +103,9 @@ __global__ void qeqea_unroute_kernel(QeqeaArgs a) {
 // full warps instead of on the 1/3 of lanes that need it.  Also records, per
 // touch, the slot_max the generation started from and whether the slot
 // carries a pending mutation (the commit consumes both).
+#ifndef ISQ_VAL_PREDRAW
+#define ISQ_VAL_PREDRAW 1
+#endif
 constexpr int kValThreads = 256;
 constexpr int kValPerThread = 3;  // touches per thread per tile: ~1 measurement task per thread
 constexpr int kValTile = kValThreads * kValPerThread;
@@ -227,6 +230,21 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);
+#if ISQ_VAL_PREDRAW
+    // the mutation draws need only the stream key: computed while the
+    // records are in flight
+    MutDraw md[kValPerThread];
+#pragma unroll
+    for (int u = 0; u < kValPerThread; ++u) {
+      const int i = u * kValThreads + threadIdx.x;
+      md[u].bits = 0;
+      md[u].d3 = 0.0;
+      if (g > 0 && base + i < t1) {
+        const uint32_t s = sm.s[i];
+        if (s != kNoSlot) md[u] = mutate_draw(a, s, g - 1);
+      }
+    }
+#endif
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 #pragma unroll
@@ -250,7 +268,11 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       int which = -1;
       double value = 0.0;
       // the qutrit stays in shared memory: a qutrit mutation only needs which / value here
+#if ISQ_VAL_PREDRAW
+      const int m = g > 0 ? mutate_apply(a, s, md[u], f, v, which, value) : MUT_NONE;
+#else
       const int m = g > 0 ? mutate_decide(a, s, g - 1, f, v, which, value) : MUT_NONE;
+#endif
       emit_theta(a, t, v.theta);
       a.touch_fbefore[t] = f;
       a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
