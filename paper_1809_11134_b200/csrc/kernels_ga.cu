@@ -150,12 +150,29 @@ __device__ double np_pairwise_sum(const double* a, int64_t n) {
 }
 
 // Final reduction + best-so-far update (ga.py:171-174) + SUS (ga.py:95-116).
-// SUS is inherently sequential (cumulative sums compared against pointer +=
-// spacing): thread 0 replays it exactly; warp 0 copies the elite genome.
+// SUS is a sequential walk (cumulative sums compared against pointer +=
+// spacing): thread 0 replays its two running sums exactly, the picks are
+// then searched in parallel (below); warp 0 copies the elite genome.
 constexpr int kSusCache = 512;   // fitness values staged in shared memory for the sequential walk
 
-__device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_improved_p, int64_t* s_elite_p) {
+struct NoIdleWork {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `idle` runs on threads 1.. of the block while thread 0 walks the SUS.
+// With `scratch` (>= P doubles of shared memory, P <= kSusCache) the walk is
+// replaced by its exact parallel form: thread 0 writes the walk's running
+// sums C[i+1] = C[i] + f[i] (in place over the staged fitness) and its
+// pointer sequence p[k+1] = p[k] + spacing, both in the walk's own
+// sequential rounding, and every thread k finds parents[k] = the first
+// i <= P-2 with C[i+1] > p[k] (else P-1) by binary search: both sequences are
+// nondecreasing (fitness >= 0), so that is where the walk stops.
+template <class Idle = NoIdleWork>
+__device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_improved_p, int64_t* s_elite_p,
+                                                   Idle idle = Idle(), double* scratch = nullptr,
+                                                   int scratch_n = 0) {
   __shared__ double sfit[kSusCache];
+  __shared__ int s_search;
   int& s_improved = *s_improved_p;
   int64_t& s_elite = *s_elite_p;
   GaDevState* st = a.st;
@@ -195,8 +212,20 @@ __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_impro
     NpStream rs;
     rs.init(a.seed, DOM_GA_SUS, st->generation, 0, 0);
     const double total = np_pairwise_sum(fit, a.P);
+    int search = 0;
     if (total <= 0.0) {
       for (int64_t k = 0; k < a.P; ++k) a.parents[k] = (int32_t)rs.integers(a.P);
+    } else if (cached && scratch != nullptr && a.P <= scratch_n) {
+      const double spacing = __ddiv_rn(total, (double)a.P);
+      double pointer = rs.uniform(0.0, spacing);
+      double cumulative = 0.0;
+      for (int k = 0; k < (int)a.P; ++k) {
+        cumulative = __dadd_rn(cumulative, sfit[k]);
+        sfit[k] = cumulative;  // C[k + 1]
+        scratch[k] = pointer;
+        pointer = __dadd_rn(pointer, spacing);
+      }
+      search = 1;
     } else {
       const double spacing = __ddiv_rn(total, (double)a.P);
       double pointer = rs.uniform(0.0, spacing);
@@ -211,8 +240,26 @@ __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_impro
         pointer = __dadd_rn(pointer, spacing);
       }
     }
+    s_search = search;
+  } else {
+    idle();
   }
   __syncthreads();
+  if (s_search) {
+    for (int k = threadIdx.x; k < (int)a.P; k += blockDim.x) {
+      const double pk = scratch[k];
+      int lo = 0, hi = (int)a.P - 1;  // first j in [0, P-2] with C[j + 1] > pk, else P - 1
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sfit[mid] <= pk)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      a.parents[k] = lo;
+    }
+    __syncthreads();
+  }
   if (s_improved && threadIdx.x < 32) {
     for (int j = threadIdx.x; j < a.L; j += 32) {
       a.best_codes[j] = a.codes[cur][s_elite * a.L + j];
@@ -224,14 +271,56 @@ __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_impro
 __global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
   __shared__ int s_improved;
   __shared__ int64_t s_elite;
+  __shared__ double pointers[kSusCache];
   if (a.st->stop) return;
-  ga_reduce_sus_body(a, &s_improved, &s_elite);
+  ga_reduce_sus_body(a, &s_improved, &s_elite, NoIdleWork(), pointers, kSusCache);
 }
 
 // ----------------------------------------------------------------- breed ---
 // Child i >= 1 is the (i-1)%2-th child of pair k = (i-1)/2 of parents
 // (parents[2k % P], parents[(2k+1) % P]) (ga.py:177-187); slot 0 is the elite.
-__device__ __forceinline__ void ga_breed_gene(const GaArgs& a, int64_t t, uint64_t g, int cur, int64_t elite) {
+// The random draws of gene t (its pair's crossover cuts, its own mutation)
+// depend only on (generation, pair / child, gene), so the cooperative kernel
+// draws them while block 0 runs the sequential SUS (ga_breed_draw), and
+// ga_breed_apply only gathers the parents' genes.
+struct GeneDraw {
+  int p, q;     // crossover cuts [p, q)
+  int mut;      // 0 none, 1 structural (code), 2 angle (delta)
+  int code;
+  double delta;
+};
+__device__ __forceinline__ GeneDraw ga_breed_draw(const GaArgs& a, int64_t t, uint64_t g) {
+  GeneDraw d;
+  d.p = d.q = d.mut = d.code = 0;
+  d.delta = 0.0;
+  const int64_t i = a.div_L.div((uint32_t)t);
+  const int j = (int)(t - i * a.L);
+  if (i == 0) return d;
+  const int64_t k = (i - 1) >> 1;
+  // two_point_crossover: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
+  if (a.L >= 2) {
+    NpStream cs;
+    cs.init(a.seed, DOM_GA_PAIR, g, (uint64_t)k, 0);
+    const int x = (int)cs.integers(a.L + 1), y = (int)cs.integers(a.L + 1);
+    d.p = x < y ? x : y;
+    d.q = x < y ? y : x;
+  }
+  // ga_mutate for this gene (ga.py:126-137)
+  NpStream ms;
+  ms.init(a.seed, DOM_GA_MUT, g, (uint64_t)i, (uint64_t)j);
+  if (ms.random() < a.rate) {
+    if (ms.random() < a.structural) {
+      d.mut = 1;
+      d.code = (int)ms.integers(a.ncodes);
+    } else {
+      d.mut = 2;
+      d.delta = ms.uniform(-a.mrange, a.mrange);
+    }
+  }
+  return d;
+}
+__device__ __forceinline__ void ga_breed_apply(const GaArgs& a, int64_t t, int cur, int64_t elite,
+                                               const GeneDraw& d) {
   const int nxt = cur ^ 1;
   const int64_t i = a.div_L.div((uint32_t)t);
   const int j = (int)(t - i * a.L);
@@ -245,32 +334,17 @@ __device__ __forceinline__ void ga_breed_gene(const GaArgs& a, int64_t t, uint64
   const uint32_t k0 = (uint32_t)(2 * k), k1 = k0 + 1u;
   const int64_t pa = a.parents[k0 - a.div_P.div(k0) * (uint32_t)a.P],
                 pb = a.parents[k1 - a.div_P.div(k1) * (uint32_t)a.P];
-  // two_point_crossover: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
-  int p = 0, q = 0;
-  if (a.L >= 2) {
-    NpStream cs;
-    cs.init(a.seed, DOM_GA_PAIR, g, (uint64_t)k, 0);
-    const int x = (int)cs.integers(a.L + 1), y = (int)cs.integers(a.L + 1);
-    p = x < y ? x : y;
-    q = x < y ? y : x;
-  }
-  const bool inside = j >= p && j < q;
+  const bool inside = j >= d.p && j < d.q;
   const int64_t src = (first != inside) ? pa : pb;  // child a: a outside, b inside
   int code = a.codes[cur][src * a.L + j];
   double theta = a.thetas[cur][src * a.L + j];
-  // ga_mutate for this gene (ga.py:126-137)
-  NpStream ms;
-  ms.init(a.seed, DOM_GA_MUT, g, (uint64_t)i, (uint64_t)j);
-  if (ms.random() < a.rate) {
-    if (ms.random() < a.structural) {
-      code = (int)ms.integers(a.ncodes);
-    } else {
-      const double u = ms.uniform(-a.mrange, a.mrange);
-      theta = py_mod(__dadd_rn(theta, u), kTwoPiD);
-    }
-  }
+  if (d.mut == 1) code = d.code;
+  else if (d.mut == 2) theta = py_mod(__dadd_rn(theta, d.delta), kTwoPiD);
   a.codes[nxt][i * a.L + j] = (uint8_t)code;
   a.thetas[nxt][i * a.L + j] = theta;
+}
+__device__ __forceinline__ void ga_breed_gene(const GaArgs& a, int64_t t, uint64_t g, int cur, int64_t elite) {
+  ga_breed_apply(a, t, cur, elite, ga_breed_draw(a, t, g));
 }
 
 __global__ void ga_breed_kernel(GaArgs a) {
@@ -323,7 +397,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_small_kernel(GaArgs a, int n_gen
       ga_reduce_partial_body(a, part, smax, ssum, sarg);
       __syncthreads();
     }
-    ga_reduce_sus_body(a, &s_improved, &s_elite);
+    ga_reduce_sus_body(a, &s_improved, &s_elite, NoIdleWork(), ssum, kGaRed);
     __syncthreads();
     const int64_t elite = a.st->elite;
     for (int64_t t = threadIdx.x; t < genes; t += kGaRed) ga_breed_gene(a, t, g, cur, elite);
@@ -445,19 +519,34 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     const int cur = ga_cur(a);
     fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
     grid.sync();
+    // this thread's first gene: its draws while block 0 reduces and selects
+    const int64_t t0 = (int64_t)blockIdx.x * kGaRed + threadIdx.x;
+    GeneDraw d0;
+    if (blockIdx.x != 0 && t0 < genes) d0 = ga_breed_draw(a, t0, g);
     if (blockIdx.x == 0) {
       for (int part = 0; part < a.n_parts; ++part) {
         ga_reduce_partial_body(a, part, smax, ssum, sarg);
         __syncthreads();
       }
-      ga_reduce_sus_body(a, &s_improved, &s_elite);
+      ga_reduce_sus_body(
+          a, &s_improved, &s_elite,
+          [&] {
+            if (t0 < genes) d0 = ga_breed_draw(a, t0, g);
+          },
+          ssum, kGaRed);
+      if (threadIdx.x == 0) {
+        if (t0 < genes) d0 = ga_breed_draw(a, t0, g);
+        // advance here (breeding reads g and cur from registers): the stop
+        // check at the top of the next iteration sees it after the barrier
+        // that ends breeding
+        ga_advance_body(a);
+      }
     }
     grid.sync();
     const int64_t elite = a.st->elite;
-    for (int64_t t = (int64_t)blockIdx.x * kGaRed + threadIdx.x; t < genes; t += (int64_t)gridDim.x * kGaRed)
+    if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0);
+    for (int64_t t = t0 + (int64_t)gridDim.x * kGaRed; t < genes; t += (int64_t)gridDim.x * kGaRed)
       ga_breed_gene(a, t, g, cur, elite);
-    grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) ga_advance_body(a);
     grid.sync();
   }
 }
@@ -525,7 +614,7 @@ __global__ void __launch_bounds__(kGaRed) ga_tail_kernel(GaArgs a) {
     ga_reduce_partial_body(a, part, smax, ssum, sarg);
     __syncthreads();
   }
-  ga_reduce_sus_body(a, &s_improved, &s_elite);
+  ga_reduce_sus_body(a, &s_improved, &s_elite, NoIdleWork(), ssum, kGaRed);
   __syncthreads();
   const int64_t elite = a.st->elite;
   for (int64_t t = threadIdx.x; t < a.P * a.L; t += kGaRed) ga_breed_gene(a, t, g, cur, elite);
