@@ -513,6 +513,13 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
   for (int i = threadIdx.x; i < G::D * G::D; i += kGaRed) Ts[i] = a.target[i];
   __syncthreads();
   const int64_t genes = a.P * a.L;
+  // One round (P <= warps of the grid, always true at the sizes this launch
+  // is chosen for): warp c scores circuit c and breeds child c, so the child
+  // it scores next is its own writes and breeding needs no grid barrier
+  // after it.  Otherwise genes are bred grid-stride behind a third barrier.
+  const bool one_round = a.P <= (int64_t)gridDim.x * kWarps;
+  const int lane = threadIdx.x & 31;
+  const int64_t wc = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's circuit / child
   for (int it = 0; it < n_gens; ++it) {
     if (a.st->stop) return;  // uniform across the grid: written before the last grid barrier
     const uint64_t g = a.st->generation;
@@ -520,7 +527,8 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
     grid.sync();
     // this thread's first gene: its draws while block 0 reduces and selects
-    const int64_t t0 = (int64_t)blockIdx.x * kGaRed + threadIdx.x;
+    const int64_t t0 = one_round ? (wc < a.P && lane < a.L ? wc * a.L + lane : genes)
+                                 : (int64_t)blockIdx.x * kGaRed + threadIdx.x;
     GeneDraw d0;
     if (blockIdx.x != 0 && t0 < genes) d0 = ga_breed_draw(a, t0, g);
     if (blockIdx.x == 0) {
@@ -544,10 +552,19 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     }
     grid.sync();
     const int64_t elite = a.st->elite;
-    if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0);
-    for (int64_t t = t0 + (int64_t)gridDim.x * kGaRed; t < genes; t += (int64_t)gridDim.x * kGaRed)
-      ga_breed_gene(a, t, g, cur, elite);
-    grid.sync();
+    if (one_round) {
+      if (wc < a.P) {
+        if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0);
+        for (int j = lane + 32; j < a.L; j += 32) ga_breed_gene(a, wc * a.L + j, g, cur, elite);
+      }
+      __threadfence_block();  // the warp's child, read back by its own next scoring
+      __syncwarp();
+    } else {
+      if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0);
+      for (int64_t t = t0 + (int64_t)gridDim.x * kGaRed; t < genes; t += (int64_t)gridDim.x * kGaRed)
+        ga_breed_gene(a, t, g, cur, elite);
+      grid.sync();
+    }
   }
 }
 
