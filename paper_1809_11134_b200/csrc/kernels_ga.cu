@@ -42,6 +42,7 @@ struct GaArgs {
   uint8_t* codes[2];
   double* thetas[2];
   double* fitness;
+  double* fitness_alt;  // cooperative single-barrier launch: odd generations' fitness
   int32_t* parents;
   GaDevState* st;
   GenRecord* records;
@@ -320,7 +321,8 @@ __device__ __forceinline__ GeneDraw ga_breed_draw(const GaArgs& a, int64_t t, ui
   return d;
 }
 __device__ __forceinline__ void ga_breed_apply(const GaArgs& a, int64_t t, int cur, int64_t elite,
-                                               const GeneDraw& d) {
+                                               const GeneDraw& d, const int32_t* parents = nullptr) {
+  if (parents == nullptr) parents = a.parents;
   const int nxt = cur ^ 1;
   const int64_t i = a.div_L.div((uint32_t)t);
   const int j = (int)(t - i * a.L);
@@ -332,8 +334,8 @@ __device__ __forceinline__ void ga_breed_apply(const GaArgs& a, int64_t t, int c
   const int64_t k = (i - 1) >> 1;
   const bool first = ((i - 1) & 1) == 0;
   const uint32_t k0 = (uint32_t)(2 * k), k1 = k0 + 1u;
-  const int64_t pa = a.parents[k0 - a.div_P.div(k0) * (uint32_t)a.P],
-                pb = a.parents[k1 - a.div_P.div(k1) * (uint32_t)a.P];
+  const int64_t pa = parents[k0 - a.div_P.div(k0) * (uint32_t)a.P],
+                pb = parents[k1 - a.div_P.div(k1) * (uint32_t)a.P];
   const bool inside = j >= d.p && j < d.q;
   const int64_t src = (first != inside) ? pa : pb;  // child a: a outside, b inside
   int code = a.codes[cur][src * a.L + j];
@@ -444,6 +446,7 @@ static void ga_free(GaHandle* h) {
     cudaFree(a.thetas[b]);
   }
   cudaFree(a.fitness);
+  cudaFree(a.fitness_alt);
   cudaFree(a.parents);
   cudaFree(a.st);
   cudaFree(a.records);
@@ -498,8 +501,134 @@ static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaSt
 // genomes): n generations in one cooperative launch of up to one block per
 // SM, the phases separated by grid-wide barriers — fitness (all blocks),
 // reductions + SUS (block 0), breeding (all blocks), advance (block 0).
+// Single-barrier generation of the cooperative launch (one round, P <= kGaRed,
+// one rank): after the fitness barrier EVERY block reduces the generation's
+// fitness and runs the SUS itself — identical inputs and arithmetic, so
+// identical picks — keeps its own copy of the engine state (generation, best,
+// stop) and breeds its own warps' children from its shared-memory parents.
+// Block 0 alone writes the device state, the record and the best genome.
+// `fit` is this generation's fitness buffer (generations alternate between
+// two, so a block that runs ahead into the next scoring never overwrites
+// values another block is still reading).  Returns the stop reason.
+template <class Idle>
+__device__ __forceinline__ int ga_select_local(const GaArgs& a, uint64_t g, int cur, const double* fit,
+                                               uint64_t rec_base, double& best, double* smax, double* ssum,
+                                               int64_t* sarg, int32_t* spar, int64_t* s_elite, Idle idle) {
+  __shared__ double sfit[kGaRed];
+  __shared__ int s_search, s_stop, s_improved;
+  // generation best / first argmax / sum (ga_reduce_partial_body + the combine of ga_reduce_sus_body)
+  double m = -1.0, sum = 0.0;
+  int64_t arg = INT64_MAX;
+  {
+    double lm = -1.0, ls = 0.0;
+    int64_t la = INT64_MAX;
+    for (int64_t i = threadIdx.x; i < a.P; i += kGaRed) {
+      const double f = fit[i];
+      sfit[i] = f;
+      ls += f;
+      if (f > lm) {
+        lm = f;
+        la = i;
+      }
+    }
+    smax[threadIdx.x] = lm;
+    ssum[threadIdx.x] = ls;
+    sarg[threadIdx.x] = la;
+    __syncthreads();
+    for (int off = kGaRed / 2; off >= 1; off >>= 1) {
+      if (threadIdx.x < off) {
+        const double m2 = smax[threadIdx.x + off];
+        const int64_t a2 = sarg[threadIdx.x + off];
+        if (m2 > smax[threadIdx.x] || (m2 == smax[threadIdx.x] && a2 < sarg[threadIdx.x])) {
+          smax[threadIdx.x] = m2;
+          sarg[threadIdx.x] = a2;
+        }
+        ssum[threadIdx.x] += ssum[threadIdx.x + off];
+      }
+      __syncthreads();
+    }
+    m = smax[0];
+    arg = sarg[0];
+    sum = 0.0 + ssum[0];
+  }
+  __syncthreads();  // ssum is reused for the pointers below
+  if (threadIdx.x == 0) {
+    const int improved = m > best;
+    if (improved) best = m;
+    const uint64_t gn = g + 1;
+    const int stop = best >= a.target_fitness ? 1 : (gn >= a.max_generations ? 2 : 0);
+    if (blockIdx.x == 0) {
+      GaDevState* st = a.st;
+      st->best_fitness = best;
+      st->elite = arg;
+      st->improved = improved;
+      GenRecord r;
+      r.gen_best = m;
+      r.gen_mean = sum / (double)a.P;
+      r.best_fitness = best;
+      r.pad = 0.0;
+      const uint64_t ri = g - rec_base;
+      if (ri < (uint64_t)a.rec_cap) a.records[ri] = r;
+      st->generation = gn;
+      st->stop = stop;
+    }
+    *s_elite = arg;
+    s_improved = improved;
+    s_stop = stop;
+    // sus_select (ga.py:95-116), the parallel-search form of ga_reduce_sus_body
+    NpStream rs;
+    rs.init(a.seed, DOM_GA_SUS, g, 0, 0);
+    const double total = np_pairwise_sum(sfit, a.P);
+    int search = 0;
+    if (total <= 0.0) {
+      for (int64_t k = 0; k < a.P; ++k) {
+        spar[k] = (int32_t)rs.integers(a.P);
+        if (blockIdx.x == 0) a.parents[k] = spar[k];  // isq_ga_parents
+      }
+    } else {
+      const double spacing = __ddiv_rn(total, (double)a.P);
+      double pointer = rs.uniform(0.0, spacing);
+      double cumulative = 0.0;
+      for (int k = 0; k < (int)a.P; ++k) {
+        cumulative = __dadd_rn(cumulative, sfit[k]);
+        sfit[k] = cumulative;  // C[k + 1]
+        ssum[k] = pointer;
+        pointer = __dadd_rn(pointer, spacing);
+      }
+      search = 1;
+    }
+    s_search = search;
+  } else {
+    idle();
+  }
+  __syncthreads();
+  if (s_search) {
+    for (int k = threadIdx.x; k < (int)a.P; k += kGaRed) {
+      const double pk = ssum[k];
+      int lo = 0, hi = (int)a.P - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sfit[mid] <= pk)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      spar[k] = lo;
+      if (blockIdx.x == 0) a.parents[k] = lo;  // isq_ga_parents
+    }
+  }
+  if (blockIdx.x == 0 && s_improved && threadIdx.x < 32) {
+    for (int j = threadIdx.x; j < a.L; j += 32) {
+      a.best_codes[j] = a.codes[cur][*s_elite * a.L + j];
+      a.best_thetas[j] = a.thetas[cur][*s_elite * a.L + j];
+    }
+  }
+  __syncthreads();
+  return s_stop;
+}
+
 template <int NQ>
-__global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens) {
+__global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens, int local_select) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   using G = Geo<NQ>;
@@ -520,6 +649,43 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
   const bool one_round = a.P <= (int64_t)gridDim.x * kWarps;
   const int lane = threadIdx.x & 31;
   const int64_t wc = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's circuit / child
+  if (local_select && one_round && a.P <= kGaRed) {
+    __shared__ int32_t spar[kGaRed];
+    uint64_t g = a.st->generation;
+    const uint64_t rec_base = a.st->rec_base;
+    double best = a.st->best_fitness;
+    if (a.st->stop) return;
+    // gene j of the warp's child on lane 31 - j: lane 0 (thread 0 of the
+    // block runs the SUS chains) has no gene for L < 32
+    const int jl = 31 - lane;
+    for (int it = 0; it < n_gens; ++it) {
+      const int cur = (int)(g & 1);
+      double* fit = (g & 1) ? a.fitness_alt : a.fitness;
+      fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, fit, kWarps);
+      grid.sync();
+      const int64_t t0 = wc < a.P && jl < a.L ? wc * a.L + jl : genes;
+      GeneDraw d0;
+      const int stop = ga_select_local(a, g, cur, fit, rec_base, best, smax, ssum, sarg, spar, &s_elite, [&] {
+        if (t0 < genes) d0 = ga_breed_draw(a, t0, g);
+      });
+      if (threadIdx.x == 0 && t0 < genes) d0 = ga_breed_draw(a, t0, g);
+      const int64_t elite = s_elite;
+      if (wc < a.P) {
+        if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0, spar);
+        for (int j = jl + 32; j < a.L; j += 32) ga_breed_apply(a, wc * a.L + j, cur, elite,
+                                                               ga_breed_draw(a, wc * a.L + j, g), spar);
+      }
+      __threadfence_block();  // the warp's child, read back by its own next scoring
+      __syncwarp();
+      ++g;
+      if (stop) break;
+    }
+    // the last scored generation's fitness belongs in a.fitness (isq_ga_fitness)
+    if ((g - 1) & 1) {
+      if (wc < a.P && lane == 0) a.fitness[wc] = a.fitness_alt[wc];
+    }
+    return;
+  }
   for (int it = 0; it < n_gens; ++it) {
     if (a.st->stop) return;  // uniform across the grid: written before the last grid barrier
     const uint64_t g = a.st->generation;
@@ -568,6 +734,9 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
   }
 }
 
+#ifndef ISQ_GA_LOCAL_SELECT
+#define ISQ_GA_LOCAL_SELECT 1
+#endif
 template <int NQ>
 static isq_status ga_launch_coop_nq(const GaArgs& a, int n_gens, cudaStream_t s) {
   int per_sm = 0;
@@ -580,7 +749,8 @@ static isq_status ga_launch_coop_nq(const GaArgs& a, int n_gens, cudaStream_t s)
     return ISQ_ERR_CUDA;
   }
   GaArgs args = a;
-  void* params[] = {(void*)&args, (void*)&n_gens};
+  int local_select = ISQ_GA_LOCAL_SELECT;
+  void* params[] = {(void*)&args, (void*)&n_gens, (void*)&local_select};
   ISQ_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)ga_coop_kernel<NQ>, dim3((unsigned)grid), dim3(kGaRed),
                                            params, 0, s));
   return ISQ_OK;
@@ -731,6 +901,7 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
     GA_TRY(cudaMalloc((void**)&a.thetas[b], a.P * a.L * 8));
   }
   GA_TRY(cudaMalloc((void**)&a.fitness, h->shard * h->world * 8));
+  GA_TRY(cudaMalloc((void**)&a.fitness_alt, h->shard * h->world * 8));
   GA_TRY(cudaMalloc((void**)&a.parents, a.P * 4));
   GA_TRY(cudaMalloc((void**)&a.st, sizeof(GaDevState)));
   GA_TRY(cudaMalloc((void**)&a.records, sizeof(GenRecord) * h->max_batch));
