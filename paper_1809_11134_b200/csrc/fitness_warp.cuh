@@ -301,18 +301,18 @@ struct FastEval {
     if constexpr (NQ < 5 || sizeof(R) < 8) {  // measured slower there: one gate at a time
 #pragma unroll 2
       for (; q < qe; ++q) apply_phase(diag_factor(q, sm, sh));
-      return;
+    } else {
+      for (; q + 3 < qe; q += 4) {
+        const R2 a = cm(diag_factor(q, sm, sh), diag_factor(q + 1, sm, sh));
+        const R2 b = cm(diag_factor(q + 2, sm, sh), diag_factor(q + 3, sm, sh));
+        apply_phase(cm(a, b));
+      }
+      if (q + 1 < qe) {
+        apply_phase(cm(diag_factor(q, sm, sh), diag_factor(q + 1, sm, sh)));
+        q += 2;
+      }
+      if (q < qe) apply_phase(diag_factor(q, sm, sh));
     }
-    for (; q + 3 < qe; q += 4) {
-      const R2 a = cm(diag_factor(q, sm, sh), diag_factor(q + 1, sm, sh));
-      const R2 b = cm(diag_factor(q + 2, sm, sh), diag_factor(q + 3, sm, sh));
-      apply_phase(cm(a, b));
-    }
-    if (q + 1 < qe) {
-      apply_phase(cm(diag_factor(q, sm, sh), diag_factor(q + 1, sm, sh)));
-      q += 2;
-    }
-    if (q < qe) apply_phase(diag_factor(q, sm, sh));
   }
 
   // One chunk: lane q < nq supplies (code_q, theta_q) for position base+q.
