@@ -488,6 +488,9 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
 // -------------------------------------------------------------- commit ---
 
 constexpr int kCommitThreads = 256;
+#ifndef ISQ_COMMIT_FULL_GRID
+#define ISQ_COMMIT_FULL_GRID 1
+#endif
 
 // Elitist accept + table update over the owned touches (engine.py:345-351 +
 // 202-222): a slot mutated at g-1 keeps its mutation iff some circuit of
@@ -831,7 +834,16 @@ isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
   qeqea_reduce_partials<<<a.n_parts, kRedThreads, 0, s>>>(a);
   qeqea_reduce_final<<<1, kRedThreads, 0, s>>>(a);
   const int64_t t1 = a.world * a.S * a.Lr;
+#if ISQ_COMMIT_FULL_GRID
+  {
+    // one touch per thread (no grid-stride loop): no partial last wave
+    int64_t nb = (t1 + kCommitThreads - 1) / kCommitThreads;
+    if (nb < 1) nb = 1;
+    qeqea_commit_table_kernel<<<(unsigned)nb, kCommitThreads, 0, s>>>(a, t1);
+  }
+#else
   qeqea_commit_table_kernel<<<blocks_for(t1, kCommitThreads), kCommitThreads, 0, s>>>(a, t1);
+#endif
   qeqea_advance_kernel<<<1, 1, 0, s>>>(a);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
