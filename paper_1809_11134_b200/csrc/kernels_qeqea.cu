@@ -113,7 +113,10 @@ __global__ void qeqea_unroute_kernel(QeqeaArgs a) {
 #define ISQ_VAL_PREDRAW 1
 #endif
 constexpr int kValThreads = 256;
-constexpr int kValPerThread = 3;  // touches per thread per tile: ~1 measurement task per thread
+#ifndef ISQ_VAL_PER_THREAD
+#define ISQ_VAL_PER_THREAD 3
+#endif
+constexpr int kValPerThread = ISQ_VAL_PER_THREAD;  // touches per thread per tile: ~1 measurement task per thread
 constexpr int kValTile = kValThreads * kValPerThread;
 
 // Per tile: the touches' committed records, staged by cp.async (no registers
