@@ -29,6 +29,9 @@ namespace isq {
 // bank gathers thread-level memory parallelism.
 
 constexpr int kSampleRun = 64;  // circuits per warp task of the batched sampler
+#ifndef ISQ_SAMPLE_FULL_GRID
+#define ISQ_SAMPLE_FULL_GRID 1
+#endif
 
 __global__ void __launch_bounds__(kThreadsPerBlock) qeqea_sample_flats_kernel(QeqeaArgs a) {
   __shared__ uint64_t blk[kWarpsPerBlock][128];
@@ -791,7 +794,14 @@ static cudaError_t launch_values(const QeqeaArgs& a, int64_t t1, cudaStream_t s)
 
 isq_status qeqea_launch_prepare(const QeqeaArgs& a, cudaStream_t s) {
   if (a.c0 < a.P) {
+#if ISQ_SAMPLE_FULL_GRID
+    // one warp task per warp (the hardware balances them; a persistent grid
+    // left ~8 % of the warps a fourth task)
+    const int64_t tasks = (a.S + kSampleRun - 1) / kSampleRun;
+    const int grid_s = (int)((tasks + kWarpsPerBlock - 1) / kWarpsPerBlock);
+#else
     const int grid_s = persistent_grid((const void*)qeqea_sample_flats_kernel, 0, (a.S + kSampleRun - 1) / kSampleRun);
+#endif
     qeqea_sample_flats_kernel<<<grid_s, kThreadsPerBlock, 0, s>>>(a);
   }
   if (a.world > 1) {
