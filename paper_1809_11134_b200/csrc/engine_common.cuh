@@ -37,6 +37,7 @@ struct QeqeaDevState {
   int32_t stop;          // 0 running, 1 target-reached, 2 generation-limit
   int32_t improved;      // best improved in the generation being finished
   double gen_best, gen_mean;
+  unsigned long long fit_next;  // next circuit batch of the fitness launch (dynamic scheduling)
 };
 
 struct GenRecord {

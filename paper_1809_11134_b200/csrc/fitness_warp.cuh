@@ -462,19 +462,36 @@ __device__ __forceinline__ void stage_chunk(Chunk& sm, int64_t count, int L, con
 
 // Grid-stride body shared by the explicit-gate fitness kernels: warp per
 // circuit over circuits [0, count) of (codes, thetas) rows of length L.
+// With `dyn` (a zeroed device counter) the warps take circuits in batches of
+// kFitGrab from it instead of a fixed grid stride, so a warp whose circuits
+// happened to hold more rotations does not leave the launch a tail.
+constexpr int kFitGrab = 4;
 template <int NQ, class R = double>
 __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t* __restrict__ codes,
                                              const double* __restrict__ thetas,
                                              const double2* __restrict__ Ts, FastChunkT<R>* sh,
                                              double* __restrict__ fitness, int warps_per_block,
-                                             int* bad_code = nullptr) {
+                                             int* bad_code = nullptr, unsigned long long* dyn = nullptr) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   FastChunkT<R>& cs = sh[wib];
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
-  int64_t c = (int64_t)blockIdx.x * warps_per_block + wib;
+  auto grab = [&]() -> int64_t {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(dyn, (unsigned long long)kFitGrab);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  int64_t c, cend = 0, ahead = 0;
+  if (dyn) {
+    c = grab();
+    cend = c + kFitGrab;
+    ahead = grab();  // the batch after this one, known early for the prefetch
+  } else {
+    c = (int64_t)blockIdx.x * warps_per_block + wib;
+  }
   stage_chunk(cs, count, L, codes, thetas, c, 0, lane);
-  for (; c < count; c += nwarps) {
+  while (c < count) {
+    const int64_t cn = dyn ? (c + 1 < cend ? c + 1 : ahead) : c + nwarps;  // this warp's next circuit
     FastEval<NQ, R> ev;
     ev.begin(Ts, lane);
     bool bad = false;
@@ -492,7 +509,7 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
       int64_t nc = c;
       int nb = base + 32;
       if (nb >= L) {
-        nc = c + nwarps;
+        nc = cn;
         nb = 0;
       }
       stage_chunk(cs, count, L, codes, thetas, nc, nb, lane);
@@ -503,6 +520,11 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
       fitness[c] = bad ? __longlong_as_double(0x7ff8000000000000LL) : f;  // NaN: invalid gate code
       if (bad && bad_code) atomicOr(bad_code, 1);
     }
+    if (dyn && !(c + 1 < cend)) {  // moved on to the batch grabbed ahead
+      cend = ahead + kFitGrab;
+      ahead = grab();
+    }
+    c = cn;
   }
 }
 

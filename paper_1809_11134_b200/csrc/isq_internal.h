@@ -46,7 +46,8 @@ isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uin
                                           double* fitness_dev, const int32_t* stop,
                                           cudaStream_t stream, int blocks_per_sm = 0,
                                           int precision = ISQ_PRECISION_FP64,
-                                          int* bad_code = nullptr);
+                                          int* bad_code = nullptr,
+                                          unsigned long long* dyn = nullptr);
 // Circuits holding a code that is not a gate of the wire count get a NaN
 // fitness, and *bad_code (device int, nullable) is set to 1.
 

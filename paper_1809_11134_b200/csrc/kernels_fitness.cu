@@ -26,14 +26,15 @@ template <int NQ, int MINB, class R>
 __global__ void ISQ_FIT_BOUNDS
     fitness_fast_kernel(int64_t count, int L, const uint8_t* __restrict__ codes,
                         const double* __restrict__ thetas, const double2* __restrict__ target,
-                        double* __restrict__ fitness, const int32_t* __restrict__ stop, int* bad_code) {
+                        double* __restrict__ fitness, const int32_t* __restrict__ stop, int* bad_code,
+                        unsigned long long* dyn) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
   __shared__ FastChunkT<R> sh[kFitWarps];
   if (stop != nullptr && *stop) return;
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
   __syncthreads();
-  fitness_rows<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps, bad_code);
+  fitness_rows<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps, bad_code, dyn);
 }
 
 // fp32 variant: the column of S in 64 float registers: 8 resident 2-warp
@@ -185,12 +186,13 @@ static isq_status launch_nq(int L, int64_t count, const uint8_t* codes, const do
 template <int NQ, int MINB, class R>
 static isq_status launch_fast(int L, int64_t count, const uint8_t* codes, const double* thetas,
                               const double* target, double* fitness, const int32_t* stop,
-                              int blocks_per_sm, cudaStream_t stream, int* bad_code) {
+                              int blocks_per_sm, cudaStream_t stream, int* bad_code,
+                              unsigned long long* dyn) {
   const void* k = (const void*)fitness_fast_kernel<NQ, MINB, R>;
   int grid = persistent_grid(k, 0, count, kFitWarps);
   if (blocks_per_sm > 0 && grid > num_sms() * blocks_per_sm) grid = num_sms() * blocks_per_sm;
   fitness_fast_kernel<NQ, MINB, R><<<grid, kFitThreads, 0, stream>>>(
-      count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop, bad_code);
+      count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop, bad_code, dyn);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
 }
@@ -198,27 +200,29 @@ static isq_status launch_fast(int L, int64_t count, const uint8_t* codes, const 
 template <int NQ>
 static isq_status launch_fast_prec(int L, int64_t count, const uint8_t* codes, const double* thetas,
                                    const double* target, double* fitness, const int32_t* stop,
-                                   int blocks_per_sm, int precision, cudaStream_t stream, int* bad) {
+                                   int blocks_per_sm, int precision, cudaStream_t stream, int* bad,
+                                   unsigned long long* dyn) {
   if (precision == ISQ_PRECISION_FP32)
     return launch_fast<NQ, fit_min_blocks<NQ, float>(), float>(L, count, codes, thetas, target, fitness, stop,
-                                                    blocks_per_sm, stream, bad);
+                                                    blocks_per_sm, stream, bad, dyn);
   return launch_fast<NQ, fit_min_blocks<NQ, double>(), double>(L, count, codes, thetas, target, fitness, stop,
-                                                  blocks_per_sm, stream, bad);
+                                                  blocks_per_sm, stream, bad, dyn);
 }
 
 isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uint8_t* codes,
                                           const double* thetas, const double* target,
                                           double* fitness, const int32_t* stop,
                                           cudaStream_t stream, int blocks_per_sm, int precision,
-                                          int* bad_code) {
+                                          int* bad_code, unsigned long long* dyn) {
   if (count <= 0) return ISQ_OK;
   const int b = blocks_per_sm, p = precision;
   int* bc = bad_code;
+  if (dyn != nullptr) ISQ_CUDA_TRY(cudaMemsetAsync(dyn, 0, sizeof(*dyn), stream));
   switch (n) {
-    case 2: return launch_fast_prec<2>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
-    case 3: return launch_fast_prec<3>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
-    case 4: return launch_fast_prec<4>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
-    case 5: return launch_fast_prec<5>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc);
+    case 2: return launch_fast_prec<2>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc, dyn);
+    case 3: return launch_fast_prec<3>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc, dyn);
+    case 4: return launch_fast_prec<4>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc, dyn);
+    case 5: return launch_fast_prec<5>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc, dyn);
     default:
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;

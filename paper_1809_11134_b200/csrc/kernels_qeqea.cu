@@ -29,6 +29,9 @@ namespace isq {
 // bank gathers thread-level memory parallelism.
 
 constexpr int kSampleRun = 64;  // circuits per warp task of the batched sampler
+#ifndef ISQ_FIT_DYNAMIC
+#define ISQ_FIT_DYNAMIC 1
+#endif
 #ifndef ISQ_SAMPLE_FULL_GRID
 #define ISQ_SAMPLE_FULL_GRID 1
 #endif
@@ -826,7 +829,8 @@ isq_status qeqea_launch_score(const QeqeaArgs& a, cudaStream_t s) {
   if (count > 0) {
     isq_status st = launch_fitness_batch_stoppable(a.n, a.L, count, a.gate_codes, a.gate_thetas,
                                                    reinterpret_cast<const double*>(a.target),
-                                                   a.fitness + a.c0, &a.st->stop, s, 0, a.precision);
+                                                   a.fitness + a.c0, &a.st->stop, s, 0, a.precision, nullptr,
+                                                   ISQ_FIT_DYNAMIC ? &a.st->fit_next : nullptr);
     if (st != ISQ_OK) return st;
   }
   if (a.world > 1) {
