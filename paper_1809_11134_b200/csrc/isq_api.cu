@@ -230,8 +230,15 @@ isq_status isq_fitness_batch_device_ex(int32_t n, int32_t length, int64_t count,
   isq_status st = check_shape(n, length, count);
   if (st == ISQ_OK) st = check_precision(precision);
   if (st != ISQ_OK) return st;
-  return launch_fitness_batch(n, length, count, codes_dev, thetas_dev, target_dev, fitness_dev,
-                              nullptr, (cudaStream_t)stream, precision);
+  if (count <= 0) return ISQ_OK;
+  // the dynamic-scheduling counter of this launch, stream-ordered
+  const cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* ctr = nullptr;
+  ISQ_CUDA_TRY(cudaMallocAsync((void**)&ctr, sizeof(*ctr), s));
+  st = launch_fitness_batch_stoppable(n, length, count, codes_dev, thetas_dev, target_dev, fitness_dev, nullptr,
+                                      s, 0, precision, nullptr, ctr);
+  cudaFreeAsync(ctr, s);
+  return st;
 }
 
 isq_status isq_fitness_of_unitaries(int64_t dim, int64_t count, const double* unitaries,
