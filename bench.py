@@ -15,6 +15,11 @@ ordered by one-element all-reduces) or as NCCL all-to-alls / all-gathers
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+`--gpus N` (N > 1) outside torchrun re-launches this script as N ranks
+through `torch.distributed.run` on 127.0.0.1 (one process per GPU, NCCL
+communicator init logged with NCCL_DEBUG=INFO / SUBSYS=INIT); under torchrun
+WORLD_SIZE must equal N.
+
 `--impl reference` times the reference algorithm's CPU path (the oracle port
 of evaluate_circuit, dense kron-matmul per gate) on all host cores for a
 bounded sample of the same workload per step.
@@ -210,6 +215,9 @@ def run_ours(args):
     share = world > 1 and os.environ.get("ISQ_BENCH_SHARE_GPU") == "1"
     if share:
         local = 0
+    if world > 1 and not share and torch.cuda.device_count() < world:
+        print(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPUs", file=sys.stderr)
+        sys.exit(2)
     torch.cuda.set_device(local)
     red_dev = "cpu" if share else f"cuda:{local}"
     if world > 1:
@@ -241,6 +249,21 @@ def run_ours(args):
         ops = DeviceQeqeaOps(eng, args.transport)  # binds the handle to `stream`
         comm = Comm() if world > 1 else None
         shard = ops.S
+        transport = args.transport if world > 1 else None
+        if world > 1 and args.transport == "p2p":
+            # map every rank's exchange buffers (CUDA IPC over NVLink); if any
+            # rank cannot, every rank falls back to the NCCL collectives
+            err = ""
+            try:
+                comm.connect_peers(ops)
+            except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+                err = str(exc).splitlines()[0][:200]
+            ok = torch.tensor([0 if err else 1], device=red_dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                _lib.check(lib.isq_qeqea_set_peers(eng._handle(), None))
+                ops.transport = "nccl"
+                transport = f"nccl (p2p unavailable: {err or 'on another rank'})"
         ops.begin_batch()
         for _ in range(args.warmup):
             ops.generation(comm)
@@ -270,6 +293,15 @@ def run_ours(args):
         ms = float(t.item())
     rec, _ = ops.read_batch()
     assert rec.size == args.steps + args.warmup, rec.size
+    ranks_agree = None
+    if world > 1:
+        # the reductions are replicated: every rank must hold the same records
+        mine = torch.tensor([float(rec["gen_best"].sum()), float(rec["gen_mean"].sum()),
+                             float(rec["best_fitness"][-1])], device=red_dev, dtype=torch.float64)
+        lo, hi = mine.clone(), mine.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        ranks_agree = bool(torch.equal(lo, hi))
 
     evals_per_s = P * args.steps / (ms * 1e-3)
     avg_eval_s = sum(eval_ms) / len(eval_ms) * 1e-3
@@ -298,7 +330,7 @@ def run_ours(args):
                                "Haar-random 32x32 target; bank 1.0e9 slots (36 GB) resident in HBM",
                    "n": N, "L": L, "P": P, "global_batch": P,
                    "parallelism": f"dp{world} (circuit shards x position-owned bank shards)"
-                                  + (f", {args.transport} transport" if world > 1 else ""),
+                                  + (f", {transport} transport" if world > 1 else ""),
                    "l2": "inputs larger than L2 (36 GB bank vs 126 MB)"},
         "gens_per_s": args.steps / (ms * 1e-3),
         "phase_ms": {"prepare (sample + route + lazy mutation + measure; world > 1: + 2 all-to-alls)":
@@ -320,8 +352,9 @@ def run_ours(args):
         **({"shared_gpu_functional_check": True} if share else {}),
         # per generation: sample, values, fitness, 2 reductions, commit, advance;
         # world > 1 adds route, unroute, elite (+ the fitness broadcast with p2p)
-        "gpu_launches": (7 if world == 1 else (11 if args.transport == "p2p" else 10)) * args.steps,
+        "gpu_launches": (7 if world == 1 else (11 if ops.transport == "p2p" else 10)) * args.steps,
         "best_fitness": float(rec["best_fitness"][-1]),
+        **({"ranks_agree": ranks_agree} if world > 1 else {}),
     }
 
     # e2e: the same metric through the C-ABI with host buffers (isq_fitness_batch:
@@ -437,6 +470,54 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> None:
+    """--gpus N: become one rank of N.  Under torchrun WORLD_SIZE must be N;
+    otherwise (N > 1) re-exec through torch.distributed.run and exit with
+    its status."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}", file=sys.stderr)
+            sys.exit(2)
+        return
+    if args.gpus <= 1 or (args.impl == "reference" and not args.launch_check):
+        return  # the reference arm runs on rank 0 only
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    print("bench.py: launching " + " ".join(cmd[1:]), file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def launch_check(args) -> None:
+    """--launch-check: the rank plumbing alone (gloo, no GPU work): every rank
+    joins the process group, rank 0 prints the world it saw."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank + 1])
+        dist.all_reduce(t)
+        ranks_sum = int(t.item())
+        dist.destroy_process_group()
+    else:
+        ranks_sum = 1
+    if rank == 0:
+        emit({"launch_check": True, "n_gpus": world, "ranks_sum": ranks_sum, "impl": args.impl})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -449,7 +530,12 @@ def main():
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: kernels store into peers over NVLink (p2p) or NCCL collectives between phases")
     ap.add_argument("--cpu-per-worker", type=int, default=400)
+    ap.add_argument("--launch-check", action="store_true", help="test the rank launcher only (gloo, no GPU)")
     args = ap.parse_args()
+    launch_ranks(args)
+    if args.launch_check:
+        launch_check(args)
+        return
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":

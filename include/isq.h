@@ -241,6 +241,14 @@ isq_status isq_qeqea_ipc_open(void* handle, const isq_ipc_handle* all);
 isq_status isq_qeqea_set_peers(void* handle, const isq_qeqea_peer_buffers* peers);
 isq_status isq_qeqea_read_batch(void* handle, isq_generation_record* records, int32_t* n_done,
                                 int32_t* stop_reason, uint64_t* generation, double* best_fitness);
+/* Stop rule of later generations (engine.py:354-358): pushes a changed
+ * engine.cfg.max_generations / target_fitness and engine.stop_reason (0 none,
+ * 1 target-reached, 2 generation-limit) to the device, e.g. the reference's
+ * resume_experiment(max_generations=...) (harness.py:95-110) replacing
+ * engine.cfg and clearing stop_reason, or step() after a stop, which runs
+ * another generation as the reference's does (engine.py:318-361). */
+isq_status isq_qeqea_set_limits(void* handle, int64_t max_generations, double target_fitness,
+                                int32_t stop);
 isq_status isq_qeqea_buffers(void* handle, void** fitness_dev, int64_t* shard_len, void** stream);
 /* engine.best_gates / best_fitness (gate codes + angles of length L). */
 isq_status isq_qeqea_best(void* handle, uint8_t* codes, double* thetas, double* fitness);
@@ -305,6 +313,9 @@ isq_status isq_ga_get_state(void* handle, uint8_t* codes, double* thetas, uint64
 isq_status isq_ga_set_state(void* handle, const uint8_t* codes, const double* thetas,
                             uint64_t generation, double best_fitness, int32_t stop,
                             const uint8_t* best_codes, const double* best_thetas);
+/* GaEngine counterpart of isq_qeqea_set_limits (ga.py:165-194 stop rule). */
+isq_status isq_ga_set_limits(void* handle, int64_t max_generations, double target_fitness,
+                             int32_t stop);
 isq_status isq_ga_fitness(void* handle, double* out);
 /* Parents drawn by SUS in the last finished generation (P int32). */
 isq_status isq_ga_parents(void* handle, int32_t* out);

@@ -141,6 +141,8 @@ SIGNATURES: dict[str, tuple] = {
     "isq_qeqea_live_population": (c_i32, [c_vp, c_vp, c_vp]),
     "isq_qeqea_sample": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
     "isq_qeqea_fitness": (c_i32, [c_vp, c_vp]),
+    "isq_qeqea_set_limits": (c_i32, [c_vp, c_i64, c_dbl, c_i32]),
+    "isq_ga_set_limits": (c_i32, [c_vp, c_i64, c_dbl, c_i32]),
     "isq_ga_create": (c_i32, [ctypes.POINTER(GaConfigC), c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "isq_ga_destroy": (c_i32, [c_vp]),
     "isq_ga_set_stream": (c_i32, [c_vp, c_vp]),

@@ -1108,6 +1108,31 @@ isq_status isq_ga_set_state(void* handle, const uint8_t* codes, const double* th
   return ISQ_OK;
 }
 
+isq_status isq_ga_set_limits(void* handle, int64_t max_generations, double target_fitness,
+                             int32_t stop) {
+  GaHandle* h = static_cast<GaHandle*>(handle);
+  if (!h) return ga_null_handle();
+  if (max_generations < 1) {
+    set_error("maxGenerations must be ≥ 1");
+    return ISQ_ERR_CONFIG;
+  }
+  if (!(target_fitness > 0.0 && target_fitness <= 1.0)) {
+    set_error("targetFitness must be in (0, 1]");
+    return ISQ_ERR_CONFIG;
+  }
+  if (stop < 0 || stop > 2) {
+    set_error("stop must be 0 (running), 1 (target-reached) or 2 (generation-limit)");
+    return ISQ_ERR_CONFIG;
+  }
+  ISQ_CUDA_TRY(cudaSetDevice(h->device));
+  ISQ_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->a.max_generations = (uint64_t)max_generations;
+  h->a.target_fitness = target_fitness;
+  h->graph.reset();
+  ISQ_CUDA_TRY(cudaMemcpy(&h->a.st->stop, &stop, sizeof(stop), cudaMemcpyHostToDevice));
+  return ISQ_OK;
+}
+
 isq_status isq_ga_fitness(void* handle, double* out) {
   GaHandle* h = static_cast<GaHandle*>(handle);
   if (!h) return ga_null_handle();

@@ -140,10 +140,73 @@ def _target_array(target: TargetSpec | np.ndarray, n: int, name: str = "target")
     return np.ascontiguousarray(m, dtype=np.complex128)
 
 
-class QeqeaEngine:
+class _DeviceLimits:
+    """`cfg` and `stop_reason` mirrored onto the device handle.
+
+    The reference's resume flow (harness.py:95-110) replaces `engine.cfg`
+    with a larger max_generations and clears `stop_reason`; the device stop
+    rule (engine.py:354-358, ga.py:189-192) reads both from the handle, so
+    assigning either attribute pushes them with isq_*_set_limits.
+    """
+
+    _limits_fn = ""
+    _structural: Tuple[str, ...] = ()
+
+    @property
+    def cfg(self):
+        return self.__dict__["_cfg"]
+
+    @cfg.setter
+    def cfg(self, cfg):
+        old = self.__dict__.get("_cfg")
+        if old is not None:
+            changed = [f for f in self._structural if getattr(old, f) != getattr(cfg, f)]
+            if changed:
+                raise ConfigurationError(
+                    f"cannot change {', '.join(changed)} of a live engine (only the stop rule)")
+        self.__dict__["_cfg"] = cfg
+        self._push_limits()
+
+    @property
+    def stop_reason(self) -> Optional[str]:
+        return self.__dict__.get("_stop_reason")
+
+    @stop_reason.setter
+    def stop_reason(self, reason: Optional[str]):
+        if reason not in _STOP_CODES:
+            raise ConfigurationError(f"stop_reason must be one of {sorted(map(str, _STOP_CODES))}")
+        self.__dict__["_stop_reason"] = reason
+        self._push_limits()
+
+    def _push_limits(self):
+        h = self.__dict__.get("_h")
+        if h is None or h.value is None:
+            return
+        c = self.cfg
+        _lib.check(getattr(self._lib, self._limits_fn)(h, int(c.max_generations), float(c.target_fitness),
+                                                       _STOP_CODES[self.stop_reason]))
+
+    def _step_once(self):
+        """One generation even after a stop, as the reference's step() runs
+        one whenever it is called (engine.py:318-361, ga.py:165-194); the
+        stop reason is then re-derived by the device and, as in the
+        reference, never cleared by the step itself."""
+        prev = self.stop_reason
+        if prev is not None:
+            self.stop_reason = None
+        rec = self.steps(1)
+        if prev is not None and self.stop_reason is None:
+            self.stop_reason = prev
+        return float(rec["gen_best"][0]), float(rec["gen_mean"][0])
+
+
+class QeqeaEngine(_DeviceLimits):
     """Stepwise generation loop on one device (or one rank of a sharded run)."""
 
     algorithm = "qeqea"
+    _limits_fn = "isq_qeqea_set_limits"
+    _structural = ("number_of_wires", "size_of_individual", "size_of_population",
+                   "probability_of_mutation", "mutation_range", "n_meas", "memory_cap_entries")
 
     def __init__(
         self,
@@ -179,7 +242,7 @@ class QeqeaEngine:
         self._open()
         self.generation = 0
         self.best_fitness = 0.0
-        self.stop_reason: Optional[str] = None
+        self.__dict__["_stop_reason"] = None
         self._best_gates: List[GateOp] = []
         self._best_dirty = False
         if population is not None:
@@ -326,14 +389,12 @@ class QeqeaEngine:
             if rec["best_fitness"][-1] > self.best_fitness:
                 self._best_dirty = True
             self.best_fitness = float(rec["best_fitness"][-1])
-        self.stop_reason = STOP_REASONS[int(stop)]
+        self.__dict__["_stop_reason"] = STOP_REASONS[int(stop)]  # already the device's
 
     def step(self) -> Tuple[float, float]:
-        """One generation; returns (generation best, generation mean) (engine.py:318-361)."""
-        rec = self.steps(1)
-        if rec.size == 0:
-            raise RuntimeError("engine already stopped: " + str(self.stop_reason))
-        return float(rec["gen_best"][0]), float(rec["gen_mean"][0])
+        """One generation; returns (generation best, generation mean) (engine.py:318-361).
+        Like the reference, a step after a stop still runs a generation."""
+        return self._step_once()
 
     @property
     def best_gates(self) -> List[GateOp]:

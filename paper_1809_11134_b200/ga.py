@@ -18,7 +18,7 @@ from typing import List, Optional, Tuple
 import numpy as np
 
 from . import _lib
-from .engine import STOP_REASONS, _STOP_CODES, _target_array
+from .engine import STOP_REASONS, _STOP_CODES, _DeviceLimits, _target_array
 from .errors import ConfigurationError
 from .fitness import TargetSpec
 from .gates import Axis, GateOp, encode_gates, gate_from_code
@@ -62,10 +62,13 @@ class GaConfig:
         return protos
 
 
-class GaEngine:
+class GaEngine(_DeviceLimits):
     """Generational GA loop with the same step interface as QeqeaEngine."""
 
     algorithm = "ga"
+    _limits_fn = "isq_ga_set_limits"
+    _structural = ("number_of_wires", "size_of_individual", "population", "mutation_rate",
+                   "mutation_range", "structural_rate")
 
     def __init__(self, cfg: GaConfig, target: TargetSpec, seed: int, workers: int = 1, *,
                  device: int = 0, genomes: Optional[List[CircuitGenome]] = None,
@@ -89,7 +92,7 @@ class GaEngine:
         self._open()
         self.generation = 0
         self.best_fitness = 0.0
-        self.stop_reason: Optional[str] = None
+        self.__dict__["_stop_reason"] = None
         self._best_gates: List[GateOp] = []
         self._best_dirty = False
         if genomes is not None:
@@ -190,14 +193,12 @@ class GaEngine:
             if rec["best_fitness"][-1] > self.best_fitness:
                 self._best_dirty = True
             self.best_fitness = float(rec["best_fitness"][-1])
-        self.stop_reason = STOP_REASONS[int(stop)]
+        self.__dict__["_stop_reason"] = STOP_REASONS[int(stop)]  # already the device's
 
     def step(self) -> Tuple[float, float]:
-        """One generation (ga.py:165-194); returns (generation best, mean)."""
-        rec = self.steps(1)
-        if rec.size == 0:
-            raise RuntimeError("engine already stopped: " + str(self.stop_reason))
-        return float(rec["gen_best"][0]), float(rec["gen_mean"][0])
+        """One generation (ga.py:165-194); returns (generation best, mean).
+        Like the reference, a step after a stop still runs a generation."""
+        return self._step_once()
 
     @property
     def best_gates(self) -> List[GateOp]:

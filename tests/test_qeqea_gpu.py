@@ -246,3 +246,32 @@ def test_handles_release_their_device_memory():
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info()[0]
     assert abs(free1 - free0) < 64 << 20, (free0, free1)
+
+
+@pytest.mark.parametrize("n_meas", [1, 3, 11])
+def test_device_measurement_matches_reference_goldens(n_meas):
+    """construct_segments on the device (Born probabilities, multinomial by
+    binomial inversion, argmax) against the reference's own measurements
+    (measure.npz: engine.construct_segments per slot stream, generations 0
+    and 9).  probability_of_mutation = 0 keeps the bank fixed across the
+    generations, so every touched rotation slot's gate code carries the axis
+    the reference measured for it."""
+    from paper_1809_11134_b200.engine import PopulationConfig, PopulationState, QeqeaEngine
+    from paper_1809_11134_b200.fitness import target_matrix
+
+    g = golden("measure")
+    q = g[f"nm{n_meas}_qutrits"]
+    cfg = PopulationConfig(number_of_wires=3, size_of_individual=8, size_of_population=25, n_meas=n_meas,
+                           probability_of_mutation=0.0)
+    assert q.shape == (cfg.qutrit_count, 3)
+    pop = PopulationState(np.zeros(cfg.qubit_count), q.copy())
+    eng = QeqeaEngine(cfg, target_matrix("Toffoli"), seed=11, population=pop)
+    checked = 0
+    for gen in range(10):
+        if gen in (0, 9):
+            flats, codes, _ = eng.sample()
+            rot = flats < cfg.qutrit_count
+            assert np.array_equal(codes[rot] % 3, g[f"nm{n_meas}_g{gen}_axes"][flats[rot]]), gen
+            checked += int(rot.sum())
+        eng.step()
+    assert checked > 100
