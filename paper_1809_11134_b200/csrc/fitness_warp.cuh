@@ -51,13 +51,22 @@ struct Cplx<float> {
 
 // Per-warp shared scratch for one 32-gate chunk (R: arithmetic type of the
 // state, double or the fp32 variant's float).
-template <class R>
+// Rotations whose flush factors one phase pass stores before the state pass
+// applies them (FastEval::chunk).
+#ifndef ISQ_FIT_NR
+#define ISQ_FIT_NR 8
+#endif
+constexpr int kFitNR = ISQ_FIT_NR;
+
+template <class R, int NR = kFitNR>
 struct FastChunkT {
   using R2 = typename Cplx<R>::T;
+  static constexpr int kNR = NR;
   R2 cs2[32][2];       // diag: {unused, e^{-i th/2}}; rotation: {(C = cos a, 0), (p, q)}
   uint32_t rpar[32];   // diag: bit r = parity of row r under the gate's wire mask; 0 for rotations
   int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit (n = 5)
-  R2 fac[32];          // flush factors, indexed by physical row
+  R2 rfac[NR][16];     // flush factors of the batch's rotations: n = 5 the 16 rows with the
+                       // rotation's bit set (row with the bit removed), n < 5 every row
   double nth[32];      // next chunk's angles / codes, staged by cp.async (no registers held)
   uint32_t ncode[8];
 };
@@ -69,17 +78,28 @@ enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
 // for (__launch_bounds__ min blocks): n = 5 holds a 32-row column in
 // registers; with a bound of 5 blocks ptxas still allocates 168 registers
 // (6 resident blocks, 3 warps per scheduler) and schedules 1.6 % faster code
-// than with the bound of 6 (7 blocks spill 1.4 KB per thread); n = 4
-// (16 rows over 2 lanes) runs 10 blocks (measured 6 % faster than 6; 8 and
-// 12 are no better); n = 3 is bound by per-gate overhead, not occupancy.
+// than with the bound of 6 (7 blocks spill 1.4 KB per thread).  n <= 4 run
+// the several-circuits-per-warp evaluator (fitness_multi.cuh): a 2^n-row
+// column per lane.
 #ifndef ISQ_FIT64_MINB
 #define ISQ_FIT64_MINB 5
 #endif
+// n <= ISQ_MULTI_MAXNQ run the several-circuits-per-warp evaluator
+// (fitness_multi.cuh: a 2^n-row column per lane), larger n this one.
+#ifndef ISQ_MULTI_MAXNQ
+#define ISQ_MULTI_MAXNQ 3
+#endif
 #ifndef ISQ_FIT64_MINB4
-#define ISQ_FIT64_MINB4 10
+#define ISQ_FIT64_MINB4 10  // this evaluator: 16 rows over 2 lanes
 #endif
 #ifndef ISQ_FIT64_MINB3
 #define ISQ_FIT64_MINB3 6
+#endif
+#ifndef ISQ_FIT64_MULTI_MINB4
+#define ISQ_FIT64_MULTI_MINB4 8
+#endif
+#ifndef ISQ_FIT64_MULTI_MINB3
+#define ISQ_FIT64_MULTI_MINB3 12
 #endif
 #ifndef ISQ_FIT32_MINB4
 #define ISQ_FIT32_MINB4 8
@@ -87,12 +107,21 @@ enum : int { GT_DIAG = 0, GT_RX = 1, GT_RY = 2 };
 #ifndef ISQ_FIT32_MINB3
 #define ISQ_FIT32_MINB3 8
 #endif
+#ifndef ISQ_FIT32_MULTI_MINB
+#define ISQ_FIT32_MULTI_MINB 16
+#endif
 template <int NQ, class R>
 constexpr int fit_min_blocks() {
-  if constexpr (sizeof(R) == 8)
-    return NQ >= 5 ? ISQ_FIT64_MINB : (NQ == 4 ? ISQ_FIT64_MINB4 : ISQ_FIT64_MINB3);
-  else
-    return NQ >= 5 ? 8 : (NQ == 4 ? ISQ_FIT32_MINB4 : ISQ_FIT32_MINB3);
+  constexpr bool multi = NQ <= ISQ_MULTI_MAXNQ;
+  if constexpr (sizeof(R) == 8) {
+    if constexpr (NQ >= 5) return ISQ_FIT64_MINB;
+    if constexpr (multi) return NQ == 4 ? ISQ_FIT64_MULTI_MINB4 : ISQ_FIT64_MULTI_MINB3;
+    return NQ == 4 ? ISQ_FIT64_MINB4 : ISQ_FIT64_MINB3;
+  } else {
+    if constexpr (NQ >= 5) return 8;
+    if constexpr (multi) return ISQ_FIT32_MULTI_MINB;
+    return NQ == 4 ? ISQ_FIT32_MINB4 : ISQ_FIT32_MINB3;
+  }
 }
 
 constexpr double kPi = 3.141592653589793;
@@ -149,11 +178,11 @@ __device__ __forceinline__ uint32_t row_parity(int mask) {
   return p;
 }
 
-template <int NQ, class R = double>
+template <int NQ, class R = double, int NR = kFitNR>
 struct FastEval {
   using G = Geo<NQ>;
   using R2 = typename Cplx<R>::T;
-  using Chunk = FastChunkT<R>;
+  using Chunk = FastChunkT<R, NR>;
   WarpUnitary<NQ, R> st;
   R wr, wi;  // pending phase factor e^{i phi} of physical row `lane` (lane < D)
 
@@ -212,12 +241,16 @@ struct FastEval {
       r = remainder(theta, kTwoPi);
     double sn, cs;
     sincos_pi4(-0.25 * r, sn, cs);
-    const double C = fma(cs, cs, -sn * sn), S = 2.0 * sn * cs;
+    // cos a as the lifting produces it (1 + p q): every gate type then gives
+    // the same cos, so circuits that differ only in a measured axis tie
+    // exactly, as the reference's dense products do (a single-gate circuit
+    // on the identity scores 4|cos(th/2)| for Rx, Ry, Rz and ZZ alike)
+    const double S = 2.0 * sn * cs, pl = -sn / cs, C = fma(pl, S, 1.0);
     if (b >= 0) {
       info = type | (b << 8);
       rpar = 0;
       e0 = Cplx<R>::make(R(C), R(0));
-      e1 = Cplx<R>::make(R(-sn / cs), R(S));
+      e1 = Cplx<R>::make(R(pl), R(S));
     } else {
       info = GT_DIAG;
       rpar = row_parity(mask);
@@ -226,7 +259,19 @@ struct FastEval {
     }
   }
 
-  // Multiply the register rows with bit B set by fac[row] (flush of pending deltas).
+  // Flush factor of physical row r1 (bit B set) in a rotation's rfac row:
+  // n = 5 keeps only the rows with the bit set, indexed by the row with bit B
+  // removed; n < 5 keeps every row.
+  template <int B>
+  static __device__ __forceinline__ int fac_index(int r1) {
+    if constexpr (NQ == 5)
+      return ((r1 >> (B + 1)) << B) | (r1 & ((1 << B) - 1));
+    else
+      return r1;
+  }
+
+  // Multiply the register rows with bit B set by their flush factor (n < 5,
+  // lane-held row bit: every row of the upper lanes; the lower lanes' factors are 1).
   template <int B>
   __device__ __forceinline__ void flush_bit(const R2* fac, int lane) {
     const int h = (lane >> NQ) & (G::LPC - 1);
@@ -251,7 +296,7 @@ struct FastEval {
       for (int r = 0; r < G::E; ++r) {
         if (r & m) continue;
         const int r1 = r | m;
-        const R2 f = fac[h * G::E + r1];
+        const R2 f = fac[fac_index<B>(h * G::E + r1)];
         st.cmul(r1, f.x, f.y);
         st.re[r] = fma(p, st.im[r1], st.re[r]);
         st.im[r1] = fma(q, st.re[r], st.im[r1]);
@@ -315,10 +360,23 @@ struct FastEval {
     }
   }
 
+  // Type | row bit << 8 of rotation qr (bit planes at n < 5, shared memory at n = 5).
+  __device__ __forceinline__ int rot_info(int qr, const Chunk& sm, unsigned ryb, unsigned bp0, unsigned bp1,
+                                          unsigned bp2) const {
+    if constexpr (NQ < 5)
+      return (((bp0 >> qr) & 1) << 8) | (((bp1 >> qr) & 1) << 9) | (((bp2 >> qr) & 1) << 10) |
+             (((ryb >> qr) & 1) ? GT_RY : GT_RX);
+    else
+      return sm.info[qr];
+  }
+
   // One chunk: lane q < nq supplies (code_q, theta_q) for position base+q.
-  // The rotation positions are found with one ballot; the diagonal runs
-  // between them touch only the pending phase (diag_run), the rotations
-  // flush the non-commuting part of it and rotate the register state.
+  // The pending row phases do not depend on the state, so each batch of up
+  // to kFitNR rotations runs in two passes: a phase pass walks the gates
+  // (diagonal runs between rotations touch only the pending phase,
+  // diag_run) and stores every rotation's flush factors, then a state pass
+  // applies the batch's flushes and liftings back to back, with no
+  // shuffle / shared-memory round trip between two rotations.
   // Returns true (warp-uniform) when a lane's code is not a valid gate code.
   __device__ __forceinline__ bool chunk(int code, double theta, int nq, Chunk& sm, int lane) {
     int info = GT_DIAG;  // lanes past the end: neutral diagonal, no parity
@@ -327,15 +385,14 @@ struct FastEval {
     if (lane < nq) prepare(code, theta, info, rpar, e0, e1);
     const bool bad = __any_sync(0xffffffffu, lane < nq && (code < 0 || code >= G::NCODES));
     // n <= 4: each rotation's type and row bit as warp-uniform bit planes (no
-    // shared-memory round trip on the rotation's critical path: -3 % at n = 3,
-    // 4); n = 5 reads them back from shared memory (the bit planes cost it
-    // spills: +1.5 %)
+    // shared-memory round trip: -3 % at n = 3, 4); n = 5 reads them back from
+    // shared memory (the bit planes cost it spills: +1.5 %)
     constexpr bool kPlanes = NQ < 5;
     if constexpr (!kPlanes) sm.info[lane] = info;
     sm.rpar[lane] = rpar;
     sm.cs2[lane][0] = e0;
     sm.cs2[lane][1] = e1;
-    unsigned rot = __ballot_sync(0xffffffffu, info != GT_DIAG);
+    unsigned todo = __ballot_sync(0xffffffffu, info != GT_DIAG);
     unsigned ryb = 0, bp0 = 0, bp1 = 0, bp2 = 0;
     if constexpr (kPlanes) {
       ryb = __ballot_sync(0xffffffffu, (info & 3) == GT_RY);
@@ -347,44 +404,50 @@ struct FastEval {
     const int row = lane;  // physical row whose phase this lane carries
     const int sh = 31 - row;
     int q = 0;
-    while (rot) {
-      const int qr = __ffs(rot) - 1;
-      diag_run(q, qr, sm, sh);
-      rot &= rot - 1;
-      q = qr + 1;
-      int inf;
-      if constexpr (kPlanes)
-        inf = (((bp0 >> qr) & 1) << 8) | (((bp1 >> qr) & 1) << 9) | (((bp2 >> qr) & 1) << 10) |
-              (((ryb >> qr) & 1) ? GT_RY : GT_RX);
-      else
-        inf = sm.info[qr];
-      const int b = inf >> 8;
-      const int m = 1 << b;
-      const bool ry = (inf & 3) == GT_RY;
-      const bool hib = (row & m) != 0;
-      // flush factor of the rows with bit b set: w_r * conj(w_{r^m}), times -i
-      // for Ry (S^dagger); those rows then carry their partner's phase (times
-      // +i for Ry: S), which commutes with the Rx.  Rows with the bit clear
-      // keep their phase; their factor is only read for lane-bit rotations
-      // (n < 5), where it must be 1.
-      // (the partner's phase comes over times i for Ry: o' = i o, so that
-      // w conj(o') = -i w conj(o) and the new phase is o')
-      const R orr = __shfl_xor_sync(0xffffffffu, ry ? -wi : wr, m);
-      const R ori = __shfl_xor_sync(0xffffffffu, ry ? wr : wi, m);
-      R fr = fma(wr, orr, wi * ori), fi = fma(wi, orr, -wr * ori);
-      if constexpr (G::LB > 0) {
-        fr = hib ? fr : R(1);
-        fi = hib ? fi : R(0);
+    while (todo) {
+      // phase pass over the next kFitNR rotations
+      unsigned t = todo;
+      int k = 0;
+      while (t && k < NR) {
+        const int qr = __ffs(t) - 1;
+        diag_run(q, qr, sm, sh);
+        t &= t - 1;
+        q = qr + 1;
+        const int inf = rot_info(qr, sm, ryb, bp0, bp1, bp2);
+        const int b = inf >> 8;
+        const int m = 1 << b;
+        const bool ry = (inf & 3) == GT_RY;
+        const bool hib = (row & m) != 0;
+        // flush factor of the rows with bit b set: w_r * conj(w_{r^m}), times -i
+        // for Ry (S^dagger); those rows then carry their partner's phase (times
+        // +i for Ry: S), which commutes with the Rx.  (The partner's phase
+        // comes over times i for Ry: o' = i o, so that w conj(o') = -i w conj(o)
+        // and the new phase is o'.)  n < 5: rows with the bit clear store 1,
+        // read by the lane-bit flush of the upper lanes only.
+        const R orr = __shfl_xor_sync(0xffffffffu, ry ? -wi : wr, m);
+        const R ori = __shfl_xor_sync(0xffffffffu, ry ? wr : wi, m);
+        const R fr = fma(wr, orr, wi * ori), fi = fma(wi, orr, -wr * ori);
+        if constexpr (NQ == 5) {
+          if (hib) sm.rfac[k][((row >> (b + 1)) << b) | (row & (m - 1))] = Cplx<R>::make(fr, fi);
+        } else {
+          if (row < G::D) sm.rfac[k][row] = hib ? Cplx<R>::make(fr, fi) : Cplx<R>::make(R(1), R(0));
+        }
+        if (hib) {
+          wr = orr;
+          wi = ori;
+        }
+        ++k;
       }
-      sm.fac[lane] = Cplx<R>::make(fr, fi);
-      if (hib) {
-        wr = orr;
-        wi = ori;
-      }
-      const R2 pq = sm.cs2[qr][1];
-      const R C = sm.cs2[qr][0].x;
       __syncwarp();
-      flush_rotate(b, sm.fac, pq.x, pq.y, C, lane);
+      // state pass: the batch's flushes + liftings back to back
+      for (int i = 0; i < k; ++i) {
+        const int qr = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int b = rot_info(qr, sm, ryb, bp0, bp1, bp2) >> 8;
+        const R2 pq = sm.cs2[qr][1];
+        const R C = sm.cs2[qr][0].x;
+        flush_rotate(b, sm.rfac[i], pq.x, pq.y, C, lane);
+      }
       __syncwarp();
     }
     diag_run(q, nq, sm, sh);
@@ -469,15 +532,15 @@ __device__ __forceinline__ void stage_chunk(Chunk& sm, int64_t count, int L, con
 #define ISQ_FIT_GRAB 4
 #endif
 constexpr int kFitGrab = ISQ_FIT_GRAB;  // measured: 4 best (1: +1 %, 2 and 8: +0.2 %)
-template <int NQ, class R = double>
+template <int NQ, class R = double, int NR = kFitNR>
 __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t* __restrict__ codes,
                                              const double* __restrict__ thetas,
-                                             const double2* __restrict__ Ts, FastChunkT<R>* sh,
+                                             const double2* __restrict__ Ts, FastChunkT<R, NR>* sh,
                                              double* __restrict__ fitness, int warps_per_block,
                                              int* bad_code = nullptr, unsigned long long* dyn = nullptr) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  FastChunkT<R>& cs = sh[wib];
+  FastChunkT<R, NR>& cs = sh[wib];
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
   auto grab = [&]() -> int64_t {
     unsigned long long v = 0;
@@ -495,7 +558,7 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
   stage_chunk(cs, count, L, codes, thetas, c, 0, lane);
   while (c < count) {
     const int64_t cn = dyn ? (c + 1 < cend ? c + 1 : ahead) : c + nwarps;  // this warp's next circuit
-    FastEval<NQ, R> ev;
+    FastEval<NQ, R, NR> ev;
     ev.begin(Ts, lane);
     bool bad = false;
     for (int base = 0; base < L; base += 32) {

@@ -2,6 +2,7 @@
 // readout, the functional API).  Replaces compose_gates + fitness_value
 // (gates.py:187-195, fitness.py:36-49) for a batch of circuits.
 #include "isq_internal.h"
+#include "fitness_multi.cuh"
 #include "fitness_warp.cuh"
 #include "unitary_warp.cuh"
 
@@ -30,11 +31,11 @@ __global__ void ISQ_FIT_BOUNDS
                         unsigned long long* dyn) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunkT<R> sh[kFitWarps];
+  __shared__ FitScratch<NQ, R> sh[kFitWarps];
   if (stop != nullptr && *stop) return;
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = target[i];
   __syncthreads();
-  fitness_rows<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps, bad_code, dyn);
+  fitness_rows_fast<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, kFitWarps, bad_code, dyn);
 }
 
 // fp32 variant: the column of S in 64 float registers: 8 resident 2-warp
@@ -189,7 +190,8 @@ static isq_status launch_fast(int L, int64_t count, const uint8_t* codes, const 
                               int blocks_per_sm, cudaStream_t stream, int* bad_code,
                               unsigned long long* dyn) {
   const void* k = (const void*)fitness_fast_kernel<NQ, MINB, R>;
-  int grid = persistent_grid(k, 0, count, kFitWarps);
+  const int64_t warps = (count + kFitCPW<NQ> - 1) / kFitCPW<NQ>;
+  int grid = persistent_grid(k, 0, warps, kFitWarps);
   if (blocks_per_sm > 0 && grid > num_sms() * blocks_per_sm) grid = num_sms() * blocks_per_sm;
   fitness_fast_kernel<NQ, MINB, R><<<grid, kFitThreads, 0, stream>>>(
       count, L, codes, thetas, reinterpret_cast<const double2*>(target), fitness, stop, bad_code, dyn);

@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 
 #include "engine_common.cuh"
+#include "fitness_multi.cuh"
 #include "fitness_warp.cuh"
 #include "isq_internal.h"
 
@@ -65,12 +66,12 @@ template <int NQ, int MINB, class R>
 __global__ void __launch_bounds__(kFitThreads, MINB) ga_eval_kernel(GaArgs a, int64_t c0, int64_t c1) {
   using G = Geo<NQ>;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunkT<R> sh[kFitWarps];
+  __shared__ FitScratch<NQ, R> sh[kFitWarps];
   if (a.st->stop) return;
   const int cur = ga_cur(a);
   for (int i = threadIdx.x; i < G::D * G::D; i += blockDim.x) Ts[i] = a.target[i];
   __syncthreads();
-  fitness_rows<NQ, R>(c1 - c0, a.L, a.codes[cur] + c0 * a.L, a.thetas[cur] + c0 * a.L, Ts, sh,
+  fitness_rows_fast<NQ, R>(c1 - c0, a.L, a.codes[cur] + c0 * a.L, a.thetas[cur] + c0 * a.L, Ts, sh,
                       a.fitness + c0, kFitWarps);
 }
 
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_small_kernel(GaArgs a, int n_gen
   using G = Geo<NQ>;
   constexpr int kWarps = kGaRed / 32;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kWarps];
+  __shared__ FitScratch<NQ, double, kSmallNR> sh[kWarps];
   __shared__ double smax[kGaRed], ssum[kGaRed];
   __shared__ int64_t sarg[kGaRed];
   __shared__ int s_improved;
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_small_kernel(GaArgs a, int n_gen
     if (a.st->stop) return;  // uniform: written by thread 0 before the barrier
     const uint64_t g = a.st->generation;
     const int cur = ga_cur(a);
-    fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
+    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
     __syncthreads();
     for (int part = 0; part < a.n_parts; ++part) {
       ga_reduce_partial_body(a, part, smax, ssum, sarg);
@@ -469,7 +470,8 @@ static int ga_blocks(int64_t n) {
 template <int NQ, int MINB, class R>
 static isq_status ga_launch_eval_nq(const GaArgs& a, int64_t c0, int64_t c1, cudaStream_t s) {
   const void* k = (const void*)ga_eval_kernel<NQ, MINB, R>;
-  const int grid = persistent_grid(k, 0, c1 - c0, kFitWarps);
+  const int64_t warps = (c1 - c0 + kFitCPW<NQ> - 1) / kFitCPW<NQ>;
+  const int grid = persistent_grid(k, 0, warps, kFitWarps);
   ga_eval_kernel<NQ, MINB, R><<<grid, kFitThreads, 0, s>>>(a, c0, c1);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
@@ -634,7 +636,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
   using G = Geo<NQ>;
   constexpr int kWarps = kGaRed / 32;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kWarps];
+  __shared__ FitScratch<NQ, double, kSmallNR> sh[kWarps];
   __shared__ double smax[kGaRed], ssum[kGaRed];
   __shared__ int64_t sarg[kGaRed];
   __shared__ int s_improved;
@@ -642,47 +644,57 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
   for (int i = threadIdx.x; i < G::D * G::D; i += kGaRed) Ts[i] = a.target[i];
   __syncthreads();
   const int64_t genes = a.P * a.L;
-  // One round (P <= warps of the grid, always true at the sizes this launch
-  // is chosen for): warp c scores circuit c and breeds child c, so the child
-  // it scores next is its own writes and breeding needs no grid barrier
-  // after it.  Otherwise genes are bred grid-stride behind a third barrier.
-  const bool one_round = a.P <= (int64_t)gridDim.x * kWarps;
+  // One round (P <= circuits of one pass of the grid, always true at the
+  // sizes this launch is chosen for): warp w scores circuits [w CPW, (w+1) CPW)
+  // (fitness_rows_fast: CPW = 1 at n = 5, 32 / 2^n below) and breeds the same
+  // children, so what it scores next is its own writes and breeding needs no
+  // grid barrier after it.  Otherwise genes are bred grid-stride behind a
+  // third barrier.
+  constexpr int CPW = kFitCPW<NQ>;
+  const bool one_round = a.P <= (int64_t)gridDim.x * kWarps * CPW;
   const int lane = threadIdx.x & 31;
-  const int64_t wc = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's circuit / child
+  const int64_t wc = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's batch
+  const int64_t wt0 = wc * CPW * a.L;          // first gene of the warp's children
+  const int wgenes = CPW * a.L;                // genes of the warp's children
+  auto wgene = [&](int u) -> int64_t {         // u-th gene of the warp's children (or `genes`)
+    const int64_t t = wt0 + u;
+    return u < wgenes && t < genes ? t : genes;
+  };
   if (local_select && one_round && a.P <= kGaRed) {
     __shared__ int32_t spar[kGaRed];
     uint64_t g = a.st->generation;
     const uint64_t rec_base = a.st->rec_base;
     double best = a.st->best_fitness;
     if (a.st->stop) return;
-    // gene j of the warp's child on lane 31 - j: lane 0 (thread 0 of the
-    // block runs the SUS chains) has no gene for L < 32
+    // gene u of the warp's children on lane 31 - u (mod 32): lane 0 (thread 0
+    // of the block runs the SUS chains) has no gene when they hold < 32
     const int jl = 31 - lane;
     for (int it = 0; it < n_gens; ++it) {
       const int cur = (int)(g & 1);
       double* fit = (g & 1) ? a.fitness_alt : a.fitness;
-      fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, fit, kWarps);
+      fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, fit, kWarps);
       grid.sync();
-      const int64_t t0 = wc < a.P && jl < a.L ? wc * a.L + jl : genes;
+      const int64_t t0 = wgene(jl);
       GeneDraw d0;
       const int stop = ga_select_local(a, g, cur, fit, rec_base, best, smax, ssum, sarg, spar, &s_elite, [&] {
         if (t0 < genes) d0 = ga_breed_draw(a, t0, g);
       });
       if (threadIdx.x == 0 && t0 < genes) d0 = ga_breed_draw(a, t0, g);
       const int64_t elite = s_elite;
-      if (wc < a.P) {
-        if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0, spar);
-        for (int j = jl + 32; j < a.L; j += 32) ga_breed_apply(a, wc * a.L + j, cur, elite,
-                                                               ga_breed_draw(a, wc * a.L + j, g), spar);
+      if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0, spar);
+      for (int u = jl + 32; u < wgenes; u += 32) {
+        const int64_t t = wgene(u);
+        if (t < genes) ga_breed_apply(a, t, cur, elite, ga_breed_draw(a, t, g), spar);
       }
-      __threadfence_block();  // the warp's child, read back by its own next scoring
+      __threadfence_block();  // the warp's children, read back by its own next scoring
       __syncwarp();
       ++g;
       if (stop) break;
     }
     // the last scored generation's fitness belongs in a.fitness (isq_ga_fitness)
     if ((g - 1) & 1) {
-      if (wc < a.P && lane == 0) a.fitness[wc] = a.fitness_alt[wc];
+      for (int i = lane; i < CPW; i += 32)
+        if (wc * CPW + i < a.P) a.fitness[wc * CPW + i] = a.fitness_alt[wc * CPW + i];
     }
     return;
   }
@@ -690,11 +702,10 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     if (a.st->stop) return;  // uniform across the grid: written before the last grid barrier
     const uint64_t g = a.st->generation;
     const int cur = ga_cur(a);
-    fitness_rows<NQ>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
+    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
     grid.sync();
     // this thread's first gene: its draws while block 0 reduces and selects
-    const int64_t t0 = one_round ? (wc < a.P && lane < a.L ? wc * a.L + lane : genes)
-                                 : (int64_t)blockIdx.x * kGaRed + threadIdx.x;
+    const int64_t t0 = one_round ? wgene(lane) : (int64_t)blockIdx.x * kGaRed + threadIdx.x;
     GeneDraw d0;
     if (blockIdx.x != 0 && t0 < genes) d0 = ga_breed_draw(a, t0, g);
     if (blockIdx.x == 0) {
@@ -719,11 +730,12 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     grid.sync();
     const int64_t elite = a.st->elite;
     if (one_round) {
-      if (wc < a.P) {
-        if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0);
-        for (int j = lane + 32; j < a.L; j += 32) ga_breed_gene(a, wc * a.L + j, g, cur, elite);
+      if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0);
+      for (int u = lane + 32; u < wgenes; u += 32) {
+        const int64_t t = wgene(u);
+        if (t < genes) ga_breed_gene(a, t, g, cur, elite);
       }
-      __threadfence_block();  // the warp's child, read back by its own next scoring
+      __threadfence_block();  // the warp's children, read back by its own next scoring
       __syncwarp();
     } else {
       if (t0 < genes) ga_breed_apply(a, t0, cur, elite, d0);
@@ -741,7 +753,8 @@ template <int NQ>
 static isq_status ga_launch_coop_nq(const GaArgs& a, int n_gens, cudaStream_t s) {
   int per_sm = 0;
   ISQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ga_coop_kernel<NQ>, kGaRed, 0));
-  const int64_t want = (a.P + kGaRed / 32 - 1) / (kGaRed / 32);  // one circuit per warp
+  constexpr int64_t per_block = (kGaRed / 32) * kFitCPW<NQ>;  // CPW circuits per warp
+  const int64_t want = (a.P + per_block - 1) / per_block;
   int64_t grid = (int64_t)num_sms() * (per_sm > 0 ? 1 : 0);
   if (grid > want) grid = want;
   if (grid < 1) {

@@ -16,6 +16,7 @@
 // immediately once a stop reason is set, so batches of generations are
 // enqueued without host round trips.
 #include "engine_common.cuh"
+#include "fitness_multi.cuh"
 #include "fitness_warp.cuh"
 #include "isq_internal.h"
 #include "qeqea_internal.h"
@@ -680,7 +681,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
   using G = Geo<NQ>;
   constexpr int kWarps = kRedThreads / 32;
   __shared__ double2 Ts[G::D * G::D];
-  __shared__ FastChunk sh[kWarps];
+  __shared__ FitScratch<NQ, double, kSmallNR> sh[kWarps];
   __shared__ uint64_t blk[kWarps][36];
   __shared__ double smax[kRedThreads], ssum[kRedThreads];
   __shared__ int64_t sarg[kRedThreads];
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
       }
     }
     __syncthreads();
-    fitness_rows<NQ>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, a.fitness, kWarps);
+    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, a.fitness, kWarps);
     __syncthreads();
     if (a.P <= 32 && a.n_parts == 1) {
       // one warp: the same pairwise tree as reduce_partial_body (its upper
