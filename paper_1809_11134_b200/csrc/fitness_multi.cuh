@@ -169,18 +169,22 @@ __device__ __forceinline__ unsigned range_mask(int lo, int hi) {
   return (w == 32 ? 0xffffffffu : ((1u << w) - 1u)) << lo;
 }
 
-// Grid-stride (or counter-scheduled, `dyn`) body of the throughput fitness
-// kernels for n <= 4: warp batches of CPW consecutive circuits.
+// Grid-stride (or counter-scheduled, `dyn`) body of the fitness kernels for
+// n <= ISQ_MULTI_MAXNQ: warp batches of `cpw` (<= CPW) consecutive circuits,
+// groups g >= cpw idle.  A circuit's arithmetic does not depend on cpw, so the
+// latency-bound single-block kernels run fewer circuits per warp (more warps,
+// fewer serialised rotation cases per step) with bit-identical results.
 template <int NQ, class R = double>
 __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const uint8_t* __restrict__ codes,
                                                    const double* __restrict__ thetas,
                                                    const double2* __restrict__ Ts, MultiChunk<NQ, R>* sh,
                                                    double* __restrict__ fitness, int warps_per_block,
-                                                   int* bad_code = nullptr, unsigned long long* dyn = nullptr) {
+                                                   int* bad_code = nullptr, unsigned long long* dyn = nullptr,
+                                                   int cpw = MGeo<NQ>::CPW) {
   using MG = MGeo<NQ>;
   using E = FastEval<NQ, R>;  // gate preparation (E::prepare) is shared with n = 5
   using R2 = typename Cplx<R>::T;
-  constexpr int D = MG::D, CPW = MG::CPW, CHUNK = MG::CHUNK;
+  constexpr int D = MG::D, CHUNK = MG::CHUNK;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int g = lane / D, j = lane & (D - 1);
@@ -188,10 +192,10 @@ __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const u
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
   auto grab = [&]() -> int64_t {
     unsigned long long v = 0;
-    if (lane == 0) v = atomicAdd(dyn, (unsigned long long)CPW);
+    if (lane == 0) v = atomicAdd(dyn, (unsigned long long)cpw);
     return (int64_t)__shfl_sync(0xffffffffu, v, 0);
   };
-  int64_t c0 = dyn ? grab() : ((int64_t)blockIdx.x * warps_per_block + wib) * CPW;
+  int64_t c0 = dyn ? grab() : ((int64_t)blockIdx.x * warps_per_block + wib) * cpw;
   // the two gates this lane prepares per chunk: k0 = lane, k1 = lane + 32
   // (circuit k / CHUNK of the batch, step k % CHUNK); loaded one chunk ahead
   auto load = [&](int64_t cb, int nb, int k, int& code, double& th) {
@@ -200,7 +204,7 @@ __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const u
     code = -2;  // neutral (past the end of the circuit or the batch)
     th = 0.0;
     const int64_t c = cb + gg;
-    if (q < nq && c < count) {
+    if (q < nq && gg < cpw && c < count) {
       const int64_t at = c * (int64_t)L + (L - 1 - nb - q);  // adjoint order: last position first
       code = codes[at];
       th = -thetas[at];
@@ -214,7 +218,7 @@ __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const u
   load(c0, 0, lane, code0, th0);
   load(c0, 0, lane + 32, code1, th1);
   while (c0 < count) {
-    const int64_t cn = dyn ? grab() : c0 + nwarps * CPW;
+    const int64_t cn = dyn ? grab() : c0 + nwarps * cpw;
     MultiEval<NQ, R> ev;
     ev.begin(Ts, j);
     bool bad0 = false, bad1 = false;
@@ -250,7 +254,7 @@ __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const u
     const unsigned badm0 = __ballot_sync(0xffffffffu, bad0), badm1 = __ballot_sync(0xffffffffu, bad1);
     const double f = ev.finish(j);
     const int64_t c = c0 + g;
-    if (j == 0 && c < count) {
+    if (j == 0 && g < cpw && c < count) {
       const bool cbad = ((badm0 & own0) | (badm1 & own1)) != 0;
       fitness[c] = cbad ? __longlong_as_double(0x7ff8000000000000LL) : f;
       if (cbad && bad_code) atomicOr(bad_code, 1);
@@ -271,14 +275,23 @@ constexpr int kSmallNR = 2;  // single-block / cooperative kernels (8 warps per 
 template <int NQ>
 constexpr int kFitCPW = kFitMulti<NQ> ? MGeo<NQ>::CPW : 1;  // circuits per warp
 
+// Circuits per warp for a latency-bound launch of `warps` warps over P
+// circuits: as few as fill the warps.
+template <int NQ>
+__device__ __forceinline__ int small_cpw(int64_t P, int64_t warps) {
+  const int64_t c = (P + warps - 1) / warps;
+  return (int)(c < 1 ? 1 : (c > kFitCPW<NQ> ? kFitCPW<NQ> : c));
+}
+
 template <int NQ, class R = double, int NR = kFitNR>
 __device__ __forceinline__ void fitness_rows_fast(int64_t count, int L, const uint8_t* __restrict__ codes,
                                                   const double* __restrict__ thetas,
                                                   const double2* __restrict__ Ts, FitScratch<NQ, R, NR>* sh,
                                                   double* __restrict__ fitness, int warps_per_block,
-                                                  int* bad_code = nullptr, unsigned long long* dyn = nullptr) {
+                                                  int* bad_code = nullptr, unsigned long long* dyn = nullptr,
+                                                  int cpw = kFitCPW<NQ>) {
   if constexpr (kFitMulti<NQ>)
-    fitness_rows_multi<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, warps_per_block, bad_code, dyn);
+    fitness_rows_multi<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, warps_per_block, bad_code, dyn, cpw);
   else
     fitness_rows<NQ, R, NR>(count, L, codes, thetas, Ts, sh, fitness, warps_per_block, bad_code, dyn);
 }

@@ -51,8 +51,9 @@ struct Cplx<float> {
 
 // Per-warp shared scratch for one 32-gate chunk (R: arithmetic type of the
 // state, double or the fp32 variant's float).
-// Rotations whose flush factors one phase pass stores before the state pass
-// applies them (FastEval::chunk).
+// kFitNR / NR: unused by this evaluator (interleaved phase and state
+// updates measured faster than a separate phase pass at n = 4, 5), kept so
+// callers can size the scratch per kernel.
 #ifndef ISQ_FIT_NR
 #define ISQ_FIT_NR 8
 #endif
@@ -61,12 +62,10 @@ constexpr int kFitNR = ISQ_FIT_NR;
 template <class R, int NR = kFitNR>
 struct FastChunkT {
   using R2 = typename Cplx<R>::T;
-  static constexpr int kNR = NR;
   R2 cs2[32][2];       // diag: {unused, e^{-i th/2}}; rotation: {(C = cos a, 0), (p, q)}
   uint32_t rpar[32];   // diag: bit r = parity of row r under the gate's wire mask; 0 for rotations
   int info[32];        // bits 0..1: type (0 diag, 1 Rx, 2 Ry); bits 8..15: row bit (n = 5)
-  R2 rfac[NR][16];     // flush factors of the batch's rotations: n = 5 the 16 rows with the
-                       // rotation's bit set (row with the bit removed), n < 5 every row
+  R2 fac[32];          // flush factors, indexed by physical row
   double nth[32];      // next chunk's angles / codes, staged by cp.async (no registers held)
   uint32_t ncode[8];
 };
@@ -259,19 +258,7 @@ struct FastEval {
     }
   }
 
-  // Flush factor of physical row r1 (bit B set) in a rotation's rfac row:
-  // n = 5 keeps only the rows with the bit set, indexed by the row with bit B
-  // removed; n < 5 keeps every row.
-  template <int B>
-  static __device__ __forceinline__ int fac_index(int r1) {
-    if constexpr (NQ == 5)
-      return ((r1 >> (B + 1)) << B) | (r1 & ((1 << B) - 1));
-    else
-      return r1;
-  }
-
-  // Multiply the register rows with bit B set by their flush factor (n < 5,
-  // lane-held row bit: every row of the upper lanes; the lower lanes' factors are 1).
+  // Multiply the register rows with bit B set by fac[row] (flush of pending deltas).
   template <int B>
   __device__ __forceinline__ void flush_bit(const R2* fac, int lane) {
     const int h = (lane >> NQ) & (G::LPC - 1);
@@ -296,7 +283,7 @@ struct FastEval {
       for (int r = 0; r < G::E; ++r) {
         if (r & m) continue;
         const int r1 = r | m;
-        const R2 f = fac[fac_index<B>(h * G::E + r1)];
+        const R2 f = fac[h * G::E + r1];
         st.cmul(r1, f.x, f.y);
         st.re[r] = fma(p, st.im[r1], st.re[r]);
         st.im[r1] = fma(q, st.re[r], st.im[r1]);
@@ -360,23 +347,10 @@ struct FastEval {
     }
   }
 
-  // Type | row bit << 8 of rotation qr (bit planes at n < 5, shared memory at n = 5).
-  __device__ __forceinline__ int rot_info(int qr, const Chunk& sm, unsigned ryb, unsigned bp0, unsigned bp1,
-                                          unsigned bp2) const {
-    if constexpr (NQ < 5)
-      return (((bp0 >> qr) & 1) << 8) | (((bp1 >> qr) & 1) << 9) | (((bp2 >> qr) & 1) << 10) |
-             (((ryb >> qr) & 1) ? GT_RY : GT_RX);
-    else
-      return sm.info[qr];
-  }
-
   // One chunk: lane q < nq supplies (code_q, theta_q) for position base+q.
-  // The pending row phases do not depend on the state, so each batch of up
-  // to kFitNR rotations runs in two passes: a phase pass walks the gates
-  // (diagonal runs between rotations touch only the pending phase,
-  // diag_run) and stores every rotation's flush factors, then a state pass
-  // applies the batch's flushes and liftings back to back, with no
-  // shuffle / shared-memory round trip between two rotations.
+  // The rotation positions are found with one ballot; the diagonal runs
+  // between them touch only the pending phase (diag_run), the rotations
+  // flush the non-commuting part of it and rotate the register state.
   // Returns true (warp-uniform) when a lane's code is not a valid gate code.
   __device__ __forceinline__ bool chunk(int code, double theta, int nq, Chunk& sm, int lane) {
     int info = GT_DIAG;  // lanes past the end: neutral diagonal, no parity
@@ -385,14 +359,15 @@ struct FastEval {
     if (lane < nq) prepare(code, theta, info, rpar, e0, e1);
     const bool bad = __any_sync(0xffffffffu, lane < nq && (code < 0 || code >= G::NCODES));
     // n <= 4: each rotation's type and row bit as warp-uniform bit planes (no
-    // shared-memory round trip: -3 % at n = 3, 4); n = 5 reads them back from
-    // shared memory (the bit planes cost it spills: +1.5 %)
+    // shared-memory round trip on the rotation's critical path: -3 % at n = 3,
+    // 4); n = 5 reads them back from shared memory (the bit planes cost it
+    // spills: +1.5 %)
     constexpr bool kPlanes = NQ < 5;
     if constexpr (!kPlanes) sm.info[lane] = info;
     sm.rpar[lane] = rpar;
     sm.cs2[lane][0] = e0;
     sm.cs2[lane][1] = e1;
-    unsigned todo = __ballot_sync(0xffffffffu, info != GT_DIAG);
+    unsigned rot = __ballot_sync(0xffffffffu, info != GT_DIAG);
     unsigned ryb = 0, bp0 = 0, bp1 = 0, bp2 = 0;
     if constexpr (kPlanes) {
       ryb = __ballot_sync(0xffffffffu, (info & 3) == GT_RY);
@@ -404,50 +379,44 @@ struct FastEval {
     const int row = lane;  // physical row whose phase this lane carries
     const int sh = 31 - row;
     int q = 0;
-    while (todo) {
-      // phase pass over the next kFitNR rotations
-      unsigned t = todo;
-      int k = 0;
-      while (t && k < NR) {
-        const int qr = __ffs(t) - 1;
-        diag_run(q, qr, sm, sh);
-        t &= t - 1;
-        q = qr + 1;
-        const int inf = rot_info(qr, sm, ryb, bp0, bp1, bp2);
-        const int b = inf >> 8;
-        const int m = 1 << b;
-        const bool ry = (inf & 3) == GT_RY;
-        const bool hib = (row & m) != 0;
-        // flush factor of the rows with bit b set: w_r * conj(w_{r^m}), times -i
-        // for Ry (S^dagger); those rows then carry their partner's phase (times
-        // +i for Ry: S), which commutes with the Rx.  (The partner's phase
-        // comes over times i for Ry: o' = i o, so that w conj(o') = -i w conj(o)
-        // and the new phase is o'.)  n < 5: rows with the bit clear store 1,
-        // read by the lane-bit flush of the upper lanes only.
-        const R orr = __shfl_xor_sync(0xffffffffu, ry ? -wi : wr, m);
-        const R ori = __shfl_xor_sync(0xffffffffu, ry ? wr : wi, m);
-        const R fr = fma(wr, orr, wi * ori), fi = fma(wi, orr, -wr * ori);
-        if constexpr (NQ == 5) {
-          if (hib) sm.rfac[k][((row >> (b + 1)) << b) | (row & (m - 1))] = Cplx<R>::make(fr, fi);
-        } else {
-          if (row < G::D) sm.rfac[k][row] = hib ? Cplx<R>::make(fr, fi) : Cplx<R>::make(R(1), R(0));
-        }
-        if (hib) {
-          wr = orr;
-          wi = ori;
-        }
-        ++k;
+    while (rot) {
+      const int qr = __ffs(rot) - 1;
+      diag_run(q, qr, sm, sh);
+      rot &= rot - 1;
+      q = qr + 1;
+      int inf;
+      if constexpr (kPlanes)
+        inf = (((bp0 >> qr) & 1) << 8) | (((bp1 >> qr) & 1) << 9) | (((bp2 >> qr) & 1) << 10) |
+              (((ryb >> qr) & 1) ? GT_RY : GT_RX);
+      else
+        inf = sm.info[qr];
+      const int b = inf >> 8;
+      const int m = 1 << b;
+      const bool ry = (inf & 3) == GT_RY;
+      const bool hib = (row & m) != 0;
+      // flush factor of the rows with bit b set: w_r * conj(w_{r^m}), times -i
+      // for Ry (S^dagger); those rows then carry their partner's phase (times
+      // +i for Ry: S), which commutes with the Rx.  Rows with the bit clear
+      // keep their phase; their factor is only read for lane-bit rotations
+      // (n < 5), where it must be 1.
+      // (the partner's phase comes over times i for Ry: o' = i o, so that
+      // w conj(o') = -i w conj(o) and the new phase is o')
+      const R orr = __shfl_xor_sync(0xffffffffu, ry ? -wi : wr, m);
+      const R ori = __shfl_xor_sync(0xffffffffu, ry ? wr : wi, m);
+      R fr = fma(wr, orr, wi * ori), fi = fma(wi, orr, -wr * ori);
+      if constexpr (G::LB > 0) {
+        fr = hib ? fr : R(1);
+        fi = hib ? fi : R(0);
       }
+      sm.fac[lane] = Cplx<R>::make(fr, fi);
+      if (hib) {
+        wr = orr;
+        wi = ori;
+      }
+      const R2 pq = sm.cs2[qr][1];
+      const R C = sm.cs2[qr][0].x;
       __syncwarp();
-      // state pass: the batch's flushes + liftings back to back
-      for (int i = 0; i < k; ++i) {
-        const int qr = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int b = rot_info(qr, sm, ryb, bp0, bp1, bp2) >> 8;
-        const R2 pq = sm.cs2[qr][1];
-        const R C = sm.cs2[qr][0].x;
-        flush_rotate(b, sm.rfac[i], pq.x, pq.y, C, lane);
-      }
+      flush_rotate(b, sm.fac, pq.x, pq.y, C, lane);
       __syncwarp();
     }
     diag_run(q, nq, sm, sh);

@@ -394,7 +394,8 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_small_kernel(GaArgs a, int n_gen
     if (a.st->stop) return;  // uniform: written by thread 0 before the barrier
     const uint64_t g = a.st->generation;
     const int cur = ga_cur(a);
-    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
+    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps,
+                                            nullptr, nullptr, small_cpw<NQ>(a.P, kWarps));
     __syncthreads();
     for (int part = 0; part < a.n_parts; ++part) {
       ga_reduce_partial_body(a, part, smax, ssum, sarg);
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
   // children, so what it scores next is its own writes and breeding needs no
   // grid barrier after it.  Otherwise genes are bred grid-stride behind a
   // third barrier.
-  constexpr int CPW = kFitCPW<NQ>;
+  const int CPW = small_cpw<NQ>(a.P, (int64_t)gridDim.x * kWarps);  // uniform over the grid
   const bool one_round = a.P <= (int64_t)gridDim.x * kWarps * CPW;
   const int lane = threadIdx.x & 31;
   const int64_t wc = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);  // this warp's batch
@@ -672,7 +673,8 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     for (int it = 0; it < n_gens; ++it) {
       const int cur = (int)(g & 1);
       double* fit = (g & 1) ? a.fitness_alt : a.fitness;
-      fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, fit, kWarps);
+      fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, fit, kWarps,
+                                              nullptr, nullptr, CPW);
       grid.sync();
       const int64_t t0 = wgene(jl);
       GeneDraw d0;
@@ -702,7 +704,8 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     if (a.st->stop) return;  // uniform across the grid: written before the last grid barrier
     const uint64_t g = a.st->generation;
     const int cur = ga_cur(a);
-    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps);
+    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps,
+                                            nullptr, nullptr, CPW);
     grid.sync();
     // this thread's first gene: its draws while block 0 reduces and selects
     const int64_t t0 = one_round ? wgene(lane) : (int64_t)blockIdx.x * kGaRed + threadIdx.x;
@@ -753,7 +756,7 @@ template <int NQ>
 static isq_status ga_launch_coop_nq(const GaArgs& a, int n_gens, cudaStream_t s) {
   int per_sm = 0;
   ISQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ga_coop_kernel<NQ>, kGaRed, 0));
-  constexpr int64_t per_block = (kGaRed / 32) * kFitCPW<NQ>;  // CPW circuits per warp
+  constexpr int64_t per_block = kGaRed / 32;  // one circuit per warp if the grid allows (small_cpw)
   const int64_t want = (a.P + per_block - 1) / per_block;
   int64_t grid = (int64_t)num_sms() * (per_sm > 0 ? 1 : 0);
   if (grid > want) grid = want;
