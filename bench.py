@@ -29,6 +29,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import math
 import os
 import subprocess
 import sys
@@ -40,7 +41,35 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "circuit fitness evals/sec (whole box) at 3–5 qubits; generations/sec"
+# BASELINE.json configs: C5 (the headline, default) and C4
+CONFIGS = {
+    "c5": dict(n=5, L=64, P=1 << 20, target="haar",
+               workload="C5: QEQEA generation, n=5 qubits, depth L=64, population 2^20, "
+                        "Haar-random 32x32 target; bank 1.0e9 slots (36 GB) resident in HBM",
+               l2="inputs larger than L2 (36 GB bank vs 126 MB)"),
+    "c4": dict(n=4, L=32, P=1 << 16, target="CCCNOT",
+               workload="C4: QEQEA generation on C^3NOT, n=4 qubits, depth L=32, population 2^16; "
+                        "bank 2.1e7 slots (738 MB) resident in HBM",
+               l2="bank larger than L2 (738 MB vs 126 MB)"),
+}
 N, L, P = 5, 64, 1 << 20
+CONFIG = "c5"
+
+
+def target_of(name: str, n: int):
+    if name == "haar":
+        from paper_1809_11134_b200.synthetic import haar_target
+
+        return haar_target(n)
+    from paper_1809_11134_b200.fitness import target_matrix
+
+    return target_matrix(name, n).matrix
+
+
+def kernel_name(n: int, precision: str = "fp64") -> str:
+    from paper_1809_11134_b200 import _lib  # noqa: F401  (instantiation names of include/isq.h kernels)
+
+    return f"fitness_fast_kernel<{n}, *, {'double' if precision == 'fp64' else 'float'}>"
 
 
 def canonical_flops(n: int, L: int) -> int:
@@ -160,13 +189,26 @@ def emit(obj):
     print(json.dumps(obj), flush=True)
 
 
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(steps: int, warmup: int, per_worker: int):
-    """The reference algorithm's CPU path on all host cores (oracle port)."""
+    """The reference algorithm's CPU path on all host cores (oracle port).
+    The worker pool is spawned and warmed (imports, lru caches) before any
+    timed step."""
     from oracle.cpu_baseline import CpuPool
-    from paper_1809_11134_b200.synthetic import haar_target, qeqea_like_circuits
+    from paper_1809_11134_b200.synthetic import qeqea_like_circuits
 
     pool = CpuPool()
-    T = haar_target(N)
+    pool.warm(N, L)
+    T = target_of(CONFIGS[CONFIG]["target"], N)
     count = per_worker * pool.workers
     times, evals = [], 0
     for i in range(warmup + steps):
@@ -181,10 +223,11 @@ def cpu_reference_sample(steps: int, warmup: int, per_worker: int):
         "value": evals / total,
         "unit": "evals/s",
         "cores": pool.workers,
+        "cpu_model": cpu_model(),
         "kind": "port",
-        "sample": (f"{count} C5-shaped circuits (n=5, L=64, QEQEA gate mix, Haar target) per step, "
-                   f"oracle restatement of evaluate_circuit (dense kron matmul per gate), "
-                   f"ProcessPool x{pool.workers}, OPENBLAS_NUM_THREADS=1"),
+        "sample": (f"{count} {CONFIG.upper()}-shaped circuits (n={N}, L={L}, QEQEA gate mix, "
+                   f"{CONFIGS[CONFIG]['target']} target) per step, oracle restatement of evaluate_circuit "
+                   f"(dense kron matmul per gate), warmed ProcessPool x{pool.workers}, OPENBLAS_NUM_THREADS=1"),
         "ms_per_step": 1000.0 * total / max(1, len(times)),
     }
 
@@ -199,10 +242,166 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C5 fitness evals (bounded sample per step)", "n": N, "L": L, "P": P},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "config": {"workload": f"{CONFIG.upper()} fitness evals (bounded sample per step)", "n": N, "L": L,
+                   "P": P},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
+
+
+def _ncu_value(text: str) -> float:
+    """'0.605691 Gbyte' / '48.2 %' -> float in base units (bytes, percent)."""
+    num, _, unit = str(text).partition(" ")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit.strip(), 1)
+    return float(num.replace(",", "")) * scale
+
+
+def profile_evidence(kernel_prefix: str):
+    """(DRAM bytes per launch, FP64 pipe fraction, source) of `kernel_prefix`
+    from the committed `ncu --set full` captures (profiles/r*_ncu_full.json,
+    newest round first); Nones when no capture of this kernel instantiation
+    exists.  Not measured by this run."""
+    for f in sorted((ROOT / "profiles").glob("r*_ncu_full.json"), reverse=True):
+        try:
+            rows = json.loads(f.read_text())
+        except (OSError, ValueError):
+            continue
+        for r in rows:
+            if r.get("kernel", "").startswith(kernel_prefix) and "dram__bytes_read.sum" in r:
+                traffic = _ncu_value(r["dram__bytes_read.sum"]) + _ncu_value(r.get("dram__bytes_write.sum", "0"))
+                pipe = r.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+                return (traffic, _ncu_value(pipe) / 100 if pipe else None,
+                        f"{f.relative_to(ROOT)}: {r['kernel'].split('(')[0]}")
+    return None, None, None
+
+
+def time_generations(ops, comm, steps: int, warmup: int, stream, dist=None, clocks=None):
+    """Warm-up, then `steps` generations bracketed by CUDA events on the
+    handle's stream (barrier + synchronize on both sides); per-generation
+    phase events (before prepare, before / after score, after finish)."""
+    import torch
+
+    ops.begin_batch()
+    for _ in range(warmup):
+        ops.generation(comm)
+    stream.synchronize()
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clocks is not None:
+        clocks.start()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start.record(stream)
+    for i in range(steps):
+        ops.generation(comm, marks=ev[i])
+    end.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    if clocks is not None:
+        clocks.clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    phases = [[e[k].elapsed_time(e[k + 1]) for e in ev] for k in range(3)]
+    return ms, [sum(p) / len(p) for p in phases]
+
+
+def fitness_peak(lib, _lib, local: int, fp64: bool = True) -> float:
+    v = ctypes.c_double()
+    _lib.check(lib.isq_fma_peak(1 if fp64 else 0, local, ctypes.cast(ctypes.pointer(v), ctypes.c_void_p)))
+    return v.value / 1e12
+
+
+def side_c4(args, local: int, fp64_peak: float, stream):
+    """BASELINE config 4 (n=4, L=32, P=2^16, C^3NOT): full generations, same
+    timing as the headline line, with the fitness kernel's roofline."""
+    import torch
+
+    from paper_1809_11134_b200.distributed import DeviceQeqeaOps
+    from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
+    from paper_1809_11134_b200.fitness import target_matrix
+
+    c = CONFIGS["c4"]
+    steps, warmup = max(args.steps, 20), max(args.warmup, 3)
+    cfg = PopulationConfig(number_of_wires=c["n"], size_of_individual=c["L"], size_of_population=c["P"],
+                           max_generations=10_000_000, target_fitness=1.0)
+    eng = QeqeaEngine(cfg, target_matrix("CCCNOT"), seed=2024, device=local, max_batch=steps + warmup + 1)
+    with torch.cuda.stream(stream):
+        ops = DeviceQeqeaOps(eng)
+        ms, (prep, fit, fin) = time_generations(ops, None, steps, warmup, stream)
+    eng.close()
+    achieved = canonical_flops(c["n"], c["L"]) * c["P"] / (fit * 1e-3) / 1e12
+    return {"workload": c["workload"], "steps": steps, "warmup": warmup,
+            "value": c["P"] * steps / (ms * 1e-3), "unit": "evals/s", "gens_per_s": steps / (ms * 1e-3),
+            "ms_per_step": ms / steps,
+            "phase_ms": {"prepare": prep, "score (fitness kernel)": fit, "finish": fin},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": achieved / fp64_peak, "kernel": kernel_name(c["n"]),
+                         "work": "canonical F(4,32) = 51,200 flop/eval x 65,536 circuits per launch"},
+            "baseline_md_target": "BASELINE.md section 2: >= 3.6e8 evals/s (fitness at 50% of FP64 peak)"}
+
+
+def side_fitness_sweep(lib, _lib, fp64_peak: float, stream):
+    """The metric's "3-5 qubits": explicit-gate fitness (isq_fitness_batch_device_ex)
+    on device-resident QEQEA- and GA-mix circuits, best of 3 trials of 10
+    launches each, canonical roofline fraction."""
+    import torch
+
+    out = {}
+    dev = torch.device("cuda", torch.cuda.current_device())
+    for n, L, count in [(3, 16, 1 << 20), (4, 32, 1 << 18), (5, 64, 1 << 18)]:
+        nc, K = 3 * n + n * (n - 1) // 2, n + n * (n - 1) // 2
+        g = torch.Generator(device=dev).manual_seed(n)
+        for mix in ("qeqea", "ga"):
+            if mix == "ga":  # uniform over the gate choices (ga.py:47-59)
+                codes = torch.randint(0, nc, (count, L), device=dev, dtype=torch.uint8, generator=g)
+            else:  # slot kind uniform over K (engine.py:180), measured axis uniform
+                kinds = torch.randint(0, K, (count, L), device=dev, generator=g)
+                axes = torch.randint(0, 3, (count, L), device=dev, generator=g)
+                codes = torch.where(kinds < n, 3 * kinds + axes, 3 * n + (kinds - n)).to(torch.uint8)
+            thetas = torch.rand((count, L), device=dev, dtype=torch.float64, generator=g) * 2 * math.pi
+            T = torch.eye(2 ** n, dtype=torch.complex128, device=dev)
+            outv = torch.empty(count, dtype=torch.float64, device=dev)
+            a = (n, L, count, codes.data_ptr(), thetas.data_ptr(), T.data_ptr(), outv.data_ptr(), 0,
+                 stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    _lib.check(lib.isq_fitness_batch_device_ex(*a))
+                best = None
+                for _ in range(3):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for _ in range(10):
+                        lib.isq_fitness_batch_device_ex(*a)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    t = e0.elapsed_time(e1) / 10
+                    best = t if best is None else min(best, t)
+            ev = count / (best * 1e-3)
+            tf = ev * canonical_flops(n, L) / 1e12
+            out[f"n{n}_L{L}_{mix}"] = {"circuits": count, "ms": best, "evals_per_s": ev, "canonical_tflops": tf,
+                                       "frac_fp64_peak": tf / fp64_peak}
+    return out
+
+
+def side_tiny(local: int):
+    """C1-C3 are latency bound (5 / 50 candidates): generations/s through the
+    engines' steps() (host wall clock, records read back per call)."""
+    from paper_1809_11134_b200 import GaConfig, GaEngine, PopulationConfig, QeqeaEngine, target_matrix
+
+    def gps(eng, n):
+        eng.steps(100)
+        t0 = time.perf_counter()
+        r = eng.steps(n)
+        return len(r) / (time.perf_counter() - t0)
+
+    t, f = target_matrix("Toffoli"), target_matrix("Fredkin")
+    big = dict(max_generations=10 ** 7, target_fitness=1.0)
+    return {"unit": "generations/s",
+            "C1 QEQEA Toffoli P=5 L=16": gps(QeqeaEngine(PopulationConfig(3, 16, 5, **big), t, 1, device=local), 4000),
+            "C2 GA Toffoli P=50 L=16": gps(GaEngine(GaConfig(3, 16, 50, **big), t, 1, device=local), 4000),
+            "C3 QEQEA Fredkin P=5 L=16 nMeas=3": gps(QeqeaEngine(PopulationConfig(3, 16, 5, n_meas=3, **big), f, 1,
+                                                                 device=local), 4000)}
 
 
 def run_ours(args):
@@ -220,6 +419,7 @@ def run_ours(args):
         sys.exit(2)
     torch.cuda.set_device(local)
     red_dev = "cpu" if share else f"cuda:{local}"
+    dist = None
     if world > 1:
         import torch.distributed as dist
 
@@ -227,23 +427,19 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    from paper_1809_11134_b200.synthetic import haar_target
     from paper_1809_11134_b200 import _lib
+    from paper_1809_11134_b200.distributed import Comm, DeviceQeqeaOps
     from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
     from paper_1809_11134_b200.fitness import TargetSpec
 
     lib = _lib.load()
-    peak = ctypes.c_double()
-    _lib.check(lib.isq_fma_peak(1, local, ctypes.cast(ctypes.pointer(peak), ctypes.c_void_p)))
-    fp64_peak = peak.value / 1e12
-
-    T = haar_target(N)
+    fp64_peak = fitness_peak(lib, _lib, local)
+    conf = CONFIGS[CONFIG]
+    T = target_of(conf["target"], N)
     cfg = PopulationConfig(number_of_wires=N, size_of_individual=L, size_of_population=P,
                            max_generations=10_000_000, target_fitness=1.0)
-    eng = QeqeaEngine(cfg, TargetSpec("haar32", N, T), seed=2024, device=local, rank=rank, world=world,
+    eng = QeqeaEngine(cfg, TargetSpec(conf["target"], N, T), seed=2024, device=local, rank=rank, world=world,
                       max_batch=max(args.steps + args.warmup, 1) + 1)
-    from paper_1809_11134_b200.distributed import Comm, DeviceQeqeaOps
-
     stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         ops = DeviceQeqeaOps(eng, args.transport)  # binds the handle to `stream`
@@ -264,29 +460,9 @@ def run_ours(args):
                 _lib.check(lib.isq_qeqea_set_peers(eng._handle(), None))
                 ops.transport = "nccl"
                 transport = f"nccl (p2p unavailable: {err or 'on another rank'})"
-        ops.begin_batch()
-        for _ in range(args.warmup):
-            ops.generation(comm)
-        stream.synchronize()
-        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(args.steps)]
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks = ClockSampler(local)
-        clocks.start()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        start.record(stream)
-        for i in range(args.steps):
-            ops.generation(comm, marks=ev[i])
-        end.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        clk = clocks.stop()
-    ms = start.elapsed_time(end)
-    prep_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    eval_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    fin_ms = [e[2].elapsed_time(e[3]) for e in ev]
+        ms, (prep_ms, eval_ms, fin_ms) = time_generations(ops, comm, args.steps, args.warmup, stream, dist, clocks)
+        clk = clocks.clk
     if world > 1:
         t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -304,50 +480,38 @@ def run_ours(args):
         ranks_agree = bool(torch.equal(lo, hi))
 
     evals_per_s = P * args.steps / (ms * 1e-3)
-    avg_eval_s = sum(eval_ms) / len(eval_ms) * 1e-3
     shard_circuits = min(shard, P - rank * shard)
-    achieved = canonical_flops(N, L) * shard_circuits / avg_eval_s / 1e12
-    traffic = None
-    tf = ROOT / "profiles" / "traffic_eval_c5.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
-    # executed FP64 pipe utilisation of the same kernel from the committed
-    # `ncu --set full` capture (profiles/, not measured by this run)
-    pipe_ncu = None
-    nf = ROOT / "profiles" / "r01_c5_ncu_full.json"
-    if nf.exists():
-        for k in json.loads(nf.read_text()):
-            if "fitness_fast_kernel<5" in k.get("kernel", ""):
-                v = k.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "")
-                pipe_ncu = float(v.split()[0]) / 100 if v else None
+    achieved = canonical_flops(N, L) * shard_circuits / (eval_ms * 1e-3) / 1e12
+    kname = kernel_name(N)
+    kprefix = f"fitness_fast_kernel<{N},"
+    traffic, pipe, prof_src = profile_evidence(f"void {kprefix}")
 
     out = {
         "metric": METRIC, "value": evals_per_s, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "C5: QEQEA generation, n=5 qubits, depth L=64, population 2^20, "
-                               "Haar-random 32x32 target; bank 1.0e9 slots (36 GB) resident in HBM",
-                   "n": N, "L": L, "P": P, "global_batch": P,
+        "config": {"workload": conf["workload"], "n": N, "L": L, "P": P, "global_batch": P,
                    "parallelism": f"dp{world} (circuit shards x position-owned bank shards)"
                                   + (f", {transport} transport" if world > 1 else ""),
-                   "l2": "inputs larger than L2 (36 GB bank vs 126 MB)"},
+                   "l2": conf["l2"]},
         "gens_per_s": args.steps / (ms * 1e-3),
-        "phase_ms": {"prepare (sample + route + lazy mutation + measure; world > 1: + 2 all-to-alls)":
-                         sum(prep_ms) / len(prep_ms),
-                     "score (fitness kernel)": sum(eval_ms) / len(eval_ms),
-                     "finish (world > 1: all-gathers; reduce + commit + table)": sum(fin_ms) / len(fin_ms)},
+        "phase_ms": {"prepare (sample + route + lazy mutation + measure; world > 1: + 2 all-to-alls)": prep_ms,
+                     "score (fitness kernel)": eval_ms,
+                     "finish (world > 1: all-gathers; reduce + commit + table)": fin_ms},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp64_peak, "traffic": traffic,
-                     "fp64_pipe_active_ncu": pipe_ncu,
-                     "kernel": "fitness_fast_kernel<5> (score phase, one launch per generation)",
+                     "frac": achieved / fp64_peak, "traffic": traffic, "fp64_pipe_active_ncu": pipe,
+                     "profile_source": prof_src,
+                     "kernel": f"{kname} (score phase, one launch per generation)",
                      "peak_source": "FP64 CUDA-core FMA peak measured live by isq_fma_peak "
                                     "(MEASURED_PEAKS.json carries no FP64 figure)",
-                     "work": "canonical F(n,L) = (6L+8) 4^n flop/eval (SURVEY.md §8d) x circuits per launch",
-                     "note": ("frac > 1 is possible: diagonal gates (Rz, ZZ; 78% of QEQEA gates) cost O(2^n) "
-                              "phase updates here, not the canonical 6*4^n; the executed FP64 pipe "
-                              "utilisation is fp64_pipe_active_ncu (ncu sm__pipe_fp64_cycles_active of the "
-                              "committed capture, profiles/r01_c5_ncu_full.json; DESIGN.md §6)")},
+                     "work": f"canonical F(n,L) = (6L+8) 4^n = {canonical_flops(N, L)} flop/eval (SURVEY.md §8d) "
+                             f"x {shard_circuits} circuits per launch",
+                     "note": ("frac > 1 is possible: diagonal gates (Rz, ZZ) cost O(2^n) phase updates here, not "
+                              "the canonical 6*4^n; fp64_pipe_active_ncu is the executed FP64 pipe utilisation "
+                              "and traffic the DRAM bytes per launch of the same kernel instantiation from the "
+                              "committed ncu capture named in profile_source (not measured by this run; "
+                              "DESIGN.md §6)")},
         "clocks": clk,
         **({"shared_gpu_functional_check": True} if share else {}),
         # per generation: sample, values, fitness, 2 reductions, commit, advance;
@@ -360,16 +524,17 @@ def run_ours(args):
     # e2e: the same metric through the C-ABI with host buffers (isq_fitness_batch:
     # pinned host codes/angles -> device, fitness -> host inside the timed
     # region), every rank on its shard of the circuits, max over ranks
+    hc = ht = hf = Tc = None
+    n_mine = shard_circuits
     if not args.skip_e2e:
-        n_mine = shard_circuits
         if world == 1:
-            _, codes, thetas = eng.sample(0, P)  # this generation's C5 circuits
-            src = "this generation's C5 circuits"
+            _, codes, thetas = eng.sample(0, P)  # this generation's circuits
+            src = f"this generation's {CONFIG.upper()} circuits"
         else:
             from paper_1809_11134_b200.synthetic import qeqea_like_circuits
 
             codes, thetas = qeqea_like_circuits(N, L, n_mine, seed=77 + rank)
-            src = "QEQEA-mix C5-shaped circuits, P/N per rank"
+            src = f"QEQEA-mix {CONFIG.upper()}-shaped circuits, P/N per rank"
         hc = torch.empty((n_mine, L), dtype=torch.uint8, pin_memory=True).numpy()
         ht = torch.empty((n_mine, L), dtype=torch.float64, pin_memory=True).numpy()
         hf = torch.empty(n_mine, dtype=torch.float64, pin_memory=True).numpy()
@@ -403,14 +568,16 @@ def run_ours(args):
             from oracle.cpu_baseline import CpuPool
 
             pool = CpuPool()
+            pool.warm(N, L)
             m = min(n_mine, args.cpu_per_worker * pool.workers)
             cpu_fit, wall = pool.evaluate(N, codes[:m], thetas[:m], T)
             pool.close()
             rel = np.abs(cpu_fit - hf[:m]) / np.maximum(np.abs(cpu_fit), 1e-300)
             out["cpu_baseline"] = {
-                "value": m / wall, "unit": "evals/s", "cores": pool.workers, "kind": "port",
+                "value": m / wall, "unit": "evals/s", "cores": pool.workers, "cpu_model": cpu_model(),
+                "kind": "port",
                 "sample": (f"first {m} circuits of the e2e batch ({src}), oracle restatement of "
-                           f"evaluate_circuit (dense kron matmul per gate), ProcessPool x{pool.workers}, "
+                           f"evaluate_circuit (dense kron matmul per gate), warmed ProcessPool x{pool.workers}, "
                            f"OPENBLAS_NUM_THREADS=1"),
                 "parity_max_rel_err_vs_gpu": float(rel.max()),
             }
@@ -429,41 +596,34 @@ def run_ours(args):
                            "path": "QeqeaEngine.step() through the C ABI (isq_qeqea_step), host wall clock"}
     eng.close()
     # the fp32 variant of the fitness kernel (include/isq.h ISQ_PRECISION_FP32):
-    # a full C5 generation with fp32 fitness, and its error on the e2e circuits
+    # a full generation with fp32 fitness, and its error on the e2e circuits
     if world == 1 and not args.skip_fp32:
-        fe = QeqeaEngine(cfg, TargetSpec("haar32", N, T), seed=2024, device=local, precision="fp32",
+        fe = QeqeaEngine(cfg, TargetSpec(conf["target"], N, T), seed=2024, device=local, precision="fp32",
                          max_batch=max(args.steps + args.warmup, 1) + 1)
         with torch.cuda.stream(stream):
             fops = DeviceQeqeaOps(fe)
-            fops.begin_batch()
-            for _ in range(args.warmup):
-                fops.generation(None)
-            fev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(args.steps)]
-            torch.cuda.synchronize()
-            start.record(stream)
-            for i in range(args.steps):
-                fops.generation(None, marks=fev[i])
-            end.record(stream)
-            torch.cuda.synchronize()
-        fms = start.elapsed_time(end)
-        fit_ms = sum(e[1].elapsed_time(e[2]) for e in fev) / args.steps
-        p32 = ctypes.c_double()
-        _lib.check(lib.isq_fma_peak(0, local, ctypes.cast(ctypes.pointer(p32), ctypes.c_void_p)))
+            fms, (_, fit_ms, _) = time_generations(fops, None, args.steps, args.warmup, stream)
+        p32 = fitness_peak(lib, _lib, local, fp64=False)
         a32 = canonical_flops(N, L) * P / (fit_ms * 1e-3) / 1e12
         var = {"value": P * args.steps / (fms * 1e-3), "unit": "evals/s", "ms_per_step": fms / args.steps,
                "fitness_kernel_ms": fit_ms,
-               "roofline": {"bound": "fp32", "achieved": a32, "peak": p32.value / 1e12, "unit": "TFLOP/s",
-                            "frac": a32 / (p32.value / 1e12),
+               "roofline": {"bound": "fp32", "achieved": a32, "peak": p32, "unit": "TFLOP/s", "frac": a32 / p32,
                             "peak_source": "FP32 CUDA-core FMA peak measured live by isq_fma_peak"},
                "bound": "|fit32 - fit64| <= 1e-4 |fit64| + 1e-6 (tests/test_fitness_gpu.py)"}
         fe.close()
-        if not args.skip_e2e:
+        if hf is not None:
             h32 = np.empty_like(hf)
             _lib.check(lib.isq_fitness_batch_ex(N, L, n_mine, _lib.ptr(hc), _lib.ptr(ht), _lib.ptr(Tc),
                                                 _lib.ptr(h32), local, _lib.PRECISIONS["fp32"]))
             var["max_abs_err_vs_fp64"] = float(np.abs(h32 - hf).max())
             var["max_rel_err_vs_fp64"] = float((np.abs(h32 - hf) / np.maximum(np.abs(hf), 1e-300)).max())
         out["fp32_variant"] = var
+    # side measurements (N = 1, headline config): BASELINE config 4, the
+    # explicit-gate fitness kernels at n = 3/4/5, and the latency-bound C1-C3
+    if world == 1 and CONFIG == "c5" and not args.skip_extras:
+        out["c4"] = side_c4(args, local, fp64_peak, stream)
+        out["fitness_sweep"] = side_fitness_sweep(lib, _lib, fp64_peak, stream)
+        out["tiny"] = side_tiny(local)
     if rank == 0:
         emit(out)
     if world > 1:
@@ -531,7 +691,14 @@ def main():
                     help="N > 1: kernels store into peers over NVLink (p2p) or NCCL collectives between phases")
     ap.add_argument("--cpu-per-worker", type=int, default=400)
     ap.add_argument("--launch-check", action="store_true", help="test the rank launcher only (gloo, no GPU)")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c5",
+                    help="BASELINE.json configuration of the timed generation (c5: the headline)")
+    ap.add_argument("--skip-extras", action="store_true",
+                    help="c5 at N=1: skip the C4 / fitness-sweep / tiny-config side measurements")
     args = ap.parse_args()
+    global N, L, P, CONFIG
+    c = CONFIGS[args.config]
+    N, L, P, CONFIG = c["n"], c["L"], c["P"], args.config
     launch_ranks(args)
     if args.launch_check:
         launch_check(args)

@@ -39,6 +39,12 @@ class CpuPool:
         self.workers = workers or os.cpu_count() or 1
         self.pool = ProcessPoolExecutor(max_workers=self.workers, mp_context=mp.get_context("spawn"))
 
+    def warm(self, n: int, L: int):
+        """Spawn every worker and run a few circuits on each (imports, lru
+        caches) so that the timed calls measure evaluation only."""
+        codes, thetas = qeqea_like_circuits(n, L, 4 * self.workers, seed=99)
+        self.evaluate(n, codes, thetas, np.eye(2 ** n, dtype=np.complex128))
+
     def evaluate(self, n: int, codes: np.ndarray, thetas: np.ndarray, target: np.ndarray):
         """Returns (fitness array, wall seconds) for all circuits, split evenly over the pool."""
         parts = np.array_split(np.arange(codes.shape[0]), self.workers)
