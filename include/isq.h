@@ -320,6 +320,59 @@ isq_status isq_ga_fitness(void* handle, double* out);
 /* Parents drawn by SUS in the last finished generation (P int32). */
 isq_status isq_ga_parents(void* handle, int32_t* out);
 
+/* ------------------------------------------------------------------------
+ * Functional API (the reference's module-level operators, engine.py:105-263,
+ * ga.py:62-138) on the device.  The reference draws from a sequential numpy
+ * Generator passed by the caller; these take the counter-stream position
+ * instead (seed, generation, index -- csrc/np_random.cuh), i.e. exactly the
+ * draws the engines make for that unit, so each call reproduces one step of
+ * the engine.  Host buffers, synchronous.  Complex arrays are numpy
+ * complex128 (interleaved re, im).
+ * ---------------------------------------------------------------------- */
+/* init_population (engine.py:105-112): thetas[Q], qutrits[Qt][3] from the
+ * per-slot init streams (theta uniform, Box-Muller qutrit). */
+isq_status isq_init_population(int32_t n, int32_t length, int64_t population, uint64_t seed, double* thetas,
+                               double* qutrits, int32_t device);
+/* construct_segments (engine.py:156-171): measured axis (0 X, 1 Y, 2 Z) of
+ * every qutrit row s from stream (seed, MEASURE, generation, s). */
+isq_status isq_construct_segments(int32_t n, int32_t length, int64_t population, int32_t n_meas, uint64_t seed,
+                                  uint64_t generation, const double* qutrits, int8_t* axes, int32_t device);
+/* sample_circuit (engine.py:174-184) for circuits [c0, c0 + count) of a
+ * generation: count * length flat slot indices (Eq. 9). */
+isq_status isq_sample_circuits(int32_t n, int32_t length, int64_t population, uint64_t seed, uint64_t generation,
+                               int64_t c0, int64_t count, int64_t* flats, int32_t device);
+/* mutate_population (engine.py:228-263) at the end of `generation`, in place
+ * on thetas[Q] / qutrits[Qt][3] with slot_max[Q]; mutated[s] = 0 untouched,
+ * 1 angle mutation, 2 qutrit mutation (uses cfg: wires, length, population,
+ * probability_of_mutation, mutation_range, seed). */
+isq_status isq_mutate_population(const isq_qeqea_config* cfg, uint64_t generation, double* thetas, double* qutrits,
+                                 const double* slot_max, uint8_t* mutated, int32_t device);
+/* SegmentFitnessTable (engine.py:202-222) on the device: entries keyed by
+ * (flat, position) in a device hash, slot_max[Q].  update: `count`
+ * blueprints of `length` flats and their fitness, in order; improved[c * length
+ * + p] = 1 when that touch raised its entry (the reference's improved set is
+ * the set of their flats).  read: slot_max (nullable), entry count, and
+ * (nullable) the entries as keys flat * length + position and values. */
+isq_status isq_table_create(int64_t qubit_count, int32_t length, int32_t device, void** table);
+isq_status isq_table_destroy(void* table);
+isq_status isq_table_update(void* table, int64_t count, const int64_t* blueprints, const double* fitness,
+                            uint8_t* improved);
+isq_status isq_table_read(void* table, double* slot_max, int64_t* n_entries, int64_t* keys, double* values);
+isq_status isq_table_set_slot_max(void* table, const double* slot_max);
+/* random_genome (ga.py:68-73) of genomes [first, first + count): count * length codes / angles. */
+isq_status isq_ga_random_genomes(int32_t n, int32_t length, uint64_t seed, int64_t first, int64_t count,
+                                 uint8_t* codes, double* thetas, int32_t device);
+/* sus_select (ga.py:95-116): `count` picks from P fitness values, stream (seed, SUS, generation). */
+isq_status isq_ga_sus_select(int64_t population, const double* fitness, int64_t count, uint64_t seed,
+                             uint64_t generation, int64_t* picks, int32_t device);
+/* two_point_crossover cuts (ga.py:81-92) of pairs [first, first + count): (p, q) per pair. */
+isq_status isq_ga_crossover_cuts(int32_t length, uint64_t seed, uint64_t generation, int64_t first, int64_t count,
+                                 int32_t* cuts, int32_t device);
+/* ga_mutate (ga.py:119-138) of children [first, first + count), in place
+ * (uses cfg: wires, length, mutation_rate, mutation_range, structural_rate, seed). */
+isq_status isq_ga_mutate_genomes(const isq_ga_config* cfg, uint64_t generation, int64_t first, int64_t count,
+                                 uint8_t* codes, double* thetas, int32_t device);
+
 /* Diagnostics: measured FP64 (fp64 != 0) or FP32 CUDA-core FMA peak in flop/s
  * on `device` (roofline denominator of the fitness kernel). */
 isq_status isq_fma_peak(int32_t fp64, int32_t device, double* flops_per_s);

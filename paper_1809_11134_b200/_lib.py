@@ -166,6 +166,19 @@ SIGNATURES: dict[str, tuple] = {
     "isq_philox_block": (None, [c_u64, c_u64, c_u64, c_u64, c_u64, c_u64, c_vp]),
     "isq_fma_peak": (c_i32, [c_i32, c_i32, c_vp]),
     "isq_fitness_of_unitaries": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_i32]),
+    "isq_init_population": (c_i32, [c_i32, c_i32, c_i64, c_u64, c_vp, c_vp, c_i32]),
+    "isq_construct_segments": (c_i32, [c_i32, c_i32, c_i64, c_i32, c_u64, c_u64, c_vp, c_vp, c_i32]),
+    "isq_sample_circuits": (c_i32, [c_i32, c_i32, c_i64, c_u64, c_u64, c_i64, c_i64, c_vp, c_i32]),
+    "isq_mutate_population": (c_i32, [ctypes.POINTER(QeqeaConfig), c_u64, c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "isq_table_create": (c_i32, [c_i64, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "isq_table_destroy": (c_i32, [c_vp]),
+    "isq_table_update": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "isq_table_read": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "isq_table_set_slot_max": (c_i32, [c_vp, c_vp]),
+    "isq_ga_random_genomes": (c_i32, [c_i32, c_i32, c_u64, c_i64, c_i64, c_vp, c_vp, c_i32]),
+    "isq_ga_sus_select": (c_i32, [c_i64, c_vp, c_i64, c_u64, c_u64, c_vp, c_i32]),
+    "isq_ga_crossover_cuts": (c_i32, [c_i32, c_u64, c_u64, c_i64, c_i64, c_vp, c_i32]),
+    "isq_ga_mutate_genomes": (c_i32, [ctypes.POINTER(GaConfigC), c_u64, c_i64, c_i64, c_vp, c_vp, c_i32]),
 }
 
 

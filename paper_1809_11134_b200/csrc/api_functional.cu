@@ -1,0 +1,593 @@
+// The reference's functional API (engine.py:105-263, ga.py:62-138) on the
+// device, with the per-unit counter streams of the engines in place of the
+// reference's sequential numpy Generators (csrc/np_random.cuh; DESIGN.md
+// §5.1): a call names the stream position (seed, generation, index) and
+// computes exactly what the engine computes for that unit, so these entry
+// points are the engine's own operators, callable one at a time.
+//
+//   init_population      per-slot stream (seed, DOM_INIT, 0, slot)
+//   construct_segments   per-slot stream (seed, DOM_MEASURE, gen, slot)
+//   sample_circuit       per-circuit stream (seed, DOM_SAMPLE, gen, circuit)
+//   mutate_population    per-slot stream (seed, DOM_MUTATE, gen, slot)
+//   SegmentFitnessTable  device hash of the (flat, position) entries + slot_max
+//   random_genome        per-gene stream (seed, DOM_GA_INIT, 0, genome, gene)
+//   sus_select           stream (seed, DOM_GA_SUS, gen)
+//   two_point_crossover  stream (seed, DOM_GA_PAIR, gen, pair)
+//   ga_mutate            per-gene stream (seed, DOM_GA_MUT, gen, child, gene)
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine_common.cuh"
+#include "isq_internal.h"
+
+namespace isq {
+
+namespace {
+
+isq_status bad_config(const std::string& m) {
+  set_error(m);
+  return ISQ_ERR_CONFIG;
+}
+
+isq_status check_layout(int n, int L, int64_t P) {
+  if (n < ISQ_MIN_WIRES || n > ISQ_MAX_WIRES) {
+    set_error("numberOfWires=" + std::to_string(n) + " is outside the compiled range 2..5");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  if (L < 1 || P < 1) return bad_config("sizeOfIndividual and sizeOfPopulation must be ≥ 1");
+  const int64_t K = n + (int64_t)n * (n - 1) / 2;
+  if (K * P * L >= (1LL << 32) - 1) {
+    set_error("qubit_count = K*P*L must stay below 2^32 for the device engine");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  return ISQ_OK;
+}
+
+// A one-rank QeqeaArgs carrying only the layout and stream parameters the
+// per-slot / per-circuit device functions read.
+QeqeaArgs functional_args(int n, int L, int64_t P, uint64_t seed) {
+  QeqeaArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = n;
+  a.L = L;
+  a.P = P;
+  a.K = n + (int64_t)n * (n - 1) / 2;
+  a.Q = a.K * P * L;
+  a.Qt = (int64_t)n * P * L;
+  a.seed = seed;
+  a.world = 1;
+  a.S = P;
+  a.Lr = L;
+  a.p_bounds[1] = L;
+  a.div_L.init((uint32_t)L);
+  a.div_LP.init((uint32_t)(L * P));
+  a.div_Lr.init((uint32_t)L);
+  a.div_S.init((uint32_t)P);
+  a.Qloc = a.Q;
+  a.Qtloc = a.Qt;
+  return a;
+}
+
+int grid_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > 148 * 32) b = 148 * 32;
+  return (int)(b < 1 ? 1 : b);
+}
+
+// RAII device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes < 16 ? 16 : bytes); }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+#define TRYF(expr)                                                          \
+  do {                                                                      \
+    cudaError_t _e = (expr);                                                \
+    if (_e != cudaSuccess) {                                                \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+      return ISQ_ERR_CUDA;                                                  \
+    }                                                                       \
+  } while (0)
+
+}  // namespace
+
+// ------------------------------------------------------------------ QEQEA ---
+
+__global__ void fn_init_population_kernel(QeqeaArgs a, double* theta, double2* q) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q; s += (int64_t)gridDim.x * blockDim.x) {
+    double t;
+    double2 qq[3];
+    init_slot_value(a.seed, s, s < a.Qt, t, qq);
+    theta[s] = t;
+    if (s < a.Qt) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) q[3 * s + k] = qq[k];
+    }
+  }
+}
+
+__global__ void fn_construct_segments_kernel(QeqeaArgs a, uint64_t g, const double2* q, int8_t* axes) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Qt; s += (int64_t)gridDim.x * blockDim.x) {
+    double re[3] = {q[3 * s].x, q[3 * s + 1].x, q[3 * s + 2].x};
+    double im[3] = {q[3 * s].y, q[3 * s + 1].y, q[3 * s + 2].y};
+    NpStream st;
+    st.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);
+    bool ok = true;
+    axes[s] = (int8_t)measure_axis(re, im, a.n_meas, st, &ok);
+  }
+}
+
+__global__ void __launch_bounds__(128) fn_sample_kernel(QeqeaArgs a, uint64_t g, int64_t c0, int64_t count,
+                                                        uint32_t* flats) {
+  __shared__ uint64_t blk[4][36];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (int64_t c = (int64_t)blockIdx.x * 4 + wib; c < count; c += (int64_t)gridDim.x * 4)
+    sample_circuit_warp(a, g, c0 + c, flats + c * a.L, blk[wib], lane);
+}
+
+__global__ void fn_widen_kernel(const uint32_t* in, int64_t* out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+__global__ void fn_mutate_population_kernel(QeqeaArgs a, uint64_t g, double* theta, double2* q,
+                                            const double* slot_max, uint8_t* mutated) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.Q; s += (int64_t)gridDim.x * blockDim.x) {
+    LiveSlot v;
+    v.theta = theta[s];
+    const bool has_q = s < a.Qt;
+    if (has_q) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v.q[k] = q[3 * s + k];
+    }
+    bool qpath = false;
+    const bool m = mutate_slot(a, s, g, slot_max[s], v, &qpath);
+    mutated[s] = m ? (qpath ? 2 : 1) : 0;
+    if (m) {
+      theta[s] = v.theta;
+      if (qpath) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) q[3 * s + k] = v.q[k];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------- SegmentFitnessTable ---
+// entries: open-addressing hash of key = flat * L + position + 1 (0 = empty)
+// -> fitness bits (u64 atomicMax: fitness >= 0); slot_max: u64 atomicMax.
+struct TableHandle {
+  int64_t Q = 0;
+  int L = 0;
+  int device = 0;
+  int64_t cap = 0;
+  unsigned long long* keys = nullptr;
+  unsigned long long* vals = nullptr;
+  unsigned long long* count = nullptr;  // occupied entries
+  double* smax = nullptr;
+};
+
+__device__ __forceinline__ uint64_t table_hash(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+
+__device__ __forceinline__ int64_t table_slot(unsigned long long* keys, unsigned long long* count, int64_t cap,
+                                              unsigned long long key) {
+  int64_t h = (int64_t)(table_hash(key) & (uint64_t)(cap - 1));
+  while (true) {
+    const unsigned long long k = atomicCAS(&keys[h], 0ULL, key);
+    if (k == 0ULL) {
+      atomicAdd(count, 1ULL);
+      return h;
+    }
+    if (k == key) return h;
+    h = (h + 1) & (cap - 1);
+  }
+}
+
+// SegmentFitnessTable.update (engine.py:211-222) for a batch of blueprints in
+// order: touch (circuit c, position p) improves iff its fitness beats the
+// running entry; the union of improved slots is order-independent (a slot is
+// in it iff the batch's best touch of one of its keys beats the entry).
+__global__ void fn_table_update_kernel(TableHandle t, int64_t touches, const int64_t* flats, const double* fits,
+                                       uint8_t* improved) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < touches;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / t.L;
+    const int p = (int)(i - c * t.L);
+    const int64_t flat = flats[i];
+    const double fit = fits[c];
+    if (!(fit > 0.0)) {  // entries.get(key, 0.0): a zero fitness creates no entry
+      improved[i] = 0;
+      continue;
+    }
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(fit);
+    const int64_t h = table_slot(t.keys, t.count, t.cap, (unsigned long long)(flat * t.L + p + 1));
+    const unsigned long long old = atomicMax(&t.vals[h], bits);
+    improved[i] = fit > __longlong_as_double((long long)old) ? 1 : 0;
+    atomicMax(reinterpret_cast<unsigned long long*>(t.smax + flat), bits);
+  }
+}
+
+__global__ void fn_table_rehash_kernel(TableHandle dst, const unsigned long long* keys,
+                                       const unsigned long long* vals, int64_t cap) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+    if (keys[i] == 0ULL) continue;
+    const int64_t h = table_slot(dst.keys, dst.count, dst.cap, keys[i]);
+    dst.vals[h] = vals[i];
+  }
+}
+
+static void table_free(TableHandle* t) {
+  if (!t) return;
+  cudaSetDevice(t->device);
+  cudaFree(t->keys);
+  cudaFree(t->vals);
+  cudaFree(t->count);
+  cudaFree(t->smax);
+  delete t;
+}
+
+// Capacity for `want` entries at load <= 1/2.
+static isq_status table_reserve(TableHandle* t, int64_t want) {
+  int64_t cap = t->cap;
+  while (cap < 2 * want) cap *= 2;
+  if (cap == t->cap) return ISQ_OK;
+  TableHandle nt = *t;
+  nt.cap = cap;
+  nt.keys = nullptr;
+  nt.vals = nullptr;
+  nt.count = nullptr;
+  TRYF(cudaMalloc((void**)&nt.keys, cap * 8));
+  TRYF(cudaMalloc((void**)&nt.vals, cap * 8));
+  TRYF(cudaMalloc((void**)&nt.count, 8));
+  TRYF(cudaMemset(nt.keys, 0, cap * 8));
+  TRYF(cudaMemset(nt.vals, 0, cap * 8));
+  TRYF(cudaMemset(nt.count, 0, 8));
+  fn_table_rehash_kernel<<<grid_for(t->cap), 256>>>(nt, t->keys, t->vals, t->cap);
+  TRYF(cudaGetLastError());
+  TRYF(cudaDeviceSynchronize());
+  cudaFree(t->keys);
+  cudaFree(t->vals);
+  cudaFree(t->count);
+  t->keys = nt.keys;
+  t->vals = nt.vals;
+  t->count = nt.count;
+  t->cap = cap;
+  return ISQ_OK;
+}
+
+// -------------------------------------------------------------------- GA ---
+
+__global__ void fn_ga_random_genomes_kernel(int L, int ncodes, uint64_t seed, int64_t first, int64_t count,
+                                            uint8_t* codes, double* thetas) {
+  const int64_t total = count * L;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / L;
+    const int j = (int)(t - i * L);
+    NpStream s;
+    s.init(seed, DOM_GA_INIT, 0, (uint64_t)(first + i), (uint64_t)j);
+    codes[t] = (uint8_t)s.integers(ncodes);
+    thetas[t] = s.uniform(0.0, kTwoPiD);
+  }
+}
+
+// sus_select (ga.py:95-116), one thread: numpy's pairwise total, the
+// sequential walk in its own rounding.
+__global__ void fn_ga_sus_kernel(const double* f, int64_t P, int64_t count, uint64_t seed, uint64_t g,
+                                 int64_t* picks) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  NpStream rs;
+  rs.init(seed, DOM_GA_SUS, g, 0, 0);
+  const double total = np_pairwise_sum(f, P);
+  if (total <= 0.0) {
+    for (int64_t k = 0; k < count; ++k) picks[k] = rs.integers(P);
+    return;
+  }
+  const double spacing = __ddiv_rn(total, (double)count);
+  double pointer = rs.uniform(0.0, spacing);
+  double cumulative = 0.0;
+  int64_t index = 0;
+  for (int64_t k = 0; k < count; ++k) {
+    while (index < P - 1 && __dadd_rn(cumulative, f[index]) <= pointer) {
+      cumulative = __dadd_rn(cumulative, f[index]);
+      ++index;
+    }
+    picks[k] = index;
+    pointer = __dadd_rn(pointer, spacing);
+  }
+}
+
+// two_point_crossover cuts (ga.py:81-92): sorted(integers(0, L + 1, size=2)), no draw for L < 2.
+__global__ void fn_ga_cuts_kernel(int L, uint64_t seed, uint64_t g, int64_t first, int64_t count, int32_t* pq) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+    int p = 0, q = 0;
+    if (L >= 2) {
+      NpStream cs;
+      cs.init(seed, DOM_GA_PAIR, g, (uint64_t)(first + k), 0);
+      const int x = (int)cs.integers(L + 1), y = (int)cs.integers(L + 1);
+      p = x < y ? x : y;
+      q = x < y ? y : x;
+    }
+    pq[2 * k] = p;
+    pq[2 * k + 1] = q;
+  }
+}
+
+// ga_mutate (ga.py:119-138), gene j of child `first + i`.
+__global__ void fn_ga_mutate_kernel(int L, int ncodes, double rate, double mrange, double structural, uint64_t seed,
+                                    uint64_t g, int64_t first, int64_t count, uint8_t* codes, double* thetas) {
+  const int64_t total = count * L;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / L;
+    const int j = (int)(t - i * L);
+    NpStream ms;
+    ms.init(seed, DOM_GA_MUT, g, (uint64_t)(first + i), (uint64_t)j);
+    if (ms.random() >= rate) continue;
+    if (ms.random() < structural)
+      codes[t] = (uint8_t)ms.integers(ncodes);
+    else
+      thetas[t] = py_mod(__dadd_rn(thetas[t], ms.uniform(-mrange, mrange)), kTwoPiD);
+  }
+}
+
+}  // namespace isq
+
+using namespace isq;
+
+extern "C" {
+
+isq_status isq_init_population(int32_t n, int32_t L, int64_t P, uint64_t seed, double* thetas, double* qutrits,
+                               int32_t device) {
+  isq_status st = check_layout(n, L, P);
+  if (st != ISQ_OK) return st;
+  TRYF(cudaSetDevice(device));
+  const QeqeaArgs a = functional_args(n, L, P, seed);
+  DevBuf dt, dq;
+  TRYF(dt.alloc(a.Q * 8));
+  TRYF(dq.alloc(a.Qt * 48));
+  fn_init_population_kernel<<<grid_for(a.Q), 256>>>(a, dt.as<double>(), dq.as<double2>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(thetas, dt.p, a.Q * 8, cudaMemcpyDeviceToHost));
+  TRYF(cudaMemcpy(qutrits, dq.p, a.Qt * 48, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_construct_segments(int32_t n, int32_t L, int64_t P, int32_t n_meas, uint64_t seed,
+                                  uint64_t generation, const double* qutrits, int8_t* axes, int32_t device) {
+  isq_status st = check_layout(n, L, P);
+  if (st != ISQ_OK) return st;
+  if (n_meas < 1) return bad_config("nMeas must be ≥ 1");
+  if (n_meas > 60) {
+    set_error("nMeas > 60 needs numpy's BTPE binomial branch, which this build does not implement");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  TRYF(cudaSetDevice(device));
+  QeqeaArgs a = functional_args(n, L, P, seed);
+  a.n_meas = n_meas;
+  DevBuf dq, dx;
+  TRYF(dq.alloc(a.Qt * 48));
+  TRYF(dx.alloc(a.Qt));
+  TRYF(cudaMemcpy(dq.p, qutrits, a.Qt * 48, cudaMemcpyHostToDevice));
+  fn_construct_segments_kernel<<<grid_for(a.Qt), 256>>>(a, generation, dq.as<double2>(), dx.as<int8_t>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(axes, dx.p, a.Qt, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_sample_circuits(int32_t n, int32_t L, int64_t P, uint64_t seed, uint64_t generation, int64_t c0,
+                               int64_t count, int64_t* flats, int32_t device) {
+  isq_status st = check_layout(n, L, P);
+  if (st != ISQ_OK) return st;
+  if (c0 < 0 || count < 0) return bad_config("circuit range out of bounds");
+  if (count == 0) return ISQ_OK;
+  TRYF(cudaSetDevice(device));
+  const QeqeaArgs a = functional_args(n, L, P, seed);
+  DevBuf d32, d64;
+  TRYF(d32.alloc(count * L * 4));
+  TRYF(d64.alloc(count * L * 8));
+  fn_sample_kernel<<<grid_for(count, 4), 128>>>(a, generation, c0, count, d32.as<uint32_t>());
+  fn_widen_kernel<<<grid_for(count * L), 256>>>(d32.as<uint32_t>(), d64.as<int64_t>(), count * L);
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(flats, d64.p, count * L * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_mutate_population(const isq_qeqea_config* cfg, uint64_t generation, double* thetas, double* qutrits,
+                                 const double* slot_max, uint8_t* mutated, int32_t device) {
+  isq_status st = check_layout(cfg->number_of_wires, cfg->size_of_individual, cfg->size_of_population);
+  if (st != ISQ_OK) return st;
+  if (!(cfg->probability_of_mutation >= 0.0 && cfg->probability_of_mutation <= 1.0))
+    return bad_config("probabilityOfMutation must be in [0, 1]");
+  if (!(cfg->mutation_range > 0.0)) return bad_config("mutationRange must be > 0");
+  TRYF(cudaSetDevice(device));
+  QeqeaArgs a = functional_args(cfg->number_of_wires, cfg->size_of_individual, cfg->size_of_population, cfg->seed);
+  a.p_mut = cfg->probability_of_mutation;
+  a.mutation_range = cfg->mutation_range;
+  DevBuf dt, dq, ds, dm;
+  TRYF(dt.alloc(a.Q * 8));
+  TRYF(dq.alloc(a.Qt * 48));
+  TRYF(ds.alloc(a.Q * 8));
+  TRYF(dm.alloc(a.Q));
+  TRYF(cudaMemcpy(dt.p, thetas, a.Q * 8, cudaMemcpyHostToDevice));
+  TRYF(cudaMemcpy(dq.p, qutrits, a.Qt * 48, cudaMemcpyHostToDevice));
+  TRYF(cudaMemcpy(ds.p, slot_max, a.Q * 8, cudaMemcpyHostToDevice));
+  fn_mutate_population_kernel<<<grid_for(a.Q), 256>>>(a, generation, dt.as<double>(), dq.as<double2>(),
+                                                      ds.as<double>(), dm.as<uint8_t>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(thetas, dt.p, a.Q * 8, cudaMemcpyDeviceToHost));
+  TRYF(cudaMemcpy(qutrits, dq.p, a.Qt * 48, cudaMemcpyDeviceToHost));
+  TRYF(cudaMemcpy(mutated, dm.p, a.Q, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_table_create(int64_t qubit_count, int32_t length, int32_t device, void** handle) {
+  *handle = nullptr;
+  if (qubit_count < 1 || length < 1) return bad_config("qubit_count and sizeOfIndividual must be ≥ 1");
+  TRYF(cudaSetDevice(device));
+  TableHandle* t = new TableHandle();
+  t->Q = qubit_count;
+  t->L = length;
+  t->device = device;
+  t->cap = 1024;
+  cudaError_t e = cudaMalloc((void**)&t->keys, t->cap * 8);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&t->vals, t->cap * 8);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&t->count, 8);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&t->smax, qubit_count * 8);
+  if (e == cudaSuccess) e = cudaMemset(t->keys, 0, t->cap * 8);
+  if (e == cudaSuccess) e = cudaMemset(t->vals, 0, t->cap * 8);
+  if (e == cudaSuccess) e = cudaMemset(t->count, 0, 8);
+  if (e == cudaSuccess) e = cudaMemset(t->smax, 0, qubit_count * 8);
+  if (e != cudaSuccess) {
+    table_free(t);
+    set_error(std::string("table allocation: ") + cudaGetErrorString(e));
+    return ISQ_ERR_CUDA;
+  }
+  *handle = t;
+  return ISQ_OK;
+}
+
+isq_status isq_table_destroy(void* handle) {
+  table_free(static_cast<TableHandle*>(handle));
+  return ISQ_OK;
+}
+
+isq_status isq_table_update(void* handle, int64_t count, const int64_t* blueprints, const double* fitness,
+                            uint8_t* improved) {
+  TableHandle* t = static_cast<TableHandle*>(handle);
+  if (!t) return bad_config("null table handle");
+  if (count <= 0) return ISQ_OK;
+  const int64_t touches = count * t->L;
+  for (int64_t i = 0; i < touches; ++i)
+    if (blueprints[i] < 0 || blueprints[i] >= t->Q) return bad_config("blueprint slot out of range");
+  for (int64_t c = 0; c < count; ++c)
+    if (!(fitness[c] >= 0.0)) return bad_config("fitness must be a number >= 0");
+  TRYF(cudaSetDevice(t->device));
+  unsigned long long have = 0;
+  TRYF(cudaMemcpy(&have, t->count, 8, cudaMemcpyDeviceToHost));
+  isq_status st = table_reserve(t, (int64_t)have + touches);
+  if (st != ISQ_OK) return st;
+  DevBuf df, dv, di;
+  TRYF(df.alloc(touches * 8));
+  TRYF(dv.alloc(count * 8));
+  TRYF(di.alloc(touches));
+  TRYF(cudaMemcpy(df.p, blueprints, touches * 8, cudaMemcpyHostToDevice));
+  TRYF(cudaMemcpy(dv.p, fitness, count * 8, cudaMemcpyHostToDevice));
+  fn_table_update_kernel<<<grid_for(touches), 256>>>(*t, touches, df.as<int64_t>(), dv.as<double>(),
+                                                    di.as<uint8_t>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(improved, di.p, touches, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_table_read(void* handle, double* slot_max, int64_t* n_entries, int64_t* keys, double* values) {
+  TableHandle* t = static_cast<TableHandle*>(handle);
+  if (!t) return bad_config("null table handle");
+  TRYF(cudaSetDevice(t->device));
+  if (slot_max) TRYF(cudaMemcpy(slot_max, t->smax, t->Q * 8, cudaMemcpyDeviceToHost));
+  unsigned long long have = 0;
+  TRYF(cudaMemcpy(&have, t->count, 8, cudaMemcpyDeviceToHost));
+  if (n_entries) *n_entries = (int64_t)have;
+  if (keys || values) {
+    std::vector<unsigned long long> k(t->cap), v(t->cap);
+    TRYF(cudaMemcpy(k.data(), t->keys, t->cap * 8, cudaMemcpyDeviceToHost));
+    TRYF(cudaMemcpy(v.data(), t->vals, t->cap * 8, cudaMemcpyDeviceToHost));
+    int64_t o = 0;
+    for (int64_t i = 0; i < t->cap; ++i) {
+      if (k[i] == 0ULL) continue;
+      if (keys) keys[o] = (int64_t)(k[i] - 1);  // flat * L + position
+      if (values) std::memcpy(&values[o], &v[i], 8);
+      ++o;
+    }
+  }
+  return ISQ_OK;
+}
+
+isq_status isq_table_set_slot_max(void* handle, const double* slot_max) {
+  TableHandle* t = static_cast<TableHandle*>(handle);
+  if (!t) return bad_config("null table handle");
+  TRYF(cudaSetDevice(t->device));
+  TRYF(cudaMemcpy(t->smax, slot_max, t->Q * 8, cudaMemcpyHostToDevice));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_random_genomes(int32_t n, int32_t L, uint64_t seed, int64_t first, int64_t count, uint8_t* codes,
+                                 double* thetas, int32_t device) {
+  isq_status st = check_layout(n, L, 1);
+  if (st != ISQ_OK) return st;
+  if (first < 0 || count < 0) return bad_config("genome range out of bounds");
+  if (count == 0) return ISQ_OK;
+  TRYF(cudaSetDevice(device));
+  DevBuf dc, dt;
+  TRYF(dc.alloc(count * L));
+  TRYF(dt.alloc(count * L * 8));
+  fn_ga_random_genomes_kernel<<<grid_for(count * L), 256>>>(L, 3 * n + n * (n - 1) / 2, seed, first, count,
+                                                            dc.as<uint8_t>(), dt.as<double>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(codes, dc.p, count * L, cudaMemcpyDeviceToHost));
+  TRYF(cudaMemcpy(thetas, dt.p, count * L * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_sus_select(int64_t P, const double* fitness, int64_t count, uint64_t seed, uint64_t generation,
+                             int64_t* picks, int32_t device) {
+  if (P < 1 || count < 0) return bad_config("sus_select needs at least one fitness value");
+  if (count == 0) return ISQ_OK;
+  TRYF(cudaSetDevice(device));
+  DevBuf df, dp;
+  TRYF(df.alloc(P * 8));
+  TRYF(dp.alloc(count * 8));
+  TRYF(cudaMemcpy(df.p, fitness, P * 8, cudaMemcpyHostToDevice));
+  fn_ga_sus_kernel<<<1, 1>>>(df.as<double>(), P, count, seed, generation, dp.as<int64_t>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(picks, dp.p, count * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_crossover_cuts(int32_t L, uint64_t seed, uint64_t generation, int64_t first, int64_t count,
+                                 int32_t* cuts, int32_t device) {
+  if (L < 0 || first < 0 || count < 0) return bad_config("crossover range out of bounds");
+  if (count == 0) return ISQ_OK;
+  TRYF(cudaSetDevice(device));
+  DevBuf dc;
+  TRYF(dc.alloc(count * 8));
+  fn_ga_cuts_kernel<<<grid_for(count), 256>>>(L, seed, generation, first, count, dc.as<int32_t>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(cuts, dc.p, count * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_ga_mutate_genomes(const isq_ga_config* cfg, uint64_t generation, int64_t first, int64_t count,
+                                 uint8_t* codes, double* thetas, int32_t device) {
+  const int n = cfg->number_of_wires, L = cfg->size_of_individual;
+  isq_status st = check_layout(n, L, 1);
+  if (st != ISQ_OK) return st;
+  if (first < 0 || count < 0) return bad_config("genome range out of bounds");
+  if (count == 0) return ISQ_OK;
+  TRYF(cudaSetDevice(device));
+  DevBuf dc, dt;
+  TRYF(dc.alloc(count * L));
+  TRYF(dt.alloc(count * L * 8));
+  TRYF(cudaMemcpy(dc.p, codes, count * L, cudaMemcpyHostToDevice));
+  TRYF(cudaMemcpy(dt.p, thetas, count * L * 8, cudaMemcpyHostToDevice));
+  fn_ga_mutate_kernel<<<grid_for(count * L), 256>>>(L, 3 * n + n * (n - 1) / 2, cfg->mutation_rate,
+                                                    cfg->mutation_range, cfg->structural_rate, cfg->seed, generation,
+                                                    first, count, dc.as<uint8_t>(), dt.as<double>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(codes, dc.p, count * L, cudaMemcpyDeviceToHost));
+  TRYF(cudaMemcpy(thetas, dt.p, count * L * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+}  // extern "C"

@@ -313,6 +313,34 @@ __device__ __forceinline__ bool mutate_slot(const QeqeaArgs& a, int64_t s, uint6
   return m != MUT_NONE;
 }
 
+// Initial value of slot s (init_population, engine.py:105-112; oracle/streams.py
+// init_slot): theta = uniform(0, 2pi) from block 1 of stream (seed, DOM_INIT, 0,
+// s), and for rotation-region slots a normalised complex Gaussian qutrit by
+// Box-Muller from the next six uniforms.
+__device__ __forceinline__ void init_slot_value(uint64_t seed, int64_t s, bool with_qutrit, double& theta,
+                                                double2 q[3]) {
+  uint64_t w0[4], w1[4];
+  stream_block(seed, DOM_INIT, 0, (uint64_t)s, 0, 1, w0);
+  theta = __dadd_rn(0.0, __dmul_rn(kTwoPiD, u64_to_double(w0[0])));
+  if (!with_qutrit) return;
+  stream_block(seed, DOM_INIT, 0, (uint64_t)s, 0, 2, w1);
+  const uint64_t u[6] = {w0[1], w0[2], w0[3], w1[0], w1[1], w1[2]};
+  double re[3], im[3], nn = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double u1 = u64_to_double(u[2 * k]), u2 = u64_to_double(u[2 * k + 1]);
+    const double r = sqrt(-2.0 * log(1.0 - u1));
+    double sn, cs;
+    sincos(kTwoPiD * u2, &sn, &cs);
+    re[k] = r * cs;
+    im[k] = r * sn;
+    nn += re[k] * re[k] + im[k] * im[k];
+  }
+  const double nrm = sqrt(nn);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) q[k] = make_double2(re[k] / nrm, im[k] / nrm);
+}
+
 // Live value of the (owned) slot s during generation g (committed value plus
 // the pending mutation drawn at the end of generation g-1).
 __device__ __forceinline__ void live_slot(const QeqeaArgs& a, int64_t s, uint64_t g, LiveSlot& v,

@@ -123,34 +123,6 @@ __global__ void __launch_bounds__(kGaRed) ga_reduce_partials(GaArgs a) {
   ga_reduce_partial_body(a, blockIdx.x, smax, ssum, sarg);
 }
 
-// numpy's pairwise summation of a contiguous float64 array (np.sum, used by
-// sus_select's total, ga.py:100): blocks of <= 128 with 8 accumulators,
-// recursive halving at multiples of 8 above.
-__device__ double np_pairwise_sum(const double* a, int64_t n) {
-  if (n < 8) {
-    double r = 0.0;
-    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
-    return r;
-  }
-  if (n <= 128) {
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
-}
-
 // Final reduction + best-so-far update (ga.py:171-174) + SUS (ga.py:95-116).
 // SUS is a sequential walk (cumulative sums compared against pointer +=
 // spacing): thread 0 replays its two running sums exactly, the picks are

@@ -565,9 +565,9 @@ __global__ void qeqea_init_kernel(QeqeaArgs a) {
   for (int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; loc < a.Qloc;
        loc += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = slot_global(a, loc);
-    uint64_t w0[4], w1[4];
-    stream_block(a.seed, DOM_INIT, 0, (uint64_t)s, 0, 1, w0);
-    const double theta = __dadd_rn(0.0, __dmul_rn(kTwoPiD, u64_to_double(w0[0])));
+    double theta;
+    double2 q[3];
+    init_slot_value(a.seed, s, loc < a.Qtloc, theta, q);
     a.claim[loc] = 0;
     if (loc >= a.Qtloc) {
       a.inter[loc - a.Qtloc].theta = theta;
@@ -575,22 +575,8 @@ __global__ void qeqea_init_kernel(QeqeaArgs a) {
     } else {
       a.rot[loc].theta = theta;
       a.rot[loc].smax = 0.0;
-      stream_block(a.seed, DOM_INIT, 0, (uint64_t)s, 0, 2, w1);
-      const uint64_t u[6] = {w0[1], w0[2], w0[3], w1[0], w1[1], w1[2]};
-      double re[3], im[3], nn = 0.0;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double u1 = u64_to_double(u[2 * k]), u2 = u64_to_double(u[2 * k + 1]);
-        const double r = sqrt(-2.0 * log(1.0 - u1));
-        double sn, cs;
-        sincos(kTwoPiD * u2, &sn, &cs);
-        re[k] = r * cs;
-        im[k] = r * sn;
-        nn += re[k] * re[k] + im[k] * im[k];
-      }
-      const double nrm = sqrt(nn);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) a.rot[loc].q[k] = make_double2(re[k] / nrm, im[k] / nrm);
+      for (int k = 0; k < 3; ++k) a.rot[loc].q[k] = q[k];
     }
   }
 }

@@ -478,3 +478,19 @@ def run_qeqea(cfg: PopulationConfig, target: TargetSpec, seed: int, workers: int
     from .report import run_engine
 
     return run_engine(QeqeaEngine(cfg, target, seed, workers=workers))
+
+
+_FUNCTIONAL = {"init_population", "SegmentBank", "construct_segments", "sample_circuit", "evaluate_circuit",
+               "SegmentFitnessTable", "mutate_population", "Snapshot", "CounterStreams"}
+
+
+def __getattr__(name):
+    """The reference's module-level operators (engine.py:105-263) live in
+    .functional (device-backed, counter streams); re-exported here so
+    `from paper_1809_11134_b200.engine import SegmentFitnessTable` works as
+    `from isingsynth.engine import SegmentFitnessTable` does."""
+    if name in _FUNCTIONAL:
+        from . import functional
+
+        return getattr(functional, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -257,3 +257,16 @@ def run_ga(cfg: GaConfig, target: TargetSpec, seed: int, workers: int = 1):
     from .report import run_engine
 
     return run_engine(GaEngine(cfg, target, seed, workers=workers))
+
+
+_FUNCTIONAL = {"random_genome", "decode_genome", "two_point_crossover", "sus_select", "ga_mutate"}
+
+
+def __getattr__(name):
+    """The reference's GA operators (ga.py:62-138) live in .functional
+    (device-backed, counter streams); re-exported as isingsynth.ga exports them."""
+    if name in _FUNCTIONAL:
+        from . import functional
+
+        return getattr(functional, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
