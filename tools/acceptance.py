@@ -51,6 +51,27 @@ def main():
           for s in SEEDS]
     out["c3_toffoli_medians"] = {"ga": round(statistics.median(ga), 4), "qeqea": round(statistics.median(qe), 4),
                                  "ga_all": [round(x, 4) for x in ga], "qeqea_all": [round(x, 4) for x in qe]}
+    # criteria 3 and 12 as distributions over seeds 1..40 (the reference's own
+    # runs of the same configurations: tests/golden/acceptance_outcomes_reference.json)
+    many = range(1, 41)
+    dist = {
+        "c3_ga_toffoli": [run(GaEngine(GaConfig(3, 16, 50, max_generations=20_000), target_matrix("Toffoli"), s))[0]
+                          for s in many],
+        "c3_qeqea_toffoli": [run(QeqeaEngine(PopulationConfig(3, 16, 5, max_generations=20_000),
+                                             target_matrix("Toffoli"), s))[0] for s in many],
+    }
+    for algo, name, gens in (("qeqea", "CCCNOT", 2000), ("qeqea", "Peres", 2000), ("ga", "Peres", 1000)):
+        spec = target_matrix(name)
+        vals = []
+        for s in many:
+            if algo == "qeqea":
+                e = QeqeaEngine(PopulationConfig(spec.number_of_wires, 16, 5, max_generations=gens), spec, s)
+            else:
+                e = GaEngine(GaConfig(spec.number_of_wires, 16, 20, max_generations=gens), spec, s)
+            vals.append(run(e)[0])
+        dist[f"c12_{algo}_{name}_{gens}"] = vals
+    out["distributions_seeds_1_40"] = {k: {str(s): round(v, 6) for s, v in zip(many, vals)}
+                                       for k, vals in dist.items()}
     r = [run(QeqeaEngine(PopulationConfig(3, 16, 5, probability_of_mutation=0.1, n_meas=11, max_generations=50_000,
                                           target_fitness=0.55), target_matrix("Toffoli"), s)) for s in SEEDS]
     out["c4_qeqea_toffoli_floor"] = [round(b, 4) for b, _, _ in r]
