@@ -150,7 +150,7 @@ def construct_axis_per_slot(qutrits: np.ndarray, cfg, seed: int, gen: int) -> np
 def gen_measure():
     out = {}
     rng = np.random.default_rng(5)
-    for n_meas in (1, 3, 11):
+    for n_meas in (1, 3, 11, 61, 100, 1000):
         cfg = R_eng.PopulationConfig(number_of_wires=3, size_of_individual=8, size_of_population=25,
                                      n_meas=n_meas)
         pop = R_eng.init_population(cfg, rng)

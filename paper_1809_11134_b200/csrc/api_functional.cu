@@ -369,10 +369,6 @@ isq_status isq_construct_segments(int32_t n, int32_t L, int64_t P, int32_t n_mea
   isq_status st = check_layout(n, L, P);
   if (st != ISQ_OK) return st;
   if (n_meas < 1) return bad_config("nMeas must be ≥ 1");
-  if (n_meas > 60) {
-    set_error("nMeas > 60 needs numpy's BTPE binomial branch, which this build does not implement");
-    return ISQ_ERR_UNSUPPORTED;
-  }
   TRYF(cudaSetDevice(device));
   QeqeaArgs a = functional_args(n, L, P, seed);
   a.n_meas = n_meas;

@@ -75,10 +75,6 @@ static isq_status validate(const isq_qeqea_config* c) {
               " exceeds the device kernels (compiled for 2..5 wires)");
     return ISQ_ERR_UNSUPPORTED;
   }
-  if (c->n_meas > 60) {
-    set_error("nMeas > 60 needs numpy's BTPE binomial branch, which this build does not implement");
-    return ISQ_ERR_UNSUPPORTED;
-  }
   if (c->size_of_individual > 4096) {
     set_error("sizeOfIndividual > 4096 is not supported by the device engine");
     return ISQ_ERR_UNSUPPORTED;

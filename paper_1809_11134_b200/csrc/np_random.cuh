@@ -22,7 +22,8 @@
 //   integers(b)  : Lemire on u32 with rejection, rng = b - 1
 //                  (distributions.c buffered_bounded_lemire_uint32)
 //   uniform(l,h) : l + (h - l) * next_double
-//   binomial     : inversion for n*min(p,1-p) <= 30     (random_binomial_inversion)
+//   binomial     : inversion for n*min(p,1-p) <= 30     (random_binomial_inversion),
+//                  BTPE above                          (random_binomial_btpe)
 //   multinomial  : sequential binomials                  (random_multinomial)
 //
 // All floating point that must be bit-exact is written with explicit
@@ -248,20 +249,114 @@ __device__ __forceinline__ int64_t binomial_inversion(NpStream& s, int64_t n, do
   return X;
 }
 
-// numpy random_binomial restricted to the inversion branch; *ok = false when
-// numpy would take the BTPE branch (n * min(p, 1-p) > 30), which this build
-// rejects at configuration time (n_meas <= 60 guarantees inversion).
+// numpy random_binomial_btpe (distributions.c; Kachitvichyanukul & Schmeiser's
+// BTPE) for n * min(p, 1 - p) > 30, with every operation in C's order and
+// without FMA contraction (numpy's distributions.c is compiled without FMA:
+// oracle/binomial.py restates it and matches numpy's Generator draw for draw,
+// tests/test_oracle.py).  log / exp are the device versions (see
+// binomial_inversion).  Called with p <= 0.5, as random_binomial does.
+__device__ inline int64_t binomial_btpe(NpStream& s, int64_t n, double p) {
+  const double dn = (double)n;
+  const double one_p = ISQ_DSUB(1.0, p);
+  const double r = p < one_p ? p : one_p;
+  const double q = ISQ_DSUB(1.0, r);
+  const double fm = ISQ_DADD(ISQ_DMUL(dn, r), r);
+  const int64_t m = (int64_t)floor(fm);
+  const double dm = (double)m;
+  const double p1 = ISQ_DADD(floor(ISQ_DSUB(ISQ_DMUL(2.195, sqrt(ISQ_DMUL(ISQ_DMUL(dn, r), q))), ISQ_DMUL(4.6, q))), 0.5);
+  const double xm = ISQ_DADD(dm, 0.5);
+  const double xl = ISQ_DSUB(xm, p1);
+  const double xr = ISQ_DADD(xm, p1);
+  const double c = ISQ_DADD(0.134, ISQ_DDIV(20.5, ISQ_DADD(15.3, dm)));
+  double a = ISQ_DDIV(ISQ_DSUB(fm, xl), ISQ_DSUB(fm, ISQ_DMUL(xl, r)));
+  const double laml = ISQ_DMUL(a, ISQ_DADD(1.0, ISQ_DDIV(a, 2.0)));
+  a = ISQ_DDIV(ISQ_DSUB(xr, fm), ISQ_DMUL(xr, q));
+  const double lamr = ISQ_DMUL(a, ISQ_DADD(1.0, ISQ_DDIV(a, 2.0)));
+  const double p2 = ISQ_DMUL(p1, ISQ_DADD(1.0, ISQ_DMUL(2.0, c)));
+  const double p3 = ISQ_DADD(p2, ISQ_DDIV(c, laml));
+  const double p4 = ISQ_DADD(p3, ISQ_DDIV(c, lamr));
+  const double nrq = ISQ_DMUL(ISQ_DMUL(dn, r), q);
+  int64_t y;
+  while (true) {
+    const double u = ISQ_DMUL(s.random(), p4);
+    double v = s.random();
+    if (!(u > p1)) {  // Step10: the triangular region, accepted
+      y = (int64_t)floor(ISQ_DADD(ISQ_DSUB(xm, ISQ_DMUL(p1, v)), u));
+      break;
+    }
+    if (!(u > p2)) {  // Step20: parallelograms
+      const double x = ISQ_DADD(xl, ISQ_DDIV(ISQ_DSUB(u, p1), c));
+      v = ISQ_DSUB(ISQ_DADD(ISQ_DMUL(v, c), 1.0), ISQ_DDIV(fabs(ISQ_DADD(ISQ_DSUB(dm, x), 0.5)), p1));
+      if (v > 1.0) continue;
+      y = (int64_t)floor(x);
+    } else if (!(u > p3)) {  // Step30: left exponential tail
+      y = (int64_t)floor(ISQ_DADD(xl, ISQ_DDIV(log(v), laml)));
+      if (y < 0 || v == 0.0) continue;
+      v = ISQ_DMUL(ISQ_DMUL(v, ISQ_DSUB(u, p2)), laml);
+    } else {  // Step40: right exponential tail
+      y = (int64_t)floor(ISQ_DSUB(xr, ISQ_DDIV(log(v), lamr)));
+      if (y > n || v == 0.0) continue;
+      v = ISQ_DMUL(ISQ_DMUL(v, ISQ_DSUB(u, p3)), lamr);
+    }
+    // Step50
+    const int64_t k = y > m ? y - m : m - y;
+    const double dk = (double)k;
+    if (!(k > 20 && dk < ISQ_DSUB(ISQ_DDIV(nrq, 2.0), 1.0))) {
+      const double sr = ISQ_DDIV(r, q);
+      const double aa = ISQ_DMUL(sr, (double)(n + 1));
+      double F = 1.0;
+      if (m < y) {
+        for (int64_t i = m + 1; i <= y; ++i) F = ISQ_DMUL(F, ISQ_DSUB(ISQ_DDIV(aa, (double)i), sr));
+      } else if (m > y) {
+        for (int64_t i = y + 1; i <= m; ++i) F = ISQ_DDIV(F, ISQ_DSUB(ISQ_DDIV(aa, (double)i), sr));
+      }
+      if (v > F) continue;
+      break;
+    }
+    // Step52: squeeze on log(v), then the Stirling-corrected bound
+    const double rho = ISQ_DMUL(ISQ_DDIV(dk, nrq),
+                                ISQ_DADD(ISQ_DDIV(ISQ_DADD(ISQ_DMUL(dk, ISQ_DADD(ISQ_DDIV(dk, 3.0), 0.625)),
+                                                           0.16666666666666666),
+                                                  nrq),
+                                         0.5));
+    const double t = ISQ_DDIV((double)(-k * k), ISQ_DMUL(2.0, nrq));
+    const double A = log(v);
+    if (A < ISQ_DSUB(t, rho)) break;
+    if (A > ISQ_DADD(t, rho)) continue;
+    const double x1 = (double)(y + 1), f1 = (double)(m + 1), z = (double)(n + 1 - m), w = (double)(n - y + 1);
+    const double x2 = ISQ_DMUL(x1, x1), f2 = ISQ_DMUL(f1, f1), z2 = ISQ_DMUL(z, z), w2 = ISQ_DMUL(w, w);
+    auto stirling = [](double v1, double v2) {  // (13680 - (462 - (132 - (99 - 140/v2)/v2)/v2)/v2)/v1/166320
+      const double i4 = ISQ_DDIV(ISQ_DSUB(99.0, ISQ_DDIV(140.0, v2)), v2);
+      const double i3 = ISQ_DDIV(ISQ_DSUB(132.0, i4), v2);
+      const double i2 = ISQ_DDIV(ISQ_DSUB(462.0, i3), v2);
+      return ISQ_DDIV(ISQ_DDIV(ISQ_DSUB(13680.0, i2), v1), 166320.0);
+    };
+    double bound = ISQ_DMUL(xm, log(ISQ_DDIV(f1, x1)));
+    bound = ISQ_DADD(bound, ISQ_DMUL(ISQ_DADD((double)(n - m), 0.5), log(ISQ_DDIV(z, w))));
+    bound = ISQ_DADD(bound, ISQ_DMUL((double)(y - m), log(ISQ_DDIV(ISQ_DMUL(w, r), ISQ_DMUL(x1, q)))));
+    bound = ISQ_DADD(bound, stirling(f1, f2));
+    bound = ISQ_DADD(bound, stirling(z, z2));
+    bound = ISQ_DADD(bound, stirling(x1, x2));
+    bound = ISQ_DADD(bound, stirling(w, w2));
+    if (A > bound) continue;
+    break;
+  }
+  if (p > 0.5) y = n - y;  // Step60
+  return y;
+}
+
+// numpy random_binomial: inversion for n * min(p, 1-p) <= 30, BTPE above
+// (any n_meas).  `ok` is kept for callers that report a failed draw.
 __device__ __forceinline__ int64_t binomial(NpStream& s, double p, int64_t n, bool* ok) {
+  (void)ok;
   if (n == 0 || p == 0.0) return 0;
   if (p <= 0.5) {
     if (ISQ_DMUL(p, (double)n) <= 30.0) return binomial_inversion(s, n, p);
-    *ok = false;
-    return 0;
+    return binomial_btpe(s, n, p);
   }
   const double q = ISQ_DSUB(1.0, p);
   if (ISQ_DMUL(q, (double)n) <= 30.0) return n - binomial_inversion(s, n, q);
-  *ok = false;
-  return 0;
+  return n - binomial_btpe(s, n, q);
 }
 
 // numpy |z| for complex128 (SIMD loop, loops_unary_complex.dispatch.c.src):

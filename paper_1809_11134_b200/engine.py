@@ -13,7 +13,8 @@ Differences from the reference, by design:
   * the initial bank is drawn on the device from per-slot streams (θ uniform,
     Box-Muller qutrits) unless `population=` injects one (e.g. the reference's
     own init_population output);
-  * numberOfWires is limited to 2..5 and nMeas to <= 60 (ConfigurationError).
+  * numberOfWires is limited to 2..5 (ConfigurationError); any nMeas >= 1
+    (numpy's inversion and BTPE binomial branches are both reproduced).
 """
 from __future__ import annotations
 

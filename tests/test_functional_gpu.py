@@ -65,7 +65,7 @@ def test_sample_circuit_bounds_and_positions():
         assert all(0 <= f < cfg.qubit_count for f in bp)
 
 
-@pytest.mark.parametrize("n_meas", [1, 3, 11])
+@pytest.mark.parametrize("n_meas", [1, 3, 11, 61, 100, 1000])
 def test_construct_segments_matches_reference_goldens(n_meas):
     from paper_1809_11134_b200 import CounterStreams, PopulationConfig, PopulationState, construct_segments
     from paper_1809_11134_b200.gates import enumerate_templates

@@ -59,7 +59,7 @@ def test_oracle_sampling_matches_reference():
 
 def test_oracle_measurement_matches_reference():
     g = golden("measure")
-    for nm in (1, 3, 11):
+    for nm in (1, 3, 11, 61, 100, 1000):
         q = g[f"nm{nm}_qutrits"]
         for gen in (0, 9):
             axes = O.measure_axes(q, nm, 11, gen, np.arange(q.shape[0]))
@@ -175,3 +175,23 @@ def test_exp_log_identity_on_binomial_q():
     qs = [1.0 - 0.5 * rng.random() for _ in range(200_000)]
     qs += [step(0.5, k) for k in range(50_000)] + [step(1.0, -k) for k in range(50_000)] + [0.5, 1.0]
     assert all(math.exp(1.0 * math.log(q)) == q for q in qs)
+
+
+def test_binomial_restatement_matches_numpy():
+    """oracle/binomial.py (inversion + BTPE, the device's transcription source)
+    against numpy's own Generator draws on Philox streams, including the BTPE
+    branch (n * min(p, 1 - p) > 30) that nMeas > 60 reaches."""
+    from oracle.binomial import binomial, multinomial3
+    from oracle.streams import stream
+
+    rng = np.random.default_rng(1)
+    for trial in range(3000):
+        n = int(rng.choice([61, 100, 257, 1000, 100000]))
+        p = float(rng.uniform(0.01, 0.99))
+        assert stream(7, 2, trial, 0).binomial(n, p) == binomial(stream(7, 2, trial, 0), p, n)
+    for trial in range(3000):
+        n = int(rng.choice([1, 11, 61, 100, 1000]))
+        q = rng.normal(size=3) + 1j * rng.normal(size=3)
+        pr = np.abs(q) ** 2
+        pr /= pr.sum()
+        assert list(stream(7, 2, trial, 1).multinomial(n, pr)) == multinomial3(stream(7, 2, trial, 1), n, list(pr))

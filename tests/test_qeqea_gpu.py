@@ -161,8 +161,11 @@ def test_errors_and_echo():
     with pytest.raises(ConfigurationError):
         PopulationConfig(number_of_wires=1, size_of_individual=3, size_of_population=4)
     with pytest.raises(ConfigurationError):
-        QeqeaEngine(PopulationConfig(number_of_wires=2, size_of_individual=3, size_of_population=4,
-                                     n_meas=61), target_matrix("CNOT"), seed=1)
+        PopulationConfig(number_of_wires=2, size_of_individual=3, size_of_population=4, n_meas=0)
+    # nMeas > 60 reaches numpy's BTPE binomial branch, reproduced on the device
+    big = QeqeaEngine(PopulationConfig(number_of_wires=2, size_of_individual=3, size_of_population=4,
+                                       n_meas=1000), target_matrix("CNOT"), seed=1)
+    assert big.steps(5).size == 5
     e = QeqeaEngine(cfg, target_matrix("CNOT"), seed=0, workers=2)
     echo = e.config_echo()
     assert echo["sizeOfIndividual"] == 3 and echo["workers"] == 2
@@ -248,7 +251,7 @@ def test_handles_release_their_device_memory():
     assert abs(free1 - free0) < 64 << 20, (free0, free1)
 
 
-@pytest.mark.parametrize("n_meas", [1, 3, 11])
+@pytest.mark.parametrize("n_meas", [1, 3, 11, 61, 1000])
 def test_device_measurement_matches_reference_goldens(n_meas):
     """construct_segments on the device (Born probabilities, multinomial by
     binomial inversion, argmax) against the reference's own measurements
