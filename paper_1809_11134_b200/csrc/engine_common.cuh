@@ -7,7 +7,6 @@
 //
 //   rot[Qt]     64 B  {q0, q1, q2 (complex), theta, slot_max}   rotation region
 //   inter[Q-Qt] 16 B  {theta, slot_max}                          interaction region
-//   claim[Q]     4 B  commit arbitration stamp (generation + 1)
 //
 // slot_max is SegmentFitnessTable.slot_max (engine.py:202-222), updated with a
 // 64-bit atomicMax (fitness >= 0, so integer order == double order).  The host
@@ -38,6 +37,7 @@ struct QeqeaDevState {
   int32_t improved;      // best improved in the generation being finished
   double gen_best, gen_mean;
   unsigned long long fit_next;  // next circuit batch of the fitness launch (dynamic scheduling)
+  unsigned long long qlive_next;  // qutrit-mutated touches of this generation so far (qlive fill)
 };
 
 struct GenRecord {
@@ -114,7 +114,6 @@ struct QeqeaArgs {
   // bank (owned slots, local index, see slot_local)
   RotRec* rot;     // Qtloc records
   IntRec* inter;   // Qloc - Qtloc records
-  uint32_t* claim; // Qloc
   // circuit side (this rank's S circuits x L positions)
   double* fitness;       // world * S: the whole (gathered) fitness vector
   uint32_t* flats;       // S * L sampled slots
@@ -125,7 +124,9 @@ struct QeqeaArgs {
   uint8_t* owner_codes;     // their gate codes / live angles (sent back to the circuit ranks)
   double* owner_thetas;
   double* touch_fbefore;    // slot_max each touch started the generation from
-  uint8_t* touch_mutated;   // bit 0 pending mutation, bit 1 it is a qutrit mutation
+  uint32_t* touch_info;     // bit 0 pending mutation, bit 1 qutrit mutation, bits 2.. its qlive index
+  double2* qlive;           // live qutrits of this generation's qutrit-mutated touches (values kernel,
+                            // compacted; the commit stores them without re-deriving them)
   // world > 1 exchange buffers (send side of flats, receive side of codes / angles)
   uint32_t* send_flats;     // S * L, grouped by owner
   uint8_t* recv_codes;      // S * L, grouped by owner

@@ -136,6 +136,7 @@ struct ValuesShared {
   uint16_t task[kValTile];  // rotation touches to measure
   uint16_t qq[kValTile];    // of which with a pending qutrit mutation
   int ntask, nq;
+  unsigned long long qbase;  // the tile's first qlive entry
 };
 
 // Gate code / live angle of owned touch t, to the owner-side arrays and, with
@@ -176,7 +177,7 @@ __device__ __forceinline__ bool value_touch_from(const QeqeaArgs& a, int64_t t, 
     emit_code(a, t, 0);
     emit_theta(a, t, 0.0);
     a.touch_fbefore[t] = 2.0;
-    a.touch_mutated[t] = 0;
+    a.touch_info[t] = 0;
     return false;
   }
   const double f = load_committed(a, slot_local(a, s), v);
@@ -184,7 +185,7 @@ __device__ __forceinline__ bool value_touch_from(const QeqeaArgs& a, int64_t t, 
   if (m != MUT_QUTRIT) which = -1;
   emit_theta(a, t, v.theta);
   a.touch_fbefore[t] = f;
-  a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
+  a.touch_info[t] = (m != MUT_NONE ? 1u : 0u) | (m == MUT_QUTRIT ? 2u : 0u);  // + qlive index: caller
   const int64_t kind = slot_kind(a, s);
   if (kind < a.n) return true;
   emit_code(a, t, (uint8_t)(3 * a.n + (kind - a.n)));
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
         emit_code(a, t, 0);
         emit_theta(a, t, 0.0);
         a.touch_fbefore[t] = 2.0;
-        a.touch_mutated[t] = 0;
+        a.touch_info[t] = 0;
         continue;
       }
       const int64_t kind = slot_kind(a, s);
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
 #endif
       emit_theta(a, t, v.theta);
       a.touch_fbefore[t] = f;
-      a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
+      if (m != MUT_QUTRIT) a.touch_info[t] = m != MUT_NONE ? 1u : 0u;  // qutrit touches: below, with their index
       if (kind < a.n) {
         sm.task[atomicAdd(&sm.ntask, 1)] = (uint16_t)i;
         if (m == MUT_QUTRIT) {
@@ -304,9 +305,16 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) sm.qbase = sm.nq ? atomicAdd(&a.st->qlive_next, (unsigned long long)sm.nq) : 0ULL;
+    __syncthreads();
     for (int j = threadIdx.x; j < sm.nq; j += kValThreads) {
       const int i = sm.qq[j];
       su3_one_param(sm.which[i], sm.value[i], sm.rec[i].q);
+      // the live qutrit for the commit (every touch of the slot holds the same value)
+      const unsigned long long qi = sm.qbase + (unsigned long long)j;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) a.qlive[3 * qi + k] = sm.rec[i].q[k];
+      a.touch_info[base + i] = 3u | ((uint32_t)qi << 2);
     }
     __syncthreads();
     for (int k = threadIdx.x; k < sm.ntask; k += kValThreads) {
@@ -514,15 +522,17 @@ __device__ __forceinline__ void commit_touch(const QeqeaArgs& a, int64_t t, uint
   if (!(fit > fb)) return;
   const uint32_t s = a.owner_flats[t];
   const int64_t loc = slot_local(a, s);
-  const uint8_t mf = a.touch_mutated[t];
+  const uint32_t mf = a.touch_info[t];
   if (mf & 2) {
-    // qutrit mutation: one improving touch per slot recomputes and writes it
-    if (atomicMax(&a.claim[loc], (uint32_t)(g + 1)) < (uint32_t)(g + 1)) {
-      LiveSlot v;
-      load_committed(a, loc, v);  // commit writes only theta / qutrit, never slot_max
-      mutate_slot(a, s, g - 1, fb, v);
-      store_committed(a, loc, v);
-    }
+    // qutrit mutation: the live qutrit the values kernel derived (the same
+    // value in every touch of the slot, so concurrent stores agree); theta
+    // is unchanged by a qutrit mutation (encoding.py:119-132)
+    const double2* q = a.qlive + 3 * (uint64_t)(mf >> 2);
+    double2* r = a.rot[loc].q;
+    const double2 q0 = q[0], q1 = q[1], q2 = q[2];
+    r[0] = q0;
+    r[1] = q1;
+    r[2] = q2;
   } else if (mf & 1) {
     // angle mutation: every improving touch holds the same live angle
     // (values kernel), so the idempotent store needs no arbitration
@@ -545,6 +555,7 @@ __global__ void __launch_bounds__(kCommitThreads) qeqea_commit_table_kernel(Qeqe
 
 __device__ __forceinline__ void advance_body(const QeqeaArgs& a) {
   QeqeaDevState* st = a.st;
+  st->qlive_next = 0;  // the next generation's values kernel refills qlive
   st->generation += 1;
   if (st->best_fitness >= a.target_fitness)
     st->stop = 1;
@@ -568,7 +579,6 @@ __global__ void qeqea_init_kernel(QeqeaArgs a) {
     double theta;
     double2 q[3];
     init_slot_value(a.seed, s, loc < a.Qtloc, theta, q);
-    a.claim[loc] = 0;
     if (loc >= a.Qtloc) {
       a.inter[loc - a.Qtloc].theta = theta;
       a.inter[loc - a.Qtloc].smax = 0.0;
@@ -626,7 +636,6 @@ __global__ void qeqea_unpack_kernel(QeqeaArgs a, const double* theta, const doub
     }
     store_committed(a, loc, v);
     *smax_ptr(a, loc) = smax ? smax[loc] : 0.0;
-    a.claim[loc] = 0;
   }
 }
 
@@ -693,7 +702,13 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
       int which;
       double value;
       if (value_touch_from(a, t, g, s, v, which, value)) {
-        if (which >= 0) su3_one_param(which, value, v.q);
+        if (which >= 0) {
+          su3_one_param(which, value, v.q);
+          const unsigned long long qi = atomicAdd(&a.st->qlive_next, 1ULL);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) a.qlive[3 * qi + k] = v.q[k];
+          a.touch_info[t] = 3u | ((uint32_t)qi << 2);
+        }
         double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
         double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
         emit_code(a, t, measure_code_on(a, s, ms, re, im));

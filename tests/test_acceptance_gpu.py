@@ -61,3 +61,36 @@ def test_criterion_3_ga_beats_qeqea_on_toffoli():
     qe = [_run(QeqeaEngine(PopulationConfig(3, 16, 5, max_generations=20_000), t, s))[0] for s in SEEDS]
     assert statistics.median(ga) >= statistics.median(qe)
     assert 0.40 < statistics.median(qe) < 0.55  # the reference's plateau (README: 0.45-0.52)
+
+
+@pytest.mark.parametrize("kind", ["c3_ga_toffoli", "c3_qeqea_toffoli", "c12_qeqea_CCCNOT_2000",
+                                  "c12_qeqea_Peres_2000", "c12_ga_Peres_1000"])
+def test_outcome_distributions_match_the_reference_over_40_seeds(kind):
+    """Criteria 3 (Toffoli, 20k generations) and 12 (smoke runs) as
+    distributions of the best fitness over seeds 1..40, against the
+    reference's own engines run on the same configurations and seeds
+    (tests/golden/acceptance_outcomes_reference.json, written by
+    oracle/gen_acceptance_outcomes.py): a two-sided Mann-Whitney U test must
+    not reject equality at the 1 % level."""
+    import json
+    from pathlib import Path
+
+    from scipy.stats import mannwhitneyu
+
+    from paper_1809_11134_b200 import GaConfig, GaEngine, PopulationConfig, QeqeaEngine, target_matrix
+
+    ref = json.loads((Path(__file__).parent / "golden" / "acceptance_outcomes_reference.json").read_text())
+    seeds = range(1, ref["seeds"] + 1)
+    if kind.startswith("c3"):
+        t = target_matrix("Toffoli")
+        make = ((lambda s: GaEngine(GaConfig(3, 16, 50, max_generations=20_000), t, s)) if "ga" in kind else
+                (lambda s: QeqeaEngine(PopulationConfig(3, 16, 5, max_generations=20_000), t, s)))
+    else:
+        _, algo, name, gens = kind.split("_")
+        spec = target_matrix(name)
+        make = ((lambda s: QeqeaEngine(PopulationConfig(spec.number_of_wires, 16, 5, max_generations=int(gens)),
+                                       spec, s)) if algo == "qeqea" else
+                (lambda s: GaEngine(GaConfig(spec.number_of_wires, 16, 20, max_generations=int(gens)), spec, s)))
+    device = [_run(make(s))[0] for s in seeds]
+    reference = [ref[kind][str(s)] for s in seeds]
+    assert mannwhitneyu(device, reference).pvalue > 0.01, (statistics.median(device), statistics.median(reference))
