@@ -38,7 +38,7 @@ static void free_handle(QeqeaHandle* h) {
   QeqeaArgs& a = h->a;
   const bool sharded = a.world > 1;
   void* bufs[] = {a.rot, a.inter, a.qlive, a.fitness, a.flats, a.gate_codes, a.gate_thetas,
-                  a.touch_fbefore, a.touch_info, a.st, a.records, a.best_codes, a.best_thetas,
+                  a.touch_fbefore, a.touch_mutated, a.st, a.records, a.best_codes, a.best_thetas,
                   (void*)a.target, a.part_max, a.part_sum, a.part_arg, a.send_flats, a.recv_codes,
                   a.recv_thetas, a.elite};
   for (void* b : bufs) cudaFree(b);
@@ -84,10 +84,6 @@ static isq_status validate(const isq_qeqea_config* c) {
   const int64_t Q = K * c->size_of_population * c->size_of_individual;
   if (Q >= (1LL << 32) - 1) {
     set_error("qubit_count = K*P*L must stay below 2^32 for the device engine");
-    return ISQ_ERR_UNSUPPORTED;
-  }
-  if (c->size_of_population * c->size_of_individual >= (1LL << 30)) {
-    set_error("sizeOfPopulation * sizeOfIndividual must stay below 2^30 for the device engine");
     return ISQ_ERR_UNSUPPORTED;
   }
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad("invalid rank/world");
@@ -179,8 +175,8 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   TRYA(cudaMalloc((void**)&a.gate_codes, nc));
   TRYA(cudaMalloc((void**)&a.gate_thetas, nc * 8));
   TRYA(cudaMalloc((void**)&a.touch_fbefore, no * 8));
-  TRYA(cudaMalloc((void**)&a.touch_info, no * 4));
-  TRYA(cudaMalloc((void**)&a.qlive, no * 48));  // worst case: every owned touch qutrit-mutated
+  TRYA(cudaMalloc((void**)&a.touch_mutated, no));
+  TRYA(cudaMalloc((void**)&a.qlive, no * 48));
   if (a.world > 1) {
     TRYA(cudaMalloc((void**)&a.owner_flats, no * 4));
     TRYA(cudaMalloc((void**)&a.owner_codes, no));

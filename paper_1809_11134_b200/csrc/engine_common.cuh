@@ -37,7 +37,6 @@ struct QeqeaDevState {
   int32_t improved;      // best improved in the generation being finished
   double gen_best, gen_mean;
   unsigned long long fit_next;  // next circuit batch of the fitness launch (dynamic scheduling)
-  unsigned long long qlive_next;  // qutrit-mutated touches of this generation so far (qlive fill)
 };
 
 struct GenRecord {
@@ -124,9 +123,9 @@ struct QeqeaArgs {
   uint8_t* owner_codes;     // their gate codes / live angles (sent back to the circuit ranks)
   double* owner_thetas;
   double* touch_fbefore;    // slot_max each touch started the generation from
-  uint32_t* touch_info;     // bit 0 pending mutation, bit 1 qutrit mutation, bits 2.. its qlive index
-  double2* qlive;           // live qutrits of this generation's qutrit-mutated touches (values kernel,
-                            // compacted; the commit stores them without re-deriving them)
+  uint8_t* touch_mutated;   // bit 0 pending mutation, bit 1 it is a qutrit mutation
+  double2* qlive;           // 3 per owned touch: the live qutrit of a qutrit-mutated touch (values
+                            // kernel), so the commit stores it without re-deriving it
   // world > 1 exchange buffers (send side of flats, receive side of codes / angles)
   uint32_t* send_flats;     // S * L, grouped by owner
   uint8_t* recv_codes;      // S * L, grouped by owner

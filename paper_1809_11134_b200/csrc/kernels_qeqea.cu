@@ -136,7 +136,6 @@ struct ValuesShared {
   uint16_t task[kValTile];  // rotation touches to measure
   uint16_t qq[kValTile];    // of which with a pending qutrit mutation
   int ntask, nq;
-  unsigned long long qbase;  // the tile's first qlive entry
 };
 
 // Gate code / live angle of owned touch t, to the owner-side arrays and, with
@@ -177,7 +176,7 @@ __device__ __forceinline__ bool value_touch_from(const QeqeaArgs& a, int64_t t, 
     emit_code(a, t, 0);
     emit_theta(a, t, 0.0);
     a.touch_fbefore[t] = 2.0;
-    a.touch_info[t] = 0;
+    a.touch_mutated[t] = 0;
     return false;
   }
   const double f = load_committed(a, slot_local(a, s), v);
@@ -185,7 +184,7 @@ __device__ __forceinline__ bool value_touch_from(const QeqeaArgs& a, int64_t t, 
   if (m != MUT_QUTRIT) which = -1;
   emit_theta(a, t, v.theta);
   a.touch_fbefore[t] = f;
-  a.touch_info[t] = (m != MUT_NONE ? 1u : 0u) | (m == MUT_QUTRIT ? 2u : 0u);  // + qlive index: caller
+  a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
   const int64_t kind = slot_kind(a, s);
   if (kind < a.n) return true;
   emit_code(a, t, (uint8_t)(3 * a.n + (kind - a.n)));
@@ -200,17 +199,19 @@ __device__ __forceinline__ bool value_touch_head(const QeqeaArgs& a, int64_t t, 
 
 // construct_segments for one rotation slot (engine.py:167-170): Born
 // measurement on the slot's (generation, slot) stream -> gate code.
+template <bool kBTPE = true>
 __device__ __forceinline__ uint8_t measure_code_on(const QeqeaArgs& a, uint32_t s, NpStream& st, double re[3],
                                                    double im[3]) {
   bool ok = true;
-  const int axis = measure_axis(re, im, a.n_meas, st, &ok);
+  const int axis = measure_axis<kBTPE>(re, im, a.n_meas, st, &ok);
   return (uint8_t)(3 * (slot_kind(a, s)) + axis);
 }
+template <bool kBTPE = true>
 __device__ __forceinline__ uint8_t measure_code(const QeqeaArgs& a, uint32_t s, uint64_t g, double re[3],
                                                 double im[3]) {
   NpStream st;
   st.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);
-  return measure_code_on(a, s, st, re, im);
+  return measure_code_on<kBTPE>(a, s, st, re, im);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -223,6 +224,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // mutations, rotation touches queued; (2) the queued qutrit mutations (5 % of
 // touches) on full warps; (3) the Born measurements of the queued rotation
 // touches on full warps.
+// BIG: n_meas > kInversionMaxMeas (the BTPE binomial branch compiled in).
+template <bool BIG>
 __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, int64_t t1) {
   extern __shared__ __align__(64) unsigned char val_smem[];
   ValuesShared& sm = *reinterpret_cast<ValuesShared*>(val_smem);
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
         emit_code(a, t, 0);
         emit_theta(a, t, 0.0);
         a.touch_fbefore[t] = 2.0;
-        a.touch_info[t] = 0;
+        a.touch_mutated[t] = 0;
         continue;
       }
       const int64_t kind = slot_kind(a, s);
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
 #endif
       emit_theta(a, t, v.theta);
       a.touch_fbefore[t] = f;
-      if (m != MUT_QUTRIT) a.touch_info[t] = m != MUT_NONE ? 1u : 0u;  // qutrit touches: below, with their index
+      a.touch_mutated[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
       if (kind < a.n) {
         sm.task[atomicAdd(&sm.ntask, 1)] = (uint16_t)i;
         if (m == MUT_QUTRIT) {
@@ -305,16 +308,12 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) sm.qbase = sm.nq ? atomicAdd(&a.st->qlive_next, (unsigned long long)sm.nq) : 0ULL;
-    __syncthreads();
     for (int j = threadIdx.x; j < sm.nq; j += kValThreads) {
       const int i = sm.qq[j];
       su3_one_param(sm.which[i], sm.value[i], sm.rec[i].q);
       // the live qutrit for the commit (every touch of the slot holds the same value)
-      const unsigned long long qi = sm.qbase + (unsigned long long)j;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) a.qlive[3 * qi + k] = sm.rec[i].q[k];
-      a.touch_info[base + i] = 3u | ((uint32_t)qi << 2);
+      for (int k = 0; k < 3; ++k) a.qlive[3 * (base + i) + k] = sm.rec[i].q[k];
     }
     __syncthreads();
     for (int k = threadIdx.x; k < sm.ntask; k += kValThreads) {
@@ -322,7 +321,7 @@ __global__ void __launch_bounds__(kValThreads) qeqea_values_kernel(QeqeaArgs a, 
       const double2* q = sm.rec[i].q;
       double re[3] = {q[0].x, q[1].x, q[2].x};
       double im[3] = {q[0].y, q[1].y, q[2].y};
-      emit_code(a, base + i, measure_code(a, sm.s[i], g, re, im));
+      emit_code(a, base + i, measure_code<BIG>(a, sm.s[i], g, re, im));
     }
     __syncthreads();
   }
@@ -522,12 +521,12 @@ __device__ __forceinline__ void commit_touch(const QeqeaArgs& a, int64_t t, uint
   if (!(fit > fb)) return;
   const uint32_t s = a.owner_flats[t];
   const int64_t loc = slot_local(a, s);
-  const uint32_t mf = a.touch_info[t];
+  const uint8_t mf = a.touch_mutated[t];
   if (mf & 2) {
     // qutrit mutation: the live qutrit the values kernel derived (the same
     // value in every touch of the slot, so concurrent stores agree); theta
     // is unchanged by a qutrit mutation (encoding.py:119-132)
-    const double2* q = a.qlive + 3 * (uint64_t)(mf >> 2);
+    const double2* q = a.qlive + 3 * t;
     double2* r = a.rot[loc].q;
     const double2 q0 = q[0], q1 = q[1], q2 = q[2];
     r[0] = q0;
@@ -555,7 +554,6 @@ __global__ void __launch_bounds__(kCommitThreads) qeqea_commit_table_kernel(Qeqe
 
 __device__ __forceinline__ void advance_body(const QeqeaArgs& a) {
   QeqeaDevState* st = a.st;
-  st->qlive_next = 0;  // the next generation's values kernel refills qlive
   st->generation += 1;
   if (st->best_fitness >= a.target_fitness)
     st->stop = 1;
@@ -704,10 +702,8 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
       if (value_touch_from(a, t, g, s, v, which, value)) {
         if (which >= 0) {
           su3_one_param(which, value, v.q);
-          const unsigned long long qi = atomicAdd(&a.st->qlive_next, 1ULL);
 #pragma unroll
-          for (int k = 0; k < 3; ++k) a.qlive[3 * qi + k] = v.q[k];
-          a.touch_info[t] = 3u | ((uint32_t)qi << 2);
+          for (int k = 0; k < 3; ++k) a.qlive[3 * t + k] = v.q[k];
         }
         double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
         double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
@@ -778,7 +774,9 @@ static int blocks_for(int64_t n, int threads) {
 
 isq_status qeqea_configure_device() {
   // > 48 KB of dynamic shared memory needs the opt-in (per device)
-  ISQ_CUDA_TRY(cudaFuncSetAttribute((const void*)qeqea_values_kernel,
+  ISQ_CUDA_TRY(cudaFuncSetAttribute((const void*)qeqea_values_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ValuesShared)));
+  ISQ_CUDA_TRY(cudaFuncSetAttribute((const void*)qeqea_values_kernel<true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(ValuesShared)));
   return ISQ_OK;
 }
@@ -791,9 +789,15 @@ static cudaError_t launch_values(const QeqeaArgs& a, int64_t t1, cudaStream_t s)
   int64_t nb = (t1 + kValTile - 1) / kValTile;
   if (nb > ISQ_VAL_GRID_CAP) nb = ISQ_VAL_GRID_CAP;
   if (nb < 1) nb = 1;
-  qeqea_values_kernel<<<(unsigned)nb, kValThreads, sizeof(ValuesShared), s>>>(a, t1);
+  if (a.n_meas > kInversionMaxMeas)
+    qeqea_values_kernel<true><<<(unsigned)nb, kValThreads, sizeof(ValuesShared), s>>>(a, t1);
+  else
+    qeqea_values_kernel<false><<<(unsigned)nb, kValThreads, sizeof(ValuesShared), s>>>(a, t1);
 #else
-  qeqea_values_kernel<<<blocks_for(t1, kValThreads), kValThreads, sizeof(ValuesShared), s>>>(a, t1);
+  if (a.n_meas > kInversionMaxMeas)
+    qeqea_values_kernel<true><<<blocks_for(t1, kValThreads), kValThreads, sizeof(ValuesShared), s>>>(a, t1);
+  else
+    qeqea_values_kernel<false><<<blocks_for(t1, kValThreads), kValThreads, sizeof(ValuesShared), s>>>(a, t1);
 #endif
   return cudaGetLastError();
 }

@@ -345,19 +345,30 @@ __device__ inline int64_t binomial_btpe(NpStream& s, int64_t n, double p) {
   return y;
 }
 
-// numpy random_binomial: inversion for n * min(p, 1-p) <= 30, BTPE above
-// (any n_meas).  `ok` is kept for callers that report a failed draw.
+// numpy random_binomial: inversion for n * min(p, 1-p) <= 30, BTPE above.
+// kBTPE = false compiles the inversion branch alone, for callers that know
+// n <= 60 (n * min(p, 1 - p) <= 30 always): the BTPE code would otherwise
+// cost the hot values kernel 26 registers and ~0.8 ms per C5 generation.
+template <bool kBTPE = true>
 __device__ __forceinline__ int64_t binomial(NpStream& s, double p, int64_t n, bool* ok) {
   (void)ok;
   if (n == 0 || p == 0.0) return 0;
-  if (p <= 0.5) {
-    if (ISQ_DMUL(p, (double)n) <= 30.0) return binomial_inversion(s, n, p);
-    return binomial_btpe(s, n, p);
+  if constexpr (!kBTPE) {
+    if (p <= 0.5) return binomial_inversion(s, n, p);
+    return n - binomial_inversion(s, n, ISQ_DSUB(1.0, p));
+  } else {
+    if (p <= 0.5) {
+      if (ISQ_DMUL(p, (double)n) <= 30.0) return binomial_inversion(s, n, p);
+      return binomial_btpe(s, n, p);
+    }
+    const double q = ISQ_DSUB(1.0, p);
+    if (ISQ_DMUL(q, (double)n) <= 30.0) return n - binomial_inversion(s, n, q);
+    return n - binomial_btpe(s, n, q);
   }
-  const double q = ISQ_DSUB(1.0, p);
-  if (ISQ_DMUL(q, (double)n) <= 30.0) return n - binomial_inversion(s, n, q);
-  return n - binomial_btpe(s, n, q);
 }
+
+// Largest n_meas whose multinomial draws never reach BTPE.
+constexpr int kInversionMaxMeas = 60;
 
 // numpy |z| for complex128 (SIMD loop, loops_unary_complex.dispatch.c.src):
 // larger * sqrt(fma(ratio, ratio, 1)), ratio = smaller / larger.
@@ -373,6 +384,7 @@ __device__ __forceinline__ double np_cabs(double re, double im) {
 // construct_segments for one qutrit (engine.py:167-170): Born probabilities
 // np.abs(q)**2 normalised by the (left-to-right) row sum, one multinomial
 // draw of n_meas measurements, argmax with ties to the lower axis.
+template <bool kBTPE = true>
 __device__ __forceinline__ int measure_axis(const double qre[3], const double qim[3], int n_meas,
                                             NpStream& s, bool* ok) {
   double pr[3];
@@ -387,11 +399,11 @@ __device__ __forceinline__ int measure_axis(const double qre[3], const double qi
   // random_multinomial with d = 3, written out so nothing is dynamically indexed
   int64_t c0 = 0, c1 = 0, c2 = 0;
   int64_t dn = n_meas;
-  c0 = binomial(s, pr[0], dn, ok);  // pix[0] / remaining_p with remaining_p = 1.0
+  c0 = binomial<kBTPE>(s, pr[0], dn, ok);  // pix[0] / remaining_p with remaining_p = 1.0
   dn -= c0;
   if (dn > 0) {
     const double remaining = __dsub_rn(1.0, pr[0]);
-    c1 = binomial(s, __ddiv_rn(pr[1], remaining), dn, ok);
+    c1 = binomial<kBTPE>(s, __ddiv_rn(pr[1], remaining), dn, ok);
     dn -= c1;
     if (dn > 0) c2 = dn;
   }
