@@ -105,7 +105,10 @@ struct MultiEval {
     }
   }
 
-  // One step of every circuit of the warp: gate k = g CHUNK + q of the chunk.
+  // Lockstep alternative to run_chunk (the latency-bound single-block kernels,
+  // one circuit per warp, where run_chunk's bit alignment is pure overhead):
+  // one step of every circuit of the warp, gate k = g CHUNK + q of the chunk,
+  // the rotation case chosen per group.  Same arithmetic per circuit.
   __device__ __forceinline__ void step(const MultiChunk<NQ, R>& sm, R2* fac, int k, int lane, int j) {
     const int inf = sm.info[k];
     R2 e = sm.e1[k];
@@ -141,15 +144,118 @@ struct MultiEval {
     __syncwarp();
   }
 
-  // |tr(S^dagger T)| of circuit g: sum over its lanes of e^{i phi_j} M[j][j].
-  __device__ __forceinline__ double finish(int j) {
+  // Physical register bit of logical row bit lb (pmap: 4 bits per logical bit).
+  static __device__ __forceinline__ int phys_bit(int pmap, int lb) { return (pmap >> (4 * lb)) & 15; }
+
+  // Exchange physical row bits 0 and B of this lane's column where `doit`:
+  // rows r with bit 0 set and bit B clear trade places with r ^ (1 | 2^B).
+  template <int B>
+  __device__ __forceinline__ void swap_bits(bool doit) {
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      if (!(r & 1) || (r & (1 << B))) continue;
+      const int r2 = r ^ 1 ^ (1 << B);
+      const R a = re[r], b = re[r2], c = im[r], d = im[r2];
+      re[r] = doit ? b : a;
+      re[r2] = doit ? a : b;
+      im[r] = doit ? d : c;
+      im[r2] = doit ? c : d;
+    }
+  }
+
+  // One chunk of every circuit of the warp (gate k = g CHUNK + q, q < nq).
+  // The circuits advance independently, each through its own gate list:
+  // a group first runs its diagonal gates up to its next rotation (they only
+  // touch the pending phase), then every group standing at a rotation
+  // applies it in the same pass.  To make that pass the same code for every
+  // group, each group first moves the rotation's row bit to physical bit 0
+  // (an exchange of register halves, under a per-lane predicate), keeping
+  // the logical -> physical bit map in `pmap`, the logical index of the row
+  // whose phase the lane carries in `lrow`, and moving the phases with the
+  // rows.  A warp then makes max over its circuits of their rotation counts
+  // lifting passes (n = 3, L = 16, 4 circuits: ~7.6) instead of one divergent
+  // case per distinct rotation bit per position (~18), and every pass does the
+  // same arithmetic per row pair as before, so the fitness is bit-identical.
+  __device__ __forceinline__ void run_chunk(const MultiChunk<NQ, R>& sm, R2* fac, int kb, int nq, int lane, int j,
+                                            int& pmap, int& lrow) {
+    const int gbase = lane & ~(D - 1);
+    int qg = 0;  // this circuit's next step (uniform within the group)
+    while (true) {
+      int inf = qg < nq ? sm.info[kb + qg] : GT_DIAG;
+      while (qg < nq && inf == GT_DIAG) {  // diagonal run: the pending phase only
+        R2 e = sm.e1[kb + qg];
+        e.y = flip_sign_bit(e.y, sm.rpar[kb + qg] << (31 - lrow));
+        const R t = wr * e.y;
+        wr = fma(wr, e.x, -wi * e.y);
+        wi = fma(wi, e.x, t);
+        ++qg;
+        inf = qg < nq ? sm.info[kb + qg] : GT_DIAG;
+      }
+      const bool pending = qg < nq;
+      if (!__any_sync(0xffffffffu, pending)) break;
+      // align: the rotation's row bit to physical bit 0
+      const int lb = inf >> 8;
+      const int pb = pending ? phys_bit(pmap, lb) : 0;
+#pragma unroll
+      for (int b = 1; b < NQ; ++b) {
+        const bool doit = pb == b;
+        if (!__any_sync(0xffffffffu, doit)) continue;
+        switch (b) {
+          case 1: swap_bits<1>(doit); break;
+          case 2: if constexpr (NQ > 2) swap_bits<2>(doit); break;
+          case 3: if constexpr (NQ > 3) swap_bits<3>(doit); break;
+          default: break;
+        }
+        // the phases and logical labels move with their rows
+        const bool moved = doit && (((j ^ (j >> b)) & 1) != 0);  // bits 0 and b of row j differ
+        const int src = gbase + (moved ? j ^ 1 ^ (1 << b) : j);
+        wr = __shfl_sync(0xffffffffu, wr, src);
+        wi = __shfl_sync(0xffffffffu, wi, src);
+        lrow = __shfl_sync(0xffffffffu, lrow, src);
+        if (doit) {  // logical bit at physical 0 <-> logical bit lb (at physical b)
+          int l0 = 0;
+#pragma unroll
+          for (int x = 0; x < NQ; ++x)
+            if (phys_bit(pmap, x) == 0) l0 = x;
+          pmap = (pmap & ~(15 << (4 * l0)) & ~(15 << (4 * lb))) | (b << (4 * l0));
+        }
+      }
+      // rotation on physical bit 0: rows with it set take w_r conj(w_{r^1})
+      // (times -i for Ry: S^dagger) and carry their partner's phase (times i)
+      const bool ry = (inf & 3) == GT_RY;
+      const R orr = __shfl_xor_sync(0xffffffffu, ry ? -wi : wr, 1);
+      const R ori = __shfl_xor_sync(0xffffffffu, ry ? wr : wi, 1);
+      R2 e = Cplx<R>::make(R(0), R(0));
+      if (pending) {
+        fac[lane] = Cplx<R>::make(fma(wr, orr, wi * ori), fma(wi, orr, -wr * ori));
+        if (j & 1) {
+          wr = orr;
+          wi = ori;
+        }
+        e = sm.e1[kb + qg];
+        ++qg;
+      }
+      __syncwarp();
+      if (pending) flush_lift<0>(fac + gbase, e.x, e.y);
+      __syncwarp();
+    }
+  }
+
+  // |tr(S^dagger T)| of circuit g: sum over its lanes (columns j) of
+  // e^{i phi} M[j][j], the diagonal entry sitting in physical row pj.
+  __device__ __forceinline__ double finish(int lane, int j, int pmap) {
+    int pj = 0;
+#pragma unroll
+    for (int lb = 0; lb < NQ; ++lb) pj |= ((j >> lb) & 1) << phys_bit(pmap, lb);
     R xr = re[0], xi = im[0];
 #pragma unroll
     for (int r = 1; r < D; ++r) {
-      xr = sel(j == r, re[r], xr);
-      xi = sel(j == r, im[r], xi);
+      xr = sel(pj == r, re[r], xr);
+      xi = sel(pj == r, im[r], xi);
     }
-    const double wx = wr, wy = wi, dr = xr, di = xi;
+    const int src = (lane & ~(D - 1)) + pj;  // the lane carrying physical row pj's phase
+    const double wx = __shfl_sync(0xffffffffu, wr, src), wy = __shfl_sync(0xffffffffu, wi, src);
+    const double dr = xr, di = xi;
     double ar = fma(wx, dr, -wy * di), ai = fma(wx, di, wy * dr);
 #pragma unroll
     for (int off = D / 2; off >= 1; off >>= 1) {
@@ -174,7 +280,7 @@ __device__ __forceinline__ unsigned range_mask(int lo, int hi) {
 // groups g >= cpw idle.  A circuit's arithmetic does not depend on cpw, so the
 // latency-bound single-block kernels run fewer circuits per warp (more warps,
 // fewer serialised rotation cases per step) with bit-identical results.
-template <int NQ, class R = double>
+template <int NQ, class R = double, bool kLockstep = false>
 __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const uint8_t* __restrict__ codes,
                                                    const double* __restrict__ thetas,
                                                    const double2* __restrict__ Ts, MultiChunk<NQ, R>* sh,
@@ -221,6 +327,9 @@ __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const u
     const int64_t cn = dyn ? grab() : c0 + nwarps * cpw;
     MultiEval<NQ, R> ev;
     ev.begin(Ts, j);
+    int pmap = 0, lrow = j;  // identity bit map; lane j carries row j's phase
+#pragma unroll
+    for (int lb = 0; lb < NQ; ++lb) pmap |= lb << (4 * lb);
     bool bad0 = false, bad1 = false;
     for (int nb = 0; nb < L; nb += CHUNK) {
       const int nq = min(CHUNK, L - nb);
@@ -245,14 +354,17 @@ __device__ __forceinline__ void fitness_rows_multi(int64_t count, int L, const u
       load(nc, nnb, lane, code0, th0);
       load(nc, nnb, lane + 32, code1, th1);
       __syncwarp();
-      const int kb = g * CHUNK;
+      if constexpr (kLockstep) {
 #pragma unroll 1
-      for (int q = 0; q < nq; ++q) ev.step(cs, cs.fac, kb + q, lane, j);
+        for (int q = 0; q < nq; ++q) ev.step(cs, cs.fac, g * CHUNK + q, lane, j);
+      } else {
+        ev.run_chunk(cs, cs.fac, g * CHUNK, nq, lane, j, pmap, lrow);
+      }
       __syncwarp();
     }
     // bad codes: NaN fitness for the circuit holding one (ISQ_ERR_CONFIG on host entry points)
     const unsigned badm0 = __ballot_sync(0xffffffffu, bad0), badm1 = __ballot_sync(0xffffffffu, bad1);
-    const double f = ev.finish(j);
+    const double f = ev.finish(lane, j, pmap);
     const int64_t c = c0 + g;
     if (j == 0 && g < cpw && c < count) {
       const bool cbad = ((badm0 & own0) | (badm1 & own1)) != 0;
@@ -283,7 +395,7 @@ __device__ __forceinline__ int small_cpw(int64_t P, int64_t warps) {
   return (int)(c < 1 ? 1 : (c > kFitCPW<NQ> ? kFitCPW<NQ> : c));
 }
 
-template <int NQ, class R = double, int NR = kFitNR>
+template <int NQ, class R = double, int NR = kFitNR, bool kLockstep = false>
 __device__ __forceinline__ void fitness_rows_fast(int64_t count, int L, const uint8_t* __restrict__ codes,
                                                   const double* __restrict__ thetas,
                                                   const double2* __restrict__ Ts, FitScratch<NQ, R, NR>* sh,
@@ -291,7 +403,8 @@ __device__ __forceinline__ void fitness_rows_fast(int64_t count, int L, const ui
                                                   int* bad_code = nullptr, unsigned long long* dyn = nullptr,
                                                   int cpw = kFitCPW<NQ>) {
   if constexpr (kFitMulti<NQ>)
-    fitness_rows_multi<NQ, R>(count, L, codes, thetas, Ts, sh, fitness, warps_per_block, bad_code, dyn, cpw);
+    fitness_rows_multi<NQ, R, kLockstep>(count, L, codes, thetas, Ts, sh, fitness, warps_per_block, bad_code, dyn,
+                                         cpw);
   else
     fitness_rows<NQ, R, NR>(count, L, codes, thetas, Ts, sh, fitness, warps_per_block, bad_code, dyn);
 }

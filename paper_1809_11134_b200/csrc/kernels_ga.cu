@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_small_kernel(GaArgs a, int n_gen
     if (a.st->stop) return;  // uniform: written by thread 0 before the barrier
     const uint64_t g = a.st->generation;
     const int cur = ga_cur(a);
-    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps,
+    fitness_rows_fast<NQ, double, kSmallNR, true>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps,
                                             nullptr, nullptr, small_cpw<NQ>(a.P, kWarps));
     __syncthreads();
     for (int part = 0; part < a.n_parts; ++part) {
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     for (int it = 0; it < n_gens; ++it) {
       const int cur = (int)(g & 1);
       double* fit = (g & 1) ? a.fitness_alt : a.fitness;
-      fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, fit, kWarps,
+      fitness_rows_fast<NQ, double, kSmallNR, true>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, fit, kWarps,
                                               nullptr, nullptr, CPW);
       grid.sync();
       const int64_t t0 = wgene(jl);
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(kGaRed, 1) ga_coop_kernel(GaArgs a, int n_gens
     if (a.st->stop) return;  // uniform across the grid: written before the last grid barrier
     const uint64_t g = a.st->generation;
     const int cur = ga_cur(a);
-    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps,
+    fitness_rows_fast<NQ, double, kSmallNR, true>(a.P, a.L, a.codes[cur], a.thetas[cur], Ts, sh, a.fitness, kWarps,
                                             nullptr, nullptr, CPW);
     grid.sync();
     // this thread's first gene: its draws while block 0 reduces and selects

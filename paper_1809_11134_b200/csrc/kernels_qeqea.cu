@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
       }
     }
     __syncthreads();
-    fitness_rows_fast<NQ, double, kSmallNR>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, a.fitness, kWarps,
+    fitness_rows_fast<NQ, double, kSmallNR, true>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, a.fitness, kWarps,
                                             nullptr, nullptr, small_cpw<NQ>(a.P, kWarps));
     __syncthreads();
     if (a.P <= 32 && a.n_parts == 1) {
