@@ -1,4 +1,5 @@
 // C ABI of libisq: argument validation, host<->device staging, error state.
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -201,6 +202,27 @@ static isq_status fitness_batch_host(int32_t n, int32_t length, int64_t count, c
   return ISQ_OK;
 }
 
+// Persistent per-(device, stream) device counters for the dynamically
+// scheduled fitness launches of isq_fitness_batch_device_ex (8 bytes each,
+// kept for the life of the process); nullptr when allocation fails.
+static unsigned long long* stream_counter(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, unsigned long long*> counters;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(dev, stream);
+  auto it = counters.find(key);
+  if (it != counters.end()) return it->second;
+  unsigned long long* c = nullptr;
+  if (cudaMalloc((void**)&c, sizeof(*c)) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free allocation error
+    return nullptr;
+  }
+  counters[key] = c;
+  return c;
+}
+
 static isq_status check_precision(int32_t precision) {
   if (precision == ISQ_PRECISION_FP64 || precision == ISQ_PRECISION_FP32) return ISQ_OK;
   set_error("precision must be ISQ_PRECISION_FP64 or ISQ_PRECISION_FP32");
@@ -231,14 +253,14 @@ isq_status isq_fitness_batch_device_ex(int32_t n, int32_t length, int64_t count,
   if (st == ISQ_OK) st = check_precision(precision);
   if (st != ISQ_OK) return st;
   if (count <= 0) return ISQ_OK;
-  // the dynamic-scheduling counter of this launch, stream-ordered
+  // the dynamic-scheduling counter of this launch: one persistent counter per
+  // (device, stream), reset in stream order by the launch itself, so
+  // launches on one stream reuse it and concurrent streams never share one;
+  // without it the kernel falls back to a static grid stride
   const cudaStream_t s = (cudaStream_t)stream;
-  unsigned long long* ctr = nullptr;
-  ISQ_CUDA_TRY(cudaMallocAsync((void**)&ctr, sizeof(*ctr), s));
-  st = launch_fitness_batch_stoppable(n, length, count, codes_dev, thetas_dev, target_dev, fitness_dev, nullptr,
-                                      s, 0, precision, nullptr, ctr);
-  cudaFreeAsync(ctr, s);
-  return st;
+  unsigned long long* ctr = stream_counter(s);
+  return launch_fitness_batch_stoppable(n, length, count, codes_dev, thetas_dev, target_dev, fitness_dev, nullptr,
+                                        s, 0, precision, nullptr, ctr);
 }
 
 isq_status isq_fitness_of_unitaries(int64_t dim, int64_t count, const double* unitaries,
