@@ -594,6 +594,8 @@ def run_ours(args):
         out["api_step"] = {"value": P * args.steps / dt, "unit": "evals/s", "ms_per_step": dt * 1e3 / args.steps,
                            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(_lib.GEN_RECORD.itemsize),
                            "path": "QeqeaEngine.step() through the C ABI (isq_qeqea_step), host wall clock"}
+    if world > 1:
+        dist.barrier()  # no rank unmaps / frees exchange buffers a peer may still store into
     eng.close()
     # the fp32 variant of the fitness kernel (include/isq.h ISQ_PRECISION_FP32):
     # a full generation with fp32 fitness, and its error on the e2e circuits
