@@ -313,8 +313,11 @@ def fitness_peak(lib, _lib, local: int, fp64: bool = True) -> float:
 
 
 def side_c4(args, local: int, fp64_peak: float, stream):
-    """BASELINE config 4 (n=4, L=32, P=2^16, C^3NOT): full generations, same
-    timing as the headline line, with the fitness kernel's roofline."""
+    """BASELINE config 4 (n=4, L=32, P=2^16, C^3NOT): full generations through
+    the engine's own steps() in its automatic launch mode for this size (16-
+    generation CUDA graphs), CUDA events on the handle's stream; the phase
+    split and the fitness roofline from a plain-kernel pass of the same
+    generations (DeviceQeqeaOps)."""
     import torch
 
     from paper_1809_11134_b200.distributed import DeviceQeqeaOps
@@ -322,19 +325,34 @@ def side_c4(args, local: int, fp64_peak: float, stream):
     from paper_1809_11134_b200.fitness import target_matrix
 
     c = CONFIGS["c4"]
-    steps, warmup = max(args.steps, 20), max(args.warmup, 3)
+    steps, warmup = max(args.steps, 48), max(args.warmup, 16)
     cfg = PopulationConfig(number_of_wires=c["n"], size_of_individual=c["L"], size_of_population=c["P"],
                            max_generations=10_000_000, target_fitness=1.0)
     eng = QeqeaEngine(cfg, target_matrix("CCCNOT"), seed=2024, device=local, max_batch=steps + warmup + 1)
+    from paper_1809_11134_b200 import _lib
+
+    _lib.check(eng._lib.isq_qeqea_set_stream(eng._handle(), ctypes.c_void_p(stream.cuda_stream)))
+    eng.steps(warmup)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    rec = eng.steps(steps)  # enqueues the generations, then reads their records back
+    end.record(stream)
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    assert rec.size == steps
+    eng.close()
+    eng = QeqeaEngine(cfg, target_matrix("CCCNOT"), seed=2024, device=local, max_batch=steps + warmup + 1)
     with torch.cuda.stream(stream):
         ops = DeviceQeqeaOps(eng)
-        ms, (prep, fit, fin) = time_generations(ops, None, steps, warmup, stream)
+        kms, (prep, fit, fin) = time_generations(ops, None, steps, warmup, stream)
     eng.close()
     achieved = canonical_flops(c["n"], c["L"]) * c["P"] / (fit * 1e-3) / 1e12
     return {"workload": c["workload"], "steps": steps, "warmup": warmup,
             "value": c["P"] * steps / (ms * 1e-3), "unit": "evals/s", "gens_per_s": steps / (ms * 1e-3),
-            "ms_per_step": ms / steps,
-            "phase_ms": {"prepare": prep, "score (fitness kernel)": fit, "finish": fin},
+            "ms_per_step": ms / steps, "launch": "engine steps(), automatic mode (16-generation CUDA graphs)",
+            "plain_kernels_ms_per_step": kms / steps,
+            "phase_ms (plain kernels)": {"prepare": prep, "score (fitness kernel)": fit, "finish": fin},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": achieved / fp64_peak, "kernel": kernel_name(c["n"]),
                          "work": "canonical F(4,32) = 51,200 flop/eval x 65,536 circuits per launch"},

@@ -9,5 +9,6 @@ while [ $# -ge 2 ]; do
   mkdir -p build/variants/$name
   ISQ_NVCC_EXTRA="$flags" ISQ_BUILD_DIR=build/variants/$name/obj ISQ_LIBRARY=build/variants/$name/libisq.so \
     python paper_1809_11134_b200/_build.py --force > build/variants/$name/build.log 2>&1 || { cat build/variants/$name/build.log; exit 1; }
+  cp build/variants/$name/obj/ptxas.log build/variants/$name/ptxas.log; rm -rf build/variants/$name/obj
   echo "built $name ($flags)"
 done
