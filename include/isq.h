@@ -40,9 +40,14 @@ typedef int32_t isq_status;
 #define ISQ_ERR_COMM 4
 #define ISQ_ERR_UNSUPPORTED 5
 
-/* Smallest / largest numberOfWires the device kernels are compiled for. */
+/* Smallest / largest numberOfWires the device kernels handle; up to
+ * ISQ_MAX_FAST_WIRES the fitness runs in the register-resident kernels, above
+ * it (fp64 only, no fused single-block launch) in a block-per-circuit kernel
+ * with the 2^n x 2^n state in device scratch.  The reference's cap is
+ * 4^n <= 2^26 (n <= 13, engine.py:43). */
 #define ISQ_MIN_WIRES 2
-#define ISQ_MAX_WIRES 5
+#define ISQ_MAX_FAST_WIRES 5
+#define ISQ_MAX_WIRES 10
 
 const char* isq_last_error(void);
 int32_t isq_abi_version(void);

@@ -25,7 +25,8 @@ ISQ_ERR_COMM = 4
 ISQ_ERR_UNSUPPORTED = 5
 
 MIN_WIRES = 2
-MAX_WIRES = 5
+MAX_WIRES = 10
+MAX_FAST_WIRES = 5
 
 _lock = threading.Lock()
 _lib = None

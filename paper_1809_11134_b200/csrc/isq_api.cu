@@ -79,7 +79,7 @@ struct BatchContext {
   double* target = nullptr;
   int* bad = nullptr;             // device flag: an invalid gate code was seen
   unsigned char* unit = nullptr;  // compose output (not pipelined)
-  size_t cap_rows = 0, cap_len = 0, cap_unit = 0;
+  size_t cap_rows = 0, cap_len = 0, cap_unit = 0, cap_target = 0;
   cudaEvent_t loaded[2], done[2];
   std::mutex mu;
 };
@@ -99,7 +99,6 @@ static BatchContext* batch_context(int device) {
       cudaEventCreateWithFlags(&c->loaded[b], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&c->done[b], cudaEventDisableTiming);
     }
-    cudaMalloc((void**)&c->target, 32 * 32 * 16);
     ctx[device] = c;
   }
   return ctx[device];
@@ -144,9 +143,20 @@ static isq_status fitness_batch_host(int32_t n, int32_t length, int64_t count, c
       ISQ_CUDA_TRY(cudaMalloc((void**)&c->fit[b], c->cap_rows * 8));
     }
   }
+  if ((size_t)(D * D * 16) > c->cap_target) {  // n > 5 targets are up to 1024 x 1024
+    ISQ_CUDA_TRY(cudaStreamSynchronize(c->comp));
+    cudaFree(c->target);
+    c->target = nullptr;
+    c->cap_target = 0;
+    ISQ_CUDA_TRY(cudaMalloc((void**)&c->target, D * D * 16));
+    c->cap_target = (size_t)(D * D * 16);
+  }
   ISQ_CUDA_TRY(cudaMemcpyAsync(c->target, target, D * D * 16, cudaMemcpyHostToDevice, c->copy));
   if (unitary_out) {
-    // composition output (readout path): chunk by chunk, not pipelined
+    // composition output (readout path): chunk by chunk, not pipelined; at
+    // most 256 MB of unitaries per chunk
+    const int64_t per_chunk = ((int64_t)256 << 20) / (D * D * 16);
+    if (chunk > per_chunk) chunk = per_chunk < 1 ? 1 : per_chunk;
     const size_t ub = (size_t)chunk * D * D * 16;
     if (ub > c->cap_unit) {
       cudaFree(c->unit);

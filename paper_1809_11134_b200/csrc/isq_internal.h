@@ -102,6 +102,15 @@ isq_status run_generations(GenGraph& g, cudaStream_t stream, int n, int per_grap
 // (measured: C4, 2^21 gate slots, 2468 -> 2551 gen/s; 2^23 slots +0.8 %).
 inline int graph_generations(int64_t touches) { return touches <= (1LL << 22) ? 16 : 0; }
 
+// n = ISQ_MAX_FAST_WIRES+1 .. ISQ_MAX_WIRES: block-per-circuit fitness (unitary
+// != nullptr: composition from I with the exact global phase, as compose_kernel).
+// codes_alt / thetas_alt / parity: the GA's double-buffered genomes (odd
+// generation counter -> the alternate buffers).
+isq_status launch_fitness_generic(int n, int L, int64_t count, const uint8_t* codes, const double* thetas,
+                                  const double* target, double* fitness, double* unitary, const int32_t* stop,
+                                  cudaStream_t stream, int* bad_code, const uint8_t* codes_alt = nullptr,
+                                  const double* thetas_alt = nullptr, const uint64_t* parity = nullptr);
+
 isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, const double* T,
                                   double* out, cudaStream_t stream);
 

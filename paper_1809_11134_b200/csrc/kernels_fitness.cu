@@ -1,6 +1,9 @@
 // Fitness / composition of explicit gate lists (GA genomes, best-circuit
 // readout, the functional API).  Replaces compose_gates + fitness_value
 // (gates.py:187-195, fitness.py:36-49) for a batch of circuits.
+#include <map>
+#include <mutex>
+
 #include "isq_internal.h"
 #include "fitness_multi.cuh"
 #include "fitness_warp.cuh"
@@ -149,6 +152,197 @@ isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, con
   return ISQ_OK;
 }
 
+// ------------------------------------------------------ n = 6 .. 10 ---
+// numberOfWires above the register-resident kernels (the reference allows up
+// to its 4^n <= 2^26 cap, engine.py:43,60-63): one block per circuit with
+// the 2^n x 2^n state in global scratch (L1 / L2 resident per block), every
+// gate applied as what it is on all columns at once -- a rotation as D/2
+// row-pair butterflies per column, Rz / ZZ as row phases -- with the exact
+// gate matrices (gates.py:60-116: cos(th/2) I - i sin(th/2) sigma,
+// exp(-i th/2 signs)).  kCompose: S from I, gates in order, the unitary and
+// its overlap with T out (compose_gates + fitness_value); otherwise
+// M = S^dagger T from T with the adjoints in reverse order and the fitness
+// from the trace (the same adjoint evaluation as the fast kernels).
+constexpr int kGenericThreads = 256;
+
+__device__ __forceinline__ void generic_apply(double2* M, int n, int code, double th) {
+  const int D = 1 << n;
+  const int64_t DD = (int64_t)D * D;
+  double s, c;
+  sincos(0.5 * th, &s, &c);
+  if (code < 3 * n && code % 3 != 2) {  // Rx / Ry on wire w: row bit n - w
+    const int b = n - 1 - code / 3;
+    const bool rx = code % 3 == 0;
+    const int m = 1 << b;
+    for (int64_t idx = threadIdx.x; idx < DD / 2; idx += blockDim.x) {
+      const int64_t i = idx / D;                                // row pair
+      const int col = (int)(idx - i * D);
+      const int64_t r0 = ((i >> b) << (b + 1)) | (i & (m - 1));  // bit b cleared
+      double2* pa = M + r0 * D + col;
+      double2* pb = pa + (int64_t)m * D;
+      const double2 a = *pa, bb = *pb;
+      if (rx) {  // [[c, -is], [-is, c]]
+        *pa = make_double2(c * a.x + s * bb.y, c * a.y - s * bb.x);
+        *pb = make_double2(c * bb.x + s * a.y, c * bb.y - s * a.x);
+      } else {  // [[c, -s], [s, c]]
+        *pa = make_double2(c * a.x - s * bb.x, c * a.y - s * bb.y);
+        *pb = make_double2(s * a.x + c * bb.x, s * a.y + c * bb.y);
+      }
+    }
+    return;
+  }
+  int mask;
+  if (code < 3 * n) {
+    mask = 1 << (n - 1 - code / 3);  // Rz: e^{-i th/2} on bit 0, e^{+i th/2} on bit 1
+  } else {
+    int i = 1, t = code - 3 * n;
+    while (t >= n - i) {
+      t -= n - i;
+      ++i;
+    }
+    mask = (1 << (n - i)) | (1 << (n - (i + 1 + t)));  // ZZ: e^{-i th/2} when the bits agree
+  }
+  for (int64_t idx = threadIdx.x; idx < DD; idx += blockDim.x) {
+    const int r = (int)(idx / D);
+    const int par = __popc(r & mask) & 1;
+    const double sg = par ? 1.0 : -1.0;  // phase e^{i sg th/2}
+    const double2 x = M[idx];
+    const double ps = sg * s;
+    M[idx] = make_double2(c * x.x - ps * x.y, c * x.y + ps * x.x);
+  }
+}
+
+// GenericInput: the circuits' codes / angles; with `parity` set (the GA's
+// generation counter) the odd generations read the alternate buffers.
+struct GenericInput {
+  const uint8_t* codes;
+  const double* thetas;
+  const uint8_t* codes_alt;
+  const double* thetas_alt;
+  const uint64_t* parity;
+};
+
+template <bool kCompose>
+__global__ void __launch_bounds__(kGenericThreads)
+    fitness_generic_kernel(int n, int L, int64_t count, GenericInput in, const double2* __restrict__ target,
+                           double* __restrict__ fitness, double2* __restrict__ unitary, double2* scratch,
+                           const int32_t* __restrict__ stop, int* bad_code) {
+  __shared__ double red_r[kGenericThreads], red_i[kGenericThreads];
+  if (stop != nullptr && *stop) return;
+  const bool alt = in.parity != nullptr && (*in.parity & 1);
+  const uint8_t* __restrict__ codes = alt ? in.codes_alt : in.codes;
+  const double* __restrict__ thetas = alt ? in.thetas_alt : in.thetas;
+  const int D = 1 << n;
+  const int64_t DD = (int64_t)D * D;
+  const int ncodes = 3 * n + n * (n - 1) / 2;
+  double2* M = scratch + (int64_t)blockIdx.x * DD;
+  for (int64_t cc = blockIdx.x; cc < count; cc += gridDim.x) {
+    for (int64_t i = threadIdx.x; i < DD; i += blockDim.x) {
+      if (kCompose) {
+        const int64_t r = i / D;
+        M[i] = make_double2(r == i - r * D ? 1.0 : 0.0, 0.0);
+      } else {
+        M[i] = target[i];
+      }
+    }
+    bool bad = false;
+    __syncthreads();
+    for (int q = 0; q < L; ++q) {
+      const int p = kCompose ? q : L - 1 - q;  // adjoints in reverse order
+      const int code = codes[cc * L + p];
+      const double th = thetas[cc * L + p];
+      if (code >= ncodes) {
+        bad = true;
+      } else {
+        generic_apply(M, n, code, kCompose ? th : -th);
+      }
+      __syncthreads();
+    }
+    double ar = 0.0, ai = 0.0;
+    if (kCompose) {  // fitness_value(S, T): |sum conj(S) * T|
+      for (int64_t i = threadIdx.x; i < DD; i += blockDim.x) {
+        const double2 x = M[i], t = target[i];
+        ar = fma(x.x, t.x, ar);
+        ar = fma(x.y, t.y, ar);
+        ai = fma(x.x, t.y, ai);
+        ai = fma(-x.y, t.x, ai);
+        unitary[cc * DD + i] = x;
+      }
+    } else {  // |tr(S^dagger T)|
+      for (int j = threadIdx.x; j < D; j += blockDim.x) {
+        const double2 x = M[(int64_t)j * D + j];
+        ar += x.x;
+        ai += x.y;
+      }
+    }
+    red_r[threadIdx.x] = ar;
+    red_i[threadIdx.x] = ai;
+    __syncthreads();
+    for (int off = kGenericThreads / 2; off >= 1; off >>= 1) {
+      if (threadIdx.x < off) {
+        red_r[threadIdx.x] += red_r[threadIdx.x + off];
+        red_i[threadIdx.x] += red_i[threadIdx.x + off];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      fitness[cc] = bad ? __longlong_as_double(0x7ff8000000000000LL)
+                        : fitness_from_overlap(hypot(red_r[0], red_i[0]), D);
+      if (bad && bad_code) atomicOr(bad_code, 1);
+    }
+    __syncthreads();
+  }
+}
+
+// Per-device scratch for the generic kernel (grow-only, process lifetime).
+static double2* generic_scratch(size_t bytes) {
+  static std::mutex mu;
+  static std::map<int, std::pair<double2*, size_t>> pool;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = pool[dev];
+  if (e.second < bytes) {
+    if (e.first) {
+      cudaDeviceSynchronize();
+      cudaFree(e.first);
+    }
+    e.first = nullptr;
+    e.second = 0;
+    if (cudaMalloc((void**)&e.first, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    e.second = bytes;
+  }
+  return e.first;
+}
+
+isq_status launch_fitness_generic(int n, int L, int64_t count, const uint8_t* codes, const double* thetas,
+                                  const double* target, double* fitness, double* unitary, const int32_t* stop,
+                                  cudaStream_t stream, int* bad_code, const uint8_t* codes_alt,
+                                  const double* thetas_alt, const uint64_t* parity) {
+  if (count <= 0) return ISQ_OK;
+  const GenericInput in{codes, thetas, codes_alt, thetas_alt, parity};
+  const int64_t DD = (int64_t)1 << (2 * n);
+  int64_t grid = (int64_t)num_sms() * (n <= 8 ? 2 : 1);
+  if (grid > count) grid = count;
+  double2* scratch = generic_scratch((size_t)grid * DD * sizeof(double2));
+  if (!scratch) {
+    set_error("cannot allocate the n >= 6 fitness scratch");
+    return ISQ_ERR_CUDA;
+  }
+  const double2* T = reinterpret_cast<const double2*>(target);
+  if (unitary)
+    fitness_generic_kernel<true><<<(unsigned)grid, kGenericThreads, 0, stream>>>(
+        n, L, count, in, T, fitness, reinterpret_cast<double2*>(unitary), scratch, stop, bad_code);
+  else
+    fitness_generic_kernel<false><<<(unsigned)grid, kGenericThreads, 0, stream>>>(
+        n, L, count, in, T, fitness, nullptr, scratch, stop, bad_code);
+  ISQ_CUDA_TRY(cudaGetLastError());
+  return ISQ_OK;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -226,6 +420,8 @@ isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uin
     case 4: return launch_fast_prec<4>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc, dyn);
     case 5: return launch_fast_prec<5>(L, count, codes, thetas, target, fitness, stop, b, p, stream, bc, dyn);
     default:
+      if (n > ISQ_MAX_FAST_WIRES && n <= ISQ_MAX_WIRES)  // fp64 only (the fp32 variant is a fast-kernel option)
+        return launch_fitness_generic(n, L, count, codes, thetas, target, fitness, nullptr, stop, stream, bc);
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;
   }
@@ -244,6 +440,9 @@ isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* code
     case 4: return launch_nq<4>(L, count, codes, thetas, target, fitness, unitary, stream);
     case 5: return launch_nq<5>(L, count, codes, thetas, target, fitness, unitary, stream);
     default:
+      if (n > ISQ_MAX_FAST_WIRES && n <= ISQ_MAX_WIRES)
+        return launch_fitness_generic(n, L, count, codes, thetas, target, fitness, unitary, nullptr, stream,
+                                      bad_code);
       set_error("numberOfWires=" + std::to_string(n) + " is outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;
   }

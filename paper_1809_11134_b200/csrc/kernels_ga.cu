@@ -464,6 +464,11 @@ static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaSt
     case 4: return ga_launch_eval_prec<4>(a, c0, c1, s);
     case 5: return ga_launch_eval_prec<5>(a, c0, c1, s);
     default:
+      if (a.n > ISQ_MAX_FAST_WIRES && a.n <= ISQ_MAX_WIRES)  // the current genomes by generation parity
+        return launch_fitness_generic(a.n, a.L, c1 - c0, a.codes[0] + c0 * a.L, a.thetas[0] + c0 * a.L,
+                                      reinterpret_cast<const double*>(a.target), a.fitness + c0, nullptr,
+                                      &a.st->stop, s, nullptr, a.codes[1] + c0 * a.L, a.thetas[1] + c0 * a.L,
+                                      &a.st->generation);
       set_error("numberOfWires outside the compiled range 2..5");
       return ISQ_ERR_UNSUPPORTED;
   }
@@ -997,7 +1002,12 @@ isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, 
     return ISQ_ERR_CONFIG;
   }
   const bool fp64 = a.precision == ISQ_PRECISION_FP64;
-  if (mode == ISQ_LAUNCH_FUSED || (mode == ISQ_LAUNCH_AUTO && fp64 && a.P * a.L <= kGaTailGenes)) {
+  if (mode == ISQ_LAUNCH_FUSED && a.n > ISQ_MAX_FAST_WIRES) {
+    set_error("the fused GA launch supports numberOfWires <= 5");
+    return ISQ_ERR_CONFIG;
+  }
+  if (mode == ISQ_LAUNCH_FUSED ||
+      (mode == ISQ_LAUNCH_AUTO && fp64 && a.n <= ISQ_MAX_FAST_WIRES && a.P * a.L <= kGaTailGenes)) {
     // one launch for n generations: one block when the population is one
     // fitness round, a cooperative grid otherwise
     const bool one_block = a.P <= kGaSmallPop && a.P * a.L <= kGaSmallGenes;

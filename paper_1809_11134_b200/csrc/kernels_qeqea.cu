@@ -874,7 +874,8 @@ isq_status qeqea_launch_finish(const QeqeaArgs& a, cudaStream_t s) {
 }
 
 bool qeqea_small(const QeqeaArgs& a) {
-  return a.world == 1 && a.precision == ISQ_PRECISION_FP64 && a.P <= kSmallPop && a.P * a.L <= kSmallTouches;
+  return a.world == 1 && a.precision == ISQ_PRECISION_FP64 && a.n <= ISQ_MAX_FAST_WIRES && a.P <= kSmallPop &&
+         a.P * a.L <= kSmallTouches;
 }
 
 isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s) {
@@ -888,7 +889,7 @@ isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s) {
     case 4: qeqea_small_kernel<4><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
     case 5: qeqea_small_kernel<5><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
     default:
-      set_error("numberOfWires outside the compiled range 2..5");
+      set_error("the fused single-block generation supports numberOfWires <= 5");
       return ISQ_ERR_UNSUPPORTED;
   }
   ISQ_CUDA_TRY(cudaGetLastError());

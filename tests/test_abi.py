@@ -77,16 +77,17 @@ def test_qeqea_create_validates_before_touching_a_device(field, value):
 
 
 def test_unsupported_shapes_are_reported_not_computed():
-    """n > 5 is a valid reference configuration the device build does not
-    implement: ISQ_ERR_UNSUPPORTED -> ConfigurationError, never a CPU fallback."""
+    """n > 10 is a valid reference configuration (its cap is 4^n <= 2^26) the
+    device build does not implement: ISQ_ERR_UNSUPPORTED ->
+    ConfigurationError, never a CPU fallback."""
     from paper_1809_11134_b200 import _lib
     from paper_1809_11134_b200.errors import ConfigurationError
 
     lib = _lib.load()
-    conf = _lib.QeqeaConfig(number_of_wires=6, size_of_individual=8, size_of_population=5,
+    conf = _lib.QeqeaConfig(number_of_wires=11, size_of_individual=8, size_of_population=5,
                             probability_of_mutation=0.3, mutation_range=0.78, n_meas=1, rank=0,
                             max_generations=10, target_fitness=0.999, seed=1, world=1, precision=0)
-    T = np.eye(64, dtype=np.complex128)
+    T = np.eye(2, dtype=np.complex128)  # never read: validation fails first
     h = ctypes.c_void_p()
     st = lib.isq_qeqea_create(ctypes.byref(conf), T.ctypes.data_as(ctypes.c_void_p), 0, 4, ctypes.byref(h))
     assert st == _lib.ISQ_ERR_UNSUPPORTED
