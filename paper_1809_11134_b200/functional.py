@@ -176,15 +176,6 @@ def evaluate_circuit(blueprint: np.ndarray, bank: SegmentBank, target: np.ndarra
     return float(evaluate_circuits(np.asarray(blueprint)[None, :], bank, target)[0])
 
 
-class _SlotMaxMirror(np.ndarray):
-    """Host copy of the device slot_max; in-place writes (table.slot_max[:] = 1.0,
-    pkg/tests/test_engine.py:192) mark it for upload before the next device use."""
-
-    def __setitem__(self, key, value):
-        super().__setitem__(key, value)
-        owner = getattr(self, "_owner", None)
-        if owner is not None:
-            owner._dirty = True
 
 
 class SegmentFitnessTable:
@@ -199,8 +190,10 @@ class SegmentFitnessTable:
         _lib.check(self._lib.isq_table_create(cfg.qubit_count, cfg.size_of_individual, self.device,
                                               ctypes.byref(h)))
         self._h = h
-        self._mirror: Optional[_SlotMaxMirror] = None
-        self._dirty = False
+        # host copy of slot_max handed out by .slot_max; callers may write it in
+        # place (table.slot_max[:] = 1.0, pkg/tests/test_engine.py:192), so it is
+        # uploaded before every device update while it is alive
+        self._mirror: Optional[np.ndarray] = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -212,17 +205,15 @@ class SegmentFitnessTable:
             self._h = None
 
     def _push(self):
-        if self._dirty and self._mirror is not None:
-            m = np.ascontiguousarray(self._mirror, dtype=np.float64).view(np.ndarray)
+        if self._mirror is not None:
+            m = np.ascontiguousarray(self._mirror, dtype=np.float64)
             _lib.check(self._lib.isq_table_set_slot_max(self._h, _lib.ptr(m)))
-        self._dirty = False
 
     @property
     def slot_max(self) -> np.ndarray:
         if self._mirror is None:
-            m = np.empty(self.cfg.qubit_count).view(_SlotMaxMirror)
-            _lib.check(self._lib.isq_table_read(self._h, _lib.ptr(m.view(np.ndarray)), None, None, None))
-            m._owner = self
+            m = np.empty(self.cfg.qubit_count)
+            _lib.check(self._lib.isq_table_read(self._h, _lib.ptr(m), None, None, None))
             self._mirror = m
         return self._mirror
 
@@ -248,7 +239,8 @@ class SegmentFitnessTable:
         improved = np.empty(bp.shape, dtype=np.uint8)
         _lib.check(self._lib.isq_table_update(self._h, fits.size, _lib.ptr(bp), _lib.ptr(fits),
                                               _lib.ptr(improved)))
-        self._mirror = None
+        if self._mirror is not None:  # the same array object stays current, as the reference's attribute
+            _lib.check(self._lib.isq_table_read(self._h, _lib.ptr(self._mirror), None, None, None))
         return {int(f) for f in np.unique(bp[improved.astype(bool)])}
 
     def update(self, blueprint: np.ndarray, fit: float) -> Set[int]:
@@ -269,7 +261,7 @@ def mutate_population(pop: PopulationState, table: SegmentFitnessTable, cfg: Pop
         raise ConfigurationError("population shape does not match the configuration")
     th, q = th0.copy(), np.ascontiguousarray(q0)
     q = q.copy()
-    smax = np.ascontiguousarray(table.slot_max, dtype=np.float64).view(np.ndarray)
+    smax = np.ascontiguousarray(table.slot_max, dtype=np.float64)
     mutated = np.empty(cfg.qubit_count, dtype=np.uint8)
     conf = _lib.QeqeaConfig(number_of_wires=cfg.number_of_wires, size_of_individual=cfg.size_of_individual,
                             size_of_population=cfg.size_of_population,
