@@ -294,17 +294,19 @@ __global__ void __launch_bounds__(kGenericThreads)
   }
 }
 
-// Per-device scratch for the generic kernel (grow-only, process lifetime).
-static double2* generic_scratch(size_t bytes) {
+// Scratch of the generic kernel per (device, stream): launches on one stream
+// are ordered, so they may share it; concurrent streams never do.  Grow-only,
+// kept for the process lifetime (n = 10: 16 MB per resident circuit).
+static double2* generic_scratch(size_t bytes, cudaStream_t stream) {
   static std::mutex mu;
-  static std::map<int, std::pair<double2*, size_t>> pool;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<double2*, size_t>> pool;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  auto& e = pool[dev];
+  auto& e = pool[std::make_pair(dev, stream)];
   if (e.second < bytes) {
     if (e.first) {
-      cudaDeviceSynchronize();
+      cudaStreamSynchronize(stream);  // earlier launches on this stream still read it
       cudaFree(e.first);
     }
     e.first = nullptr;
@@ -327,7 +329,7 @@ isq_status launch_fitness_generic(int n, int L, int64_t count, const uint8_t* co
   const int64_t DD = (int64_t)1 << (2 * n);
   int64_t grid = (int64_t)num_sms() * (n <= 8 ? 2 : 1);
   if (grid > count) grid = count;
-  double2* scratch = generic_scratch((size_t)grid * DD * sizeof(double2));
+  double2* scratch = generic_scratch((size_t)grid * DD * sizeof(double2), stream);
   if (!scratch) {
     set_error("cannot allocate the n >= 6 fitness scratch");
     return ISQ_ERR_CUDA;
