@@ -444,9 +444,11 @@ isq_status isq_qeqea_step(void* handle, int32_t n_generations, isq_generation_re
     if (st != ISQ_OK) return st;
     return isq_qeqea_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
   }
-  const int per_graph = mode == ISQ_LAUNCH_KERNELS ? 0
-                        : mode == ISQ_LAUNCH_GRAPH  ? 16
-                                                    : graph_generations(a.P * a.L);
+  // n > 5 runs the generic fitness kernel, whose scratch is allocated on
+  // first use: plain launches only (a capture would record the allocation)
+  const int per_graph = (mode == ISQ_LAUNCH_KERNELS || a.n > ISQ_MAX_FAST_WIRES) ? 0
+                        : mode == ISQ_LAUNCH_GRAPH                              ? 16
+                                                                                : graph_generations(a.P * a.L);
   st = run_generations(h->graph, h->stream, n_generations, per_graph,
                        [&a](cudaStream_t s) {
                          isq_status r = qeqea_launch_eval(a, s);

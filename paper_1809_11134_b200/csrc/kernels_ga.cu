@@ -1015,9 +1015,11 @@ isq_status isq_ga_step(void* handle, int32_t n, isq_generation_record* records, 
     if (st != ISQ_OK) return st;
     return isq_ga_read_batch(handle, records, n_done, stop_reason, nullptr, nullptr);
   }
-  const int per_graph = mode == ISQ_LAUNCH_KERNELS ? 0
-                        : mode == ISQ_LAUNCH_GRAPH  ? 16
-                                                    : graph_generations(a.P * a.L);
+  // n > 5 runs the generic fitness kernel, whose scratch is allocated on
+  // first use: plain launches only (a capture would record the allocation)
+  const int per_graph = (mode == ISQ_LAUNCH_KERNELS || a.n > ISQ_MAX_FAST_WIRES) ? 0
+                        : mode == ISQ_LAUNCH_GRAPH                              ? 16
+                                                                                : graph_generations(a.P * a.L);
   st = run_generations(h->graph, h->stream, n, per_graph, [&a](cudaStream_t s) {
     isq_status r = ga_launch_eval(a, 0, a.P, s);
     return r != ISQ_OK ? r : ga_launch_finish(a, s);

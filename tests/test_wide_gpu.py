@@ -32,6 +32,11 @@ def test_qeqea_trajectory_n6_matches_reference(mode):
     g = golden("traj_qeqea_n6")
     eng = _engine_from_golden(g)
     eng.set_launch_mode(mode)
+    if mode == "graph":  # batches of generations (graph mode is plain launches above 5 wires)
+        b = _engine_from_golden(g)
+        b.set_launch_mode(mode)
+        rec = b.steps(int(g["gens"]))
+        assert fit_close(rec["gen_best"], g["records"][:, 0]).all()
     gen = 0
     while not eng.done:
         flats, _, _ = eng.sample()
