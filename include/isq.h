@@ -364,6 +364,13 @@ isq_status isq_table_update(void* table, int64_t count, const int64_t* blueprint
                             uint8_t* improved);
 isq_status isq_table_read(void* table, double* slot_max, int64_t* n_entries, int64_t* keys, double* values);
 isq_status isq_table_set_slot_max(void* table, const double* slot_max);
+/* apply_gate (gates.py:173-184) for gate sequences: acc_out[c] = G_{L-1} ... G_0
+ * acc_in[c] (each gate left-multiplied in order, exact gate matrices), for
+ * `count` circuits of `length` gate codes / angles and count x 2^n x 2^n
+ * complex matrices (numpy complex128); n = 2..10.  compose_gates is
+ * acc_in = I; expand_rotation / interaction_gate one gate on I. */
+isq_status isq_apply_gates(int32_t n, int32_t length, int64_t count, const uint8_t* codes, const double* thetas,
+                           const double* acc_in, double* acc_out, int32_t device);
 /* random_genome (ga.py:68-73) of genomes [first, first + count): count * length codes / angles. */
 isq_status isq_ga_random_genomes(int32_t n, int32_t length, uint64_t seed, int64_t first, int64_t count,
                                  uint8_t* codes, double* thetas, int32_t device);

@@ -176,6 +176,7 @@ SIGNATURES: dict[str, tuple] = {
     "isq_table_update": (c_i32, [c_vp, c_i64, c_vp, c_vp, c_vp]),
     "isq_table_read": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "isq_table_set_slot_max": (c_i32, [c_vp, c_vp]),
+    "isq_apply_gates": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32]),
     "isq_ga_random_genomes": (c_i32, [c_i32, c_i32, c_u64, c_i64, c_i64, c_vp, c_vp, c_i32]),
     "isq_ga_sus_select": (c_i32, [c_i64, c_vp, c_i64, c_u64, c_u64, c_vp, c_i32]),
     "isq_ga_crossover_cuts": (c_i32, [c_i32, c_u64, c_u64, c_i64, c_i64, c_vp, c_i32]),

@@ -518,6 +518,40 @@ isq_status isq_table_set_slot_max(void* handle, const double* slot_max) {
   return ISQ_OK;
 }
 
+isq_status isq_apply_gates(int32_t n, int32_t length, int64_t count, const uint8_t* codes, const double* thetas,
+                           const double* acc_in, double* acc_out, int32_t device) {
+  if (n < ISQ_MIN_WIRES || n > ISQ_MAX_WIRES) {
+    set_error("numberOfWires=" + std::to_string(n) + " is outside the supported range 2..10");
+    return n < 2 ? ISQ_ERR_CONFIG : ISQ_ERR_UNSUPPORTED;
+  }
+  if (length < 0 || count < 0) return bad_config("negative circuit length or count");
+  const int ncodes = 3 * n + n * (n - 1) / 2;
+  for (int64_t i = 0; i < count * (int64_t)length; ++i)
+    if (codes[i] >= ncodes) return bad_config("gate code out of range for numberOfWires");
+  if (count == 0) return ISQ_OK;
+  TRYF(cudaSetDevice(device));
+  const int64_t DD = (int64_t)1 << (2 * n);
+  DevBuf dc, dt, di, dout, df, dT;
+  TRYF(dc.alloc(count * length + 1));
+  TRYF(dt.alloc((count * length + 1) * 8));
+  TRYF(di.alloc(count * DD * 16));
+  TRYF(dout.alloc(count * DD * 16));
+  TRYF(df.alloc(count * 8));
+  TRYF(dT.alloc(DD * 16));
+  TRYF(cudaMemset(dT.p, 0, DD * 16));
+  if (length > 0) {
+    TRYF(cudaMemcpy(dc.p, codes, count * length, cudaMemcpyHostToDevice));
+    TRYF(cudaMemcpy(dt.p, thetas, count * length * 8, cudaMemcpyHostToDevice));
+  }
+  TRYF(cudaMemcpy(di.p, acc_in, count * DD * 16, cudaMemcpyHostToDevice));
+  isq_status st = launch_fitness_generic(n, length, count, dc.as<uint8_t>(), dt.as<double>(), dT.as<double>(),
+                                         df.as<double>(), dout.as<double>(), nullptr, nullptr, nullptr,
+                                         nullptr, nullptr, nullptr, di.as<double>());
+  if (st != ISQ_OK) return st;
+  TRYF(cudaMemcpy(acc_out, dout.p, count * DD * 16, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
 isq_status isq_ga_random_genomes(int32_t n, int32_t L, uint64_t seed, int64_t first, int64_t count, uint8_t* codes,
                                  double* thetas, int32_t device) {
   isq_status st = check_layout(n, L, 1);

@@ -109,7 +109,8 @@ inline int graph_generations(int64_t touches) { return touches <= (1LL << 22) ? 
 isq_status launch_fitness_generic(int n, int L, int64_t count, const uint8_t* codes, const double* thetas,
                                   const double* target, double* fitness, double* unitary, const int32_t* stop,
                                   cudaStream_t stream, int* bad_code, const uint8_t* codes_alt = nullptr,
-                                  const double* thetas_alt = nullptr, const uint64_t* parity = nullptr);
+                                  const double* thetas_alt = nullptr, const uint64_t* parity = nullptr,
+                                  const double* init = nullptr);
 
 isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, const double* T,
                                   double* out, cudaStream_t stream);

@@ -220,6 +220,7 @@ struct GenericInput {
   const uint8_t* codes_alt;
   const double* thetas_alt;
   const uint64_t* parity;
+  const double2* init;  // kCompose: starting matrices (count x D x D) instead of I (apply_gate)
 };
 
 template <bool kCompose>
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kGenericThreads)
     for (int64_t i = threadIdx.x; i < DD; i += blockDim.x) {
       if (kCompose) {
         const int64_t r = i / D;
-        M[i] = make_double2(r == i - r * D ? 1.0 : 0.0, 0.0);
+        M[i] = in.init ? in.init[cc * DD + i] : make_double2(r == i - r * D ? 1.0 : 0.0, 0.0);
       } else {
         M[i] = target[i];
       }
@@ -323,9 +324,9 @@ static double2* generic_scratch(size_t bytes, cudaStream_t stream) {
 isq_status launch_fitness_generic(int n, int L, int64_t count, const uint8_t* codes, const double* thetas,
                                   const double* target, double* fitness, double* unitary, const int32_t* stop,
                                   cudaStream_t stream, int* bad_code, const uint8_t* codes_alt,
-                                  const double* thetas_alt, const uint64_t* parity) {
+                                  const double* thetas_alt, const uint64_t* parity, const double* init) {
   if (count <= 0) return ISQ_OK;
-  const GenericInput in{codes, thetas, codes_alt, thetas_alt, parity};
+  const GenericInput in{codes, thetas, codes_alt, thetas_alt, parity, reinterpret_cast<const double2*>(init)};
   const int64_t DD = (int64_t)1 << (2 * n);
   int64_t grid = (int64_t)num_sms() * (n <= 8 ? 2 : 1);
   if (grid > count) grid = count;

@@ -158,3 +158,48 @@ def compose_gates(gates: Sequence[GateOp], number_of_wires: int) -> np.ndarray:
 
     codes, thetas = encode_gates(gates, number_of_wires)
     return compose_batch(codes[None, :], thetas[None, :], number_of_wires)[0]
+
+
+def apply_gates(acc: np.ndarray, gates: Sequence[GateOp], number_of_wires: int, device: int = 0) -> np.ndarray:
+    """acc left-multiplied by every gate in order (position 0 first), on the
+    GPU (isq_apply_gates: each gate applied as row-pair butterflies / row
+    phases with its exact matrix).  acc: (D, D) or (count, D, D)."""
+    from . import _lib
+
+    n = number_of_wires
+    a = np.ascontiguousarray(acc, dtype=np.complex128)
+    single = a.ndim == 2
+    if single:
+        a = a[None]
+    d = 2 ** n
+    if a.shape[1:] != (d, d):
+        raise ConfigurationError(f"accumulator shape {a.shape[1:]} != ({d}, {d})")
+    codes, thetas = encode_gates(gates, n)
+    count = a.shape[0]
+    codes = np.ascontiguousarray(np.broadcast_to(codes, (count, codes.size)))
+    thetas = np.ascontiguousarray(np.broadcast_to(thetas, (count, thetas.size)))
+    out = np.empty_like(a)
+    lib = _lib.load()
+    _lib.check(lib.isq_apply_gates(n, codes.shape[1], count, _lib.ptr(codes), _lib.ptr(thetas), _lib.ptr(a),
+                                   _lib.ptr(out), int(device)))
+    return out[0] if single else out
+
+
+def apply_gate(acc: np.ndarray, gate: GateOp, number_of_wires: int) -> np.ndarray:
+    """gates.py:173-184: the accumulator left-multiplied by the expanded gate."""
+    return apply_gates(acc, [gate], number_of_wires)
+
+
+def expand_rotation(axis: Axis, theta: float, wire: int, number_of_wires: int) -> np.ndarray:
+    """gates.py:101-116: a single-wire rotation embedded in the 2^n width."""
+    if not 1 <= wire <= number_of_wires:
+        raise ConfigurationError(f"wire {wire} out of range 1..{number_of_wires}")
+    gate = GateOp(kind="rotation", theta=theta, wire=wire, axis=Axis(int(axis)))
+    return apply_gate(np.eye(2 ** number_of_wires, dtype=np.complex128), gate, number_of_wires)
+
+
+def interaction_gate(template: InteractionTemplate, theta: float) -> np.ndarray:
+    """gates.py:96-98: the dense diagonal matrix of J_ij(theta)."""
+    n = int(round(math.log2(template.signs.size)))
+    gate = GateOp(kind="interaction", theta=theta, pair=tuple(template.pair))
+    return apply_gate(np.eye(2 ** n, dtype=np.complex128), gate, n)

@@ -302,3 +302,37 @@ def test_module_level_names_resolve_like_the_reference():
     assert all(callable(f) for f in (SegmentFitnessTable, construct_segments, evaluate_circuit, init_population,
                                      mutate_population, sample_circuit, decode_genome, ga_mutate, random_genome,
                                      sus_select, two_point_crossover))
+
+
+def test_apply_gate_expand_rotation_interaction_gate_match_the_reference_definitions():
+    """gates.py:96-116,173-184: dense Kronecker expansion / diagonal, left
+    multiplication of an arbitrary accumulator (pkg/tests/test_gates.py:112-132)."""
+    from paper_1809_11134_b200.gates import (Axis, GateOp, apply_gate, apply_gates, compose_gates,
+                                             enumerate_templates, expand_rotation, interaction_gate,
+                                             interaction_diagonal, rotation_gate)
+
+    rng = np.random.default_rng(4)
+    for n in (2, 3, 5, 6):
+        d = 2 ** n
+        acc = rng.normal(size=(d, d)) + 1j * rng.normal(size=(d, d))
+        for wire in (1, n):
+            for axis in Axis:
+                th = float(rng.uniform(0, 2 * math.pi))
+                left, right = 2 ** (wire - 1), 2 ** (n - wire)
+                dense = np.kron(np.kron(np.eye(left), rotation_gate(axis, th)), np.eye(right))
+                np.testing.assert_allclose(expand_rotation(axis, th, wire, n), dense, atol=1e-14)
+                g = GateOp(kind="rotation", theta=th, wire=wire, axis=axis)
+                np.testing.assert_allclose(apply_gate(acc, g, n), dense @ acc, atol=1e-12)
+        tpl = enumerate_templates(n)[-1]
+        th = float(rng.uniform(0, 2 * math.pi))
+        np.testing.assert_allclose(interaction_gate(tpl, th), np.diag(interaction_diagonal(tpl, th)), atol=1e-14)
+        gates = [GateOp(kind="rotation", theta=0.3, wire=1, axis=Axis.Y),
+                 GateOp(kind="interaction", theta=1.1, pair=tpl.pair)]
+        np.testing.assert_allclose(apply_gates(np.eye(d), gates, n), compose_gates(gates, n), atol=1e-13)
+
+
+def test_target_is_valid():
+    from paper_1809_11134_b200.fitness import TargetSpec, target_is_valid, target_matrix
+
+    assert target_is_valid(target_matrix("Toffoli"))
+    assert not target_is_valid(TargetSpec("bad", 1, np.array([[1, 0], [0, 2]], dtype=complex)))
