@@ -43,11 +43,12 @@ typedef int32_t isq_status;
 /* Smallest / largest numberOfWires the device kernels handle; up to
  * ISQ_MAX_FAST_WIRES the fitness runs in the register-resident kernels, above
  * it (fp64 only, no fused single-block launch) in a block-per-circuit kernel
- * with the 2^n x 2^n state in device scratch.  The reference's cap is
- * 4^n <= 2^26 (n <= 13, engine.py:43). */
+ * with the 2^n x 2^n state in device scratch, up to the reference's default
+ * cap 4^n <= 2^26 (n <= 13, engine.py:43; a raised memory_cap_entries above
+ * that is ISQ_ERR_UNSUPPORTED here). */
 #define ISQ_MIN_WIRES 2
 #define ISQ_MAX_FAST_WIRES 5
-#define ISQ_MAX_WIRES 10
+#define ISQ_MAX_WIRES 13
 
 const char* isq_last_error(void);
 int32_t isq_abi_version(void);
@@ -367,7 +368,7 @@ isq_status isq_table_set_slot_max(void* table, const double* slot_max);
 /* apply_gate (gates.py:173-184) for gate sequences: acc_out[c] = G_{L-1} ... G_0
  * acc_in[c] (each gate left-multiplied in order, exact gate matrices), for
  * `count` circuits of `length` gate codes / angles and count x 2^n x 2^n
- * complex matrices (numpy complex128); n = 2..10.  compose_gates is
+ * complex matrices (numpy complex128); n = 2..13.  compose_gates is
  * acc_in = I; expand_rotation / interaction_gate one gate on I. */
 isq_status isq_apply_gates(int32_t n, int32_t length, int64_t count, const uint8_t* codes, const double* thetas,
                            const double* acc_in, double* acc_out, int32_t device);

@@ -25,7 +25,7 @@ ISQ_ERR_COMM = 4
 ISQ_ERR_UNSUPPORTED = 5
 
 MIN_WIRES = 2
-MAX_WIRES = 10
+MAX_WIRES = 13
 MAX_FAST_WIRES = 5
 
 _lock = threading.Lock()

@@ -72,7 +72,7 @@ static isq_status validate(const isq_qeqea_config* c) {
     return bad("targetFitness must be in (0, 1]");
   if (c->number_of_wires > ISQ_MAX_WIRES) {
     set_error("numberOfWires=" + std::to_string(c->number_of_wires) +
-              " exceeds the device kernels (compiled for 2..5 wires)");
+              " exceeds the device kernels (2..13 wires, the reference's default 4^n <= 2^26 cap)");
     return ISQ_ERR_UNSUPPORTED;
   }
   if (c->size_of_individual > 4096) {

@@ -330,6 +330,13 @@ isq_status launch_fitness_generic(int n, int L, int64_t count, const uint8_t* co
   const int64_t DD = (int64_t)1 << (2 * n);
   int64_t grid = (int64_t)num_sms() * (n <= 8 ? 2 : 1);
   if (grid > count) grid = count;
+  // n >= 11: one resident matrix is 64 MB .. 1 GB (n = 13); bound the
+  // scratch by a quarter of the free memory (at least one circuit)
+  size_t free_b = 0, total_b = 0;
+  if (n >= 11 && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+    const int64_t fit = (int64_t)(free_b / 4 / (size_t)(DD * sizeof(double2)));
+    if (grid > fit) grid = fit < 1 ? 1 : fit;
+  }
   double2* scratch = generic_scratch((size_t)grid * DD * sizeof(double2), stream);
   if (!scratch) {
     set_error("cannot allocate the n >= 6 fitness scratch");

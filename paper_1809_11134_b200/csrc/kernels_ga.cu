@@ -855,7 +855,7 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
     return bad("targetFitness must be in (0, 1]");
   if (cfg->max_generations < 1) return bad("maxGenerations must be ≥ 1");
   if (cfg->number_of_wires > ISQ_MAX_WIRES)
-    return bad("numberOfWires exceeds the device kernels (compiled for 2..5 wires)",
+    return bad("numberOfWires exceeds the device kernels (2..13 wires, the reference's default 4^n <= 2^26 cap)",
                ISQ_ERR_UNSUPPORTED);
   if (cfg->population >= (1LL << 31)) return bad("population must be < 2^31", ISQ_ERR_UNSUPPORTED);
   if ((int64_t)cfg->population * cfg->size_of_individual >= (1LL << 32))

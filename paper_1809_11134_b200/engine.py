@@ -13,8 +13,9 @@ Differences from the reference, by design:
   * the initial bank is drawn on the device from per-slot streams (θ uniform,
     Box-Muller qutrits) unless `population=` injects one (e.g. the reference's
     own init_population output);
-  * numberOfWires is limited to 2..10 (ConfigurationError; the reference
-    allows its 4^n <= 2^26 cap, n <= 13); any nMeas >= 1
+  * numberOfWires is limited to 2..13, the reference's default
+    4^n <= 2^26 cap (a raised memory_cap_entries beyond it is a
+    ConfigurationError here); any nMeas >= 1
     (numpy's inversion and BTPE binomial branches are both reproduced).
 """
 from __future__ import annotations

@@ -77,14 +77,15 @@ def test_qeqea_create_validates_before_touching_a_device(field, value):
 
 
 def test_unsupported_shapes_are_reported_not_computed():
-    """n > 10 is a valid reference configuration (its cap is 4^n <= 2^26) the
-    device build does not implement: ISQ_ERR_UNSUPPORTED ->
+    """n = 14 is a valid reference configuration once its memory_cap_entries
+    is raised above the default 2^26 (engine.py:43,60-63); the device build
+    stops at the default cap (n = 13): ISQ_ERR_UNSUPPORTED ->
     ConfigurationError, never a CPU fallback."""
     from paper_1809_11134_b200 import _lib
     from paper_1809_11134_b200.errors import ConfigurationError
 
     lib = _lib.load()
-    conf = _lib.QeqeaConfig(number_of_wires=11, size_of_individual=8, size_of_population=5,
+    conf = _lib.QeqeaConfig(number_of_wires=14, size_of_individual=8, size_of_population=5,
                             probability_of_mutation=0.3, mutation_range=0.78, n_meas=1, rank=0,
                             max_generations=10, target_fitness=0.999, seed=1, world=1, precision=0)
     T = np.eye(2, dtype=np.complex128)  # never read: validation fails first
@@ -93,6 +94,11 @@ def test_unsupported_shapes_are_reported_not_computed():
     assert st == _lib.ISQ_ERR_UNSUPPORTED
     with pytest.raises(ConfigurationError):
         _lib.check(st)
+    codes, thetas = np.zeros(1, np.uint8), np.zeros(1)
+    fit = np.zeros(1)
+    st = lib.isq_fitness_batch_ex(14, 1, 1, _lib.ptr(codes), _lib.ptr(thetas), T.ctypes.data_as(ctypes.c_void_p),
+                                  _lib.ptr(fit), 0, 0)
+    assert st == _lib.ISQ_ERR_UNSUPPORTED
 
 
 def test_null_handles_are_rejected():
