@@ -29,3 +29,19 @@ def product_target(n: int, seed: int) -> np.ndarray:
     par = ((r >> (n - 1)) ^ (r >> (n - 2))) & 1
     m *= np.exp(1j * 0.35 * (1 - 2 * par))[:, None]
     return m
+
+
+def sus_fitness(P: int, seed: int, kind: str) -> np.ndarray:
+    """Fitness vectors for the large-population SUS fixtures
+    (oracle/gen_golden_sus.py): `skewed` spans many binades, `zeros` adds 30 %
+    exact zeros, `ties` are dyadic multiples of 1/8 (exact sums, pointer ties)."""
+    rng = np.random.default_rng(seed)
+    if kind == "skewed":
+        return rng.random(P) ** 6
+    if kind == "zeros":
+        f = rng.random(P) ** 2
+        f[rng.random(P) < 0.3] = 0.0
+        return f
+    if kind == "ties":
+        return rng.integers(0, 5, P) * 0.125
+    raise ValueError(kind)

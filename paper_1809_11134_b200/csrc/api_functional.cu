@@ -20,6 +20,7 @@
 
 #include "engine_common.cuh"
 #include "isq_internal.h"
+#include "sus.cuh"
 
 namespace isq {
 
@@ -283,30 +284,27 @@ __global__ void fn_ga_random_genomes_kernel(int L, int ncodes, uint64_t seed, in
   }
 }
 
-// sus_select (ga.py:95-116), one thread: numpy's pairwise total, the
-// sequential walk in its own rounding.
-__global__ void fn_ga_sus_kernel(const double* f, int64_t P, int64_t count, uint64_t seed, uint64_t g,
-                                 int64_t* picks) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+// sus_select (ga.py:95-116) on one block (sus.cuh): numpy's pairwise total,
+// the walk's two running sums in their own rounding, then sus_search_kernel
+// (skipped through *flag when every fitness is zero: uniform draws here).
+__global__ void __launch_bounds__(kSusThreads)
+    fn_ga_sus_kernel(const double* f, int64_t P, int64_t count, uint64_t seed, uint64_t g, int64_t* picks,
+                     double* C, double* Pt, int* flag) {
+  __shared__ double sm[kSusThreads];
+  const double total = np_pairwise_sum_block<kSusThreads>(f, P, sm);
   NpStream rs;
   rs.init(seed, DOM_GA_SUS, g, 0, 0);
-  const double total = np_pairwise_sum(f, P);
   if (total <= 0.0) {
-    for (int64_t k = 0; k < count; ++k) picks[k] = rs.integers(P);
+    if (threadIdx.x == 0) {
+      for (int64_t k = 0; k < count; ++k) picks[k] = rs.integers(P);
+      *flag = 0;
+    }
     return;
   }
   const double spacing = __ddiv_rn(total, (double)count);
-  double pointer = rs.uniform(0.0, spacing);
-  double cumulative = 0.0;
-  int64_t index = 0;
-  for (int64_t k = 0; k < count; ++k) {
-    while (index < P - 1 && __dadd_rn(cumulative, f[index]) <= pointer) {
-      cumulative = __dadd_rn(cumulative, f[index]);
-      ++index;
-    }
-    picks[k] = index;
-    pointer = __dadd_rn(pointer, spacing);
-  }
+  const double pointer = rs.uniform(0.0, spacing);
+  sus_chains_block(f, P - 1, pointer, spacing, count, C, Pt);
+  if (threadIdx.x == 0) *flag = 1;
 }
 
 // two_point_crossover cuts (ga.py:81-92): sorted(integers(0, L + 1, size=2)), no draw for L < 2.
@@ -579,7 +577,15 @@ isq_status isq_ga_sus_select(int64_t P, const double* fitness, int64_t count, ui
   TRYF(df.alloc(P * 8));
   TRYF(dp.alloc(count * 8));
   TRYF(cudaMemcpy(df.p, fitness, P * 8, cudaMemcpyHostToDevice));
-  fn_ga_sus_kernel<<<1, 1>>>(df.as<double>(), P, count, seed, generation, dp.as<int64_t>());
+  DevBuf dC, dP, dflag;
+  TRYF(dC.alloc(P * 8));
+  TRYF(dP.alloc(count * 8));
+  TRYF(dflag.alloc(sizeof(int)));
+  fn_ga_sus_kernel<<<1, kSusThreads>>>(df.as<double>(), P, count, seed, generation, dp.as<int64_t>(),
+                                       dC.as<double>(), dP.as<double>(), dflag.as<int>());
+  TRYF(cudaGetLastError());
+  sus_search_kernel<int64_t><<<grid_for(count), 256>>>(dC.as<double>(), P - 1, dP.as<double>(), count,
+                                                       dp.as<int64_t>(), dflag.as<int>(), nullptr);
   TRYF(cudaGetLastError());
   TRYF(cudaMemcpy(picks, dp.p, count * 8, cudaMemcpyDeviceToHost));
   return ISQ_OK;

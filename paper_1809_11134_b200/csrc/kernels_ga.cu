@@ -23,6 +23,7 @@
 #include "fitness_multi.cuh"
 #include "fitness_warp.cuh"
 #include "isq_internal.h"
+#include "sus.cuh"
 
 namespace isq {
 
@@ -55,6 +56,9 @@ struct GaArgs {
   double* part_sum;
   int64_t* part_arg;
   int n_parts;
+  double* sus_C;  // P > kSusCache: the walk's running sums (sus.cuh)
+  double* sus_P;
+  int* sus_flag;
   int precision;  // fitness arithmetic: ISQ_PRECISION_FP64 / _FP32
   FastDiv div_L, div_P;  // gene index -> genome; pair index mod P (P * L < 2^32)
 };
@@ -141,6 +145,35 @@ struct NoIdleWork {
 // sequential rounding, and every thread k finds parents[k] = the first
 // i <= P-2 with C[i+1] > p[k] (else P-1) by binary search: both sequences are
 // nondecreasing (fitness >= 0), so that is where the walk stops.
+// Thread 0: combine the partial reductions, best-so-far update (ga.py:171-174),
+// generation record.
+__device__ __forceinline__ void ga_reduce_final(const GaArgs& a, int& s_improved, int64_t& s_elite) {
+  GaDevState* st = a.st;
+  double m = -1.0, sum = 0.0;
+  int64_t arg = INT64_MAX;
+  for (int i = 0; i < a.n_parts; ++i) {
+    const double pm = a.part_max[i];
+    if (pm > m || (pm == m && a.part_arg[i] < arg)) {
+      m = pm;
+      arg = a.part_arg[i];
+    }
+    sum += a.part_sum[i];
+  }
+  const int improved = m > st->best_fitness;
+  if (improved) st->best_fitness = m;
+  st->elite = arg;
+  st->improved = improved;
+  GenRecord r;
+  r.gen_best = m;
+  r.gen_mean = sum / (double)a.P;
+  r.best_fitness = st->best_fitness;
+  r.pad = 0.0;
+  const uint64_t ri = st->generation - st->rec_base;
+  if (ri < (uint64_t)a.rec_cap) a.records[ri] = r;
+  s_improved = improved;
+  s_elite = arg;
+}
+
 template <class Idle = NoIdleWork>
 __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_improved_p, int64_t* s_elite_p,
                                                    Idle idle = Idle(), double* scratch = nullptr,
@@ -158,29 +191,7 @@ __device__ __forceinline__ void ga_reduce_sus_body(const GaArgs& a, int* s_impro
   __syncthreads();
   const double* fit = cached ? sfit : a.fitness;
   if (threadIdx.x == 0) {
-    double m = -1.0, sum = 0.0;
-    int64_t arg = INT64_MAX;
-    for (int i = 0; i < a.n_parts; ++i) {
-      const double pm = a.part_max[i];
-      if (pm > m || (pm == m && a.part_arg[i] < arg)) {
-        m = pm;
-        arg = a.part_arg[i];
-      }
-      sum += a.part_sum[i];
-    }
-    const int improved = m > st->best_fitness;
-    if (improved) st->best_fitness = m;
-    st->elite = arg;
-    st->improved = improved;
-    GenRecord r;
-    r.gen_best = m;
-    r.gen_mean = sum / (double)a.P;
-    r.best_fitness = st->best_fitness;
-    r.pad = 0.0;
-    const uint64_t ri = st->generation - st->rec_base;
-    if (ri < (uint64_t)a.rec_cap) a.records[ri] = r;
-    s_improved = improved;
-    s_elite = arg;
+    ga_reduce_final(a, s_improved, s_elite);
 
     // ---- sus_select(fitnesses, P, stream) ----
     NpStream rs;
@@ -248,6 +259,40 @@ __global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
   __shared__ double pointers[kSusCache];
   if (a.st->stop) return;
   ga_reduce_sus_body(a, &s_improved, &s_elite, NoIdleWork(), pointers, kSusCache);
+}
+
+// P > kSusCache: the same selection on a whole block (sus.cuh): numpy's
+// pairwise total by subtrees, the two running sums on two threads over
+// staged tiles, then sus_search_kernel writes the parents (unless every
+// fitness is zero: then the uniform draws are written here and the flag
+// tells the search to skip).
+__global__ void __launch_bounds__(kSusThreads) ga_reduce_sus_large_kernel(GaArgs a) {
+  __shared__ int s_improved;
+  __shared__ int64_t s_elite;
+  __shared__ double sm[kSusThreads];
+  if (a.st->stop) return;
+  if (threadIdx.x == 0) ga_reduce_final(a, s_improved, s_elite);
+  const double total = np_pairwise_sum_block<kSusThreads>(a.fitness, a.P, sm);  // syncs first
+  NpStream rs;
+  rs.init(a.seed, DOM_GA_SUS, a.st->generation, 0, 0);
+  if (total <= 0.0) {
+    if (threadIdx.x == 0) {
+      for (int64_t k = 0; k < a.P; ++k) a.parents[k] = (int32_t)rs.integers(a.P);
+      *a.sus_flag = 0;
+    }
+  } else {
+    const double spacing = __ddiv_rn(total, (double)a.P);
+    const double pointer = rs.uniform(0.0, spacing);
+    sus_chains_block(a.fitness, a.P - 1, pointer, spacing, a.P, a.sus_C, a.sus_P);
+    if (threadIdx.x == 0) *a.sus_flag = 1;
+  }
+  if (s_improved && threadIdx.x < 32) {
+    const int cur = ga_cur(a);
+    for (int j = threadIdx.x; j < a.L; j += 32) {
+      a.best_codes[j] = a.codes[cur][s_elite * a.L + j];
+      a.best_thetas[j] = a.thetas[cur][s_elite * a.L + j];
+    }
+  }
 }
 
 // ----------------------------------------------------------------- breed ---
@@ -430,6 +475,9 @@ static void ga_free(GaHandle* h) {
   cudaFree(a.part_max);
   cudaFree(a.part_sum);
   cudaFree(a.part_arg);
+  cudaFree(a.sus_C);
+  cudaFree(a.sus_P);
+  cudaFree(a.sus_flag);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -809,7 +857,13 @@ static isq_status ga_launch_finish(const GaArgs& a, cudaStream_t s) {
     return ISQ_OK;
   }
   ga_reduce_partials<<<a.n_parts, kGaRed, 0, s>>>(a);
-  ga_reduce_sus_kernel<<<1, kGaRed, 0, s>>>(a);
+  if (a.P > kSusCache) {
+    ga_reduce_sus_large_kernel<<<1, kSusThreads, 0, s>>>(a);
+    sus_search_kernel<int32_t><<<ga_blocks(a.P), 256, 0, s>>>(a.sus_C, a.P - 1, a.sus_P, a.P, a.parents,
+                                                              a.sus_flag, &a.st->stop);
+  } else {
+    ga_reduce_sus_kernel<<<1, kGaRed, 0, s>>>(a);
+  }
   ga_breed_kernel<<<ga_blocks(a.P * a.L), 256, 0, s>>>(a);
   ga_advance_kernel<<<1, 1, 0, s>>>(a);
   ISQ_CUDA_TRY(cudaGetLastError());
@@ -907,6 +961,11 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
   GA_TRY(cudaMalloc((void**)&a.part_max, a.n_parts * 8));
   GA_TRY(cudaMalloc((void**)&a.part_sum, a.n_parts * 8));
   GA_TRY(cudaMalloc((void**)&a.part_arg, a.n_parts * 8));
+  if (a.P > kSusCache) {
+    GA_TRY(cudaMalloc((void**)&a.sus_C, a.P * 8));
+    GA_TRY(cudaMalloc((void**)&a.sus_P, a.P * 8));
+    GA_TRY(cudaMalloc((void**)&a.sus_flag, sizeof(int)));
+  }
   GA_TRY(cudaMemcpy((void*)a.target, target, D * D * 16, cudaMemcpyHostToDevice));
   GaDevState s0;
   std::memset(&s0, 0, sizeof(s0));

@@ -421,29 +421,60 @@ __device__ __forceinline__ int measure_axis(const double qre[3], const double qi
 // pairwise_sum in numpy/_core/src/umath/loops_utils.h.src: blocks of 8
 // partial sums below 128 elements, recursive halving above), so device
 // reductions that the reference computes with np.sum round identically.
-__device__ inline double np_pairwise_sum(const double* a, int64_t n) {
+__device__ inline double np_pairwise_leaf(const double* a, int64_t n) {  // n <= 128
   if (n < 8) {
     double r = 0.0;
     for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
     return r;
   }
-  if (n <= 128) {
-    double r[8];
+  double r[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8) {
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
   }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// The recursion S(a, n) = S(a, h) + S(a + h, n - h), h = n/2 rounded down
+// to a multiple of 8, as an explicit post-order walk (a device recursion
+// overflowed the default 1 KB thread stack from n = 2^17).
+__device__ inline double np_pairwise_sum(const double* a, int64_t n) {
+  if (n <= 128) return np_pairwise_leaf(a, n);
+  int64_t r_off[40], r_len[40];  // right subtree still to sum, per pending node
+  double left[40];                // (depth <= log2(n / 128) + 1 < 40)
+  uint64_t has_left = 0;          // bit: the pending node's left sum is in left[]
+  int sp = 0;
+  int64_t off = 0, m = n;
+  for (;;) {
+    while (m > 128) {  // descend left, remembering the right halves
+      int64_t h = m / 2;
+      h -= h % 8;
+      r_off[sp] = off + h;
+      r_len[sp] = m - h;
+      has_left &= ~(1ull << sp);
+      ++sp;
+      m = h;
+    }
+    double acc = np_pairwise_leaf(a + off, m);
+    for (;;) {
+      if (sp == 0) return acc;
+      if (!((has_left >> (sp - 1)) & 1)) {  // left child done: sum the right one next
+        has_left |= 1ull << (sp - 1);
+        left[sp - 1] = acc;
+        off = r_off[sp - 1];
+        m = r_len[sp - 1];
+        break;
+      }
+      acc = __dadd_rn(left[sp - 1], acc);  // both children done
+      --sp;
+    }
+  }
 }
 
 }  // namespace isq

@@ -253,6 +253,26 @@ def test_ga_operators_match_reference_goldens(name):
         assert sus_select(list(g["fitness"][gen]), P, CounterStreams(seed, gen)) == list(g["parents"][gen])
 
 
+def test_sus_select_at_large_populations_matches_reference():
+    """The block SUS (sus.cuh: pairwise total by subtrees, the two running sums
+    on staged tiles, the picks by binary search) against the reference's own
+    picks, P = 600 .. 300k, count = P / about P/2 / 2P, with zeros and ties
+    (oracle/gen_golden_sus.py)."""
+    import hashlib
+
+    from oracle.targets import sus_fitness
+    from paper_1809_11134_b200 import CounterStreams, sus_select
+
+    g = golden("sus_large")
+    names = sorted({k.rsplit("_", 1)[0] for k in g.files})
+    for name in names:
+        P, count, seed, gen = (int(x) for x in g[name + "_meta"])
+        f = sus_fitness(P, seed, str(g[name + "_kind"]))
+        picks = np.asarray(sus_select(f, count, CounterStreams(seed, gen)), dtype=np.int64)
+        assert np.array_equal(picks[:64], g[name + "_head"]) and np.array_equal(picks[-64:], g[name + "_tail"]), name
+        assert hashlib.sha256(picks.astype("<i8").tobytes()).hexdigest() == str(g[name + "_sha"]), name
+
+
 def test_sus_all_zero_falls_back_to_uniform_draws():
     from paper_1809_11134_b200 import CounterStreams, sus_select
 

@@ -113,3 +113,22 @@ def test_ga_batched_steps_equal_single_steps(mode):
     ca, ta = a.genome_arrays()
     cb, tb = b.genome_arrays()
     assert np.array_equal(ca, cb) and np.array_equal(ta, tb)
+
+
+@pytest.mark.parametrize("P", [513, 1 << 17])
+def test_large_population_parents_match_the_oracle_walk(P):
+    """P > 512 selects on the block SUS + search kernels (kernels_ga.cu
+    ga_reduce_sus_large_kernel); its parents must be the sequential walk's
+    (oracle/ga.sus_select, pinned to the reference by tests/golden/sus_large)
+    on the engine's own fitness, generation by generation."""
+    from oracle.ga import sus_select
+    from oracle.streams import DOM_GA_SUS, stream
+    from paper_1809_11134_b200 import GaConfig, GaEngine, target_matrix
+
+    eng = GaEngine(GaConfig(2, 4, P, max_generations=100, target_fitness=1.0), target_matrix("CNOT"), 5)
+    eng.set_launch_mode("kernels")
+    for gen in range(3):
+        eng.step()
+        fit = eng.last_fitness()
+        want = sus_select(list(map(float, fit)), P, stream(5, DOM_GA_SUS, gen))
+        assert np.array_equal(eng.last_parents(), np.asarray(want)), gen

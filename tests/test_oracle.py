@@ -195,3 +195,26 @@ def test_binomial_restatement_matches_numpy():
         pr = np.abs(q) ** 2
         pr /= pr.sum()
         assert list(stream(7, 2, trial, 1).multinomial(n, pr)) == multinomial3(stream(7, 2, trial, 1), n, list(pr))
+
+
+def _sus_cases():
+    g = golden("sus_large")
+    return g, sorted({k.rsplit("_", 1)[0] for k in g.files})
+
+
+def test_oracle_sus_select_matches_reference_at_large_populations():
+    """oracle/ga.sus_select (the restatement the device is checked against)
+    against the reference's own picks at P up to 300k (oracle/gen_golden_sus.py)."""
+    import hashlib
+
+    from oracle.streams import DOM_GA_SUS
+    from oracle.targets import sus_fitness
+
+    g, names = _sus_cases()
+    assert len(names) == 5
+    for name in names:
+        P, count, seed, gen = (int(x) for x in g[name + "_meta"])
+        f = sus_fitness(P, seed, str(g[name + "_kind"]))
+        assert float(np.sum(list(map(float, f)))) == float(g[name + "_total"])
+        picks = np.asarray(OG.sus_select(list(map(float, f)), count, stream(seed, DOM_GA_SUS, gen)), dtype=np.int64)
+        assert hashlib.sha256(picks.astype("<i8").tobytes()).hexdigest() == str(g[name + "_sha"]), name
