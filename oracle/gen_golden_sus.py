@@ -24,6 +24,10 @@ CASES = [  # (name, P, count, kind, seed, generation)
     ("p131k_ties_half", 131_072, 65_537, "ties", 13, 1),
     ("p200k_skewed_double", 200_003, 400_000, "skewed", 14, 0),
     ("p600_ties", 600, 600, "ties", 15, 2),
+    ("p131k_dyadic_pow2", 131_072, 131_072, "dyadic", 16, 4),
+    ("p100k_range", 100_000, 100_000, "range", 17, 5),
+    ("p1m_skewed", 1_048_576, 1_048_576, "skewed", 18, 6),
+    ("p100k_tie40", 100_000, 65_536, "tie40", 19, 8),
 ]
 
 

@@ -44,4 +44,21 @@ def sus_fitness(P: int, seed: int, kind: str) -> np.ndarray:
         return f
     if kind == "ties":
         return rng.integers(0, 5, P) * 0.125
+    if kind in ("range", "dyadic", "tie40"):
+        return sus_fitness_extra(P, seed, kind)
+    raise ValueError(kind)
+
+
+def sus_fitness_extra(P: int, seed: int, kind: str) -> np.ndarray:
+    """More SUS fixtures: `range` spans 1e-300 .. 1 (many binade crossings,
+    subnormal-free), `dyadic` are multiples of 1/8 with a power-of-two count
+    (an exactly dyadic spacing: a whole binade of exact rounding ties in the
+    pointer sum)."""
+    rng = np.random.default_rng(seed)
+    if kind == "range":
+        return 10.0 ** rng.uniform(-300.0, 0.0, P)
+    if kind == "dyadic":
+        return rng.integers(1, 9, P) * 0.125
+    if kind == "tie40":  # k 2^-40: while the running sum is in [2^13, 2^14), half the adds are exact ties
+        return rng.integers(1, 1 << 40, P).astype(np.float64) * 2.0 ** -40
     raise ValueError(kind)

@@ -284,13 +284,18 @@ __global__ void fn_ga_random_genomes_kernel(int L, int ncodes, uint64_t seed, in
   }
 }
 
-// sus_select (ga.py:95-116) on one block (sus.cuh): numpy's pairwise total,
-// the walk's two running sums in their own rounding, then sus_search_kernel
-// (skipped through *flag when every fitness is zero: uniform draws here).
+// sus_select (ga.py:95-116) on two blocks (sus.cuh): block 0 the cumulative
+// sums C[1..P-1], block 1 numpy's pairwise total and the pointers (or the
+// uniform draws when every fitness is zero: *flag = 0 skips the search).
 __global__ void __launch_bounds__(kSusThreads)
     fn_ga_sus_kernel(const double* f, int64_t P, int64_t count, uint64_t seed, uint64_t g, int64_t* picks,
                      double* C, double* Pt, int* flag) {
   __shared__ double sm[kSusThreads];
+  extern __shared__ double chain_smem[];
+  if (blockIdx.x == 0) {
+    exact_chain_block(f, 0.0, P - 1, 0.0, C, chain_smem);
+    return;
+  }
   const double total = np_pairwise_sum_block<kSusThreads>(f, P, sm);
   NpStream rs;
   rs.init(seed, DOM_GA_SUS, g, 0, 0);
@@ -303,8 +308,11 @@ __global__ void __launch_bounds__(kSusThreads)
   }
   const double spacing = __ddiv_rn(total, (double)count);
   const double pointer = rs.uniform(0.0, spacing);
-  sus_chains_block(f, P - 1, pointer, spacing, count, C, Pt);
-  if (threadIdx.x == 0) *flag = 1;
+  if (threadIdx.x == 0) {
+    Pt[0] = pointer;
+    *flag = 1;
+  }
+  exact_const_chain_block(spacing, count - 1, pointer, Pt + 1);
 }
 
 // two_point_crossover cuts (ga.py:81-92): sorted(integers(0, L + 1, size=2)), no draw for L < 2.
@@ -581,7 +589,9 @@ isq_status isq_ga_sus_select(int64_t P, const double* fitness, int64_t count, ui
   TRYF(dC.alloc(P * 8));
   TRYF(dP.alloc(count * 8));
   TRYF(dflag.alloc(sizeof(int)));
-  fn_ga_sus_kernel<<<1, kSusThreads>>>(df.as<double>(), P, count, seed, generation, dp.as<int64_t>(),
+  TRYF(cudaFuncSetAttribute((const void*)fn_ga_sus_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kChainSmem));
+  fn_ga_sus_kernel<<<2, kSusThreads, kChainSmem>>>(df.as<double>(), P, count, seed, generation, dp.as<int64_t>(),
                                        dC.as<double>(), dP.as<double>(), dflag.as<int>());
   TRYF(cudaGetLastError());
   sus_search_kernel<int64_t><<<grid_for(count), 256>>>(dC.as<double>(), P - 1, dP.as<double>(), count,

@@ -261,18 +261,32 @@ __global__ void __launch_bounds__(kGaRed) ga_reduce_sus_kernel(GaArgs a) {
   ga_reduce_sus_body(a, &s_improved, &s_elite, NoIdleWork(), pointers, kSusCache);
 }
 
-// P > kSusCache: the same selection on a whole block (sus.cuh): numpy's
-// pairwise total by subtrees, the two running sums on two threads over
-// staged tiles, then sus_search_kernel writes the parents (unless every
-// fitness is zero: then the uniform draws are written here and the flag
-// tells the search to skip).
+// P > kSusCache: the same selection on two blocks (sus.cuh).  Block 0: the
+// final reduction and record, then the cumulative sums C[1..P-1] and the
+// elite copy; block 1: numpy's pairwise total, then the pointer sequence (or,
+// when every fitness is zero, the uniform draws, with the flag telling
+// sus_search_kernel to skip).  The running sums are exact-parallel
+// (exact_chain_block), bit-identical to the sequential walk.
 __global__ void __launch_bounds__(kSusThreads) ga_reduce_sus_large_kernel(GaArgs a) {
   __shared__ int s_improved;
   __shared__ int64_t s_elite;
   __shared__ double sm[kSusThreads];
+  extern __shared__ double chain_smem[];
   if (a.st->stop) return;
-  if (threadIdx.x == 0) ga_reduce_final(a, s_improved, s_elite);
-  const double total = np_pairwise_sum_block<kSusThreads>(a.fitness, a.P, sm);  // syncs first
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) ga_reduce_final(a, s_improved, s_elite);
+    exact_chain_block(a.fitness, 0.0, a.P - 1, 0.0, a.sus_C, chain_smem);
+    __syncthreads();  // s_improved / s_elite
+    if (s_improved && threadIdx.x < 32) {
+      const int cur = ga_cur(a);
+      for (int j = threadIdx.x; j < a.L; j += 32) {
+        a.best_codes[j] = a.codes[cur][s_elite * a.L + j];
+        a.best_thetas[j] = a.thetas[cur][s_elite * a.L + j];
+      }
+    }
+    return;
+  }
+  const double total = np_pairwise_sum_block<kSusThreads>(a.fitness, a.P, sm);
   NpStream rs;
   rs.init(a.seed, DOM_GA_SUS, a.st->generation, 0, 0);
   if (total <= 0.0) {
@@ -280,19 +294,15 @@ __global__ void __launch_bounds__(kSusThreads) ga_reduce_sus_large_kernel(GaArgs
       for (int64_t k = 0; k < a.P; ++k) a.parents[k] = (int32_t)rs.integers(a.P);
       *a.sus_flag = 0;
     }
-  } else {
-    const double spacing = __ddiv_rn(total, (double)a.P);
-    const double pointer = rs.uniform(0.0, spacing);
-    sus_chains_block(a.fitness, a.P - 1, pointer, spacing, a.P, a.sus_C, a.sus_P);
-    if (threadIdx.x == 0) *a.sus_flag = 1;
+    return;
   }
-  if (s_improved && threadIdx.x < 32) {
-    const int cur = ga_cur(a);
-    for (int j = threadIdx.x; j < a.L; j += 32) {
-      a.best_codes[j] = a.codes[cur][s_elite * a.L + j];
-      a.best_thetas[j] = a.thetas[cur][s_elite * a.L + j];
-    }
+  const double spacing = __ddiv_rn(total, (double)a.P);
+  const double pointer = rs.uniform(0.0, spacing);
+  if (threadIdx.x == 0) {
+    a.sus_P[0] = pointer;
+    *a.sus_flag = 1;
   }
+  exact_const_chain_block(spacing, a.P - 1, pointer, a.sus_P + 1);
 }
 
 // ----------------------------------------------------------------- breed ---
@@ -858,7 +868,7 @@ static isq_status ga_launch_finish(const GaArgs& a, cudaStream_t s) {
   }
   ga_reduce_partials<<<a.n_parts, kGaRed, 0, s>>>(a);
   if (a.P > kSusCache) {
-    ga_reduce_sus_large_kernel<<<1, kSusThreads, 0, s>>>(a);
+    ga_reduce_sus_large_kernel<<<2, kSusThreads, kChainSmem, s>>>(a);
     sus_search_kernel<int32_t><<<ga_blocks(a.P), 256, 0, s>>>(a.sus_C, a.P - 1, a.sus_P, a.P, a.parents,
                                                               a.sus_flag, &a.st->stop);
   } else {
@@ -962,6 +972,8 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
   GA_TRY(cudaMalloc((void**)&a.part_sum, a.n_parts * 8));
   GA_TRY(cudaMalloc((void**)&a.part_arg, a.n_parts * 8));
   if (a.P > kSusCache) {
+    GA_TRY(cudaFuncSetAttribute((const void*)ga_reduce_sus_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kChainSmem));
     GA_TRY(cudaMalloc((void**)&a.sus_C, a.P * 8));
     GA_TRY(cudaMalloc((void**)&a.sus_P, a.P * 8));
     GA_TRY(cudaMalloc((void**)&a.sus_flag, sizeof(int)));

@@ -13,23 +13,23 @@
 // first j <= P-2 with C[j+1] > p[k] (else P-1).  Here:
 //   * np.sum's pairwise tree (numpy's pairwise_sum: 8 accumulators below 128
 //     elements, halving at a multiple of 8 above) is evaluated by a block:
-//     the recursion's top levels are expanded into up to 2^8 subtrees, one
+//     the recursion's top levels are expanded into up to 2^10 subtrees, one
 //     per thread (np_pairwise_sum, iterative), then combined level by level
 //     in the recursion's own order -- bit-identical to the sequential sum;
-//   * the two recurrences run on two threads of different warps (the only
-//     sequential part left: one dependent add per element) over
-//     shared-memory tiles the other warps load and store, double-buffered;
+//   * the two recurrences are evaluated exactly in parallel (exact_chain_block:
+//     integer prefix sums on each binade's grid, plain adds only where the
+//     grid form does not hold), one block each;
 //   * the picks are a grid-wide binary search over C (sus_search_kernel).
 #pragma once
 
+#include <climits>
 #include <cstdint>
 
 #include "np_random.cuh"
 
 namespace isq {
 
-constexpr int kSusThreads = 512;  // block of sus_chains_block / np_pairwise_sum_block
-constexpr int kSusTile = 1024;    // elements per staged tile (2 buffers x (f/C + p) = 32 KB)
+constexpr int kSusThreads = 1024;  // block of exact_chain_block / np_pairwise_sum_block
 
 // Node `i` (d path bits, most significant first: 0 = left) of numpy's
 // pairwise recursion over n elements: its offset and length.
@@ -48,15 +48,16 @@ __device__ __forceinline__ void pairwise_node(int64_t n, int d, int i, int64_t& 
   }
 }
 
-// np.sum(a[0..n)) on a whole block of kThreads (>= 256) threads; `sm` holds
+// np.sum(a[0..n)) on a whole block of kThreads (a power of two >= 256) threads; `sm` holds
 // kThreads doubles.  Every thread returns the total.
 template <int kThreads>
 __device__ double np_pairwise_sum_block(const double* a, int64_t n, double* sm) {
-  static_assert(kThreads >= 256, "the expansion uses up to 256 subtrees");
+  static_assert(kThreads >= 256 && (kThreads & (kThreads - 1)) == 0, "a power of two >= 256");
+  constexpr int kMaxD = __builtin_ctz(kThreads);  // up to one subtree per thread
   // depth d: 2^d subtrees, every node above them internal (> 128 elements);
   // node lengths at depth d are >= n / 2^d - 8 d
   int d = 0;
-  while (d < 8 && (n >> (d + 1)) >= 256) ++d;
+  while (d < kMaxD && (n >> (d + 1)) >= 256) ++d;
   const int nodes = 1 << d;
   if ((int)threadIdx.x < nodes) {
     int64_t off, m;
@@ -76,68 +77,345 @@ __device__ double np_pairwise_sum_block(const double* a, int64_t n, double* sm) 
   return total;
 }
 
-// Cg[j] = C[j+1] for j < nf and Pg[k] = p[k] for k < np, in the walk's own
-// rounding, on a block of kSusThreads: thread 0 runs the C chain, thread 32
-// the pointer chain, warps 2.. stage the tiles (load f of tile t+1, store
-// tile t-1) while the chains run on tile t.
-__device__ inline void sus_chains_block(const double* f, int64_t nf, double pointer, double spacing, int64_t np,
-                                 double* Cg, double* Pg) {
-  __shared__ double X[2][kSusTile];  // f of a tile, overwritten in place by C
-  __shared__ double Y[2][kSusTile];  // pointers of a tile
-  const int tid = threadIdx.x;
-  const int64_t len = nf > np ? nf : np;
-  const int64_t ntiles = (len + kSusTile - 1) / kSusTile;
-  constexpr int kStagers = kSusThreads - 64;
-  const int sid = tid - 64;
-  auto load = [&](int64_t t, int b) {
-    const int64_t base = t * kSusTile;
-    for (int i = sid; i < kSusTile; i += kStagers)
-      if (base + i < nf) X[b][i] = f[base + i];
-  };
-  auto store = [&](int64_t t, int b) {
-    const int64_t base = t * kSusTile;
-    for (int i = sid; i < kSusTile; i += kStagers) {
-      if (base + i < nf) Cg[base + i] = X[b][i];
-      if (base + i < np) Pg[base + i] = Y[b][i];
+// ------------------------------------------------------------------------
+// A sequentially rounded running sum, evaluated in parallel and exactly:
+//   x[i+1] = RN(x[i] + f[i])          out[i] = x[i+1],  i < n
+// (f[i] >= 0; f == nullptr: every f[i] = fconst).  Write x = (2^52 + K) u +
+// 0 with K its mantissa field and u = 2^(E-1075) its ulp (E the biased
+// exponent).  While x stays in one binade, RN(x + f) only moves K along that
+// grid: with f/u = g + r (g integer, 0 <= r < 1)
+//   r != 1/2:  K -> K + G,  G = g + (r > 1/2)
+//   r == 1/2:  K -> even(K + g)   (round half to even: the even of K+g, K+g+1)
+// as long as x + f < 2^(E-1022) - u/2.  Both maps are of the form
+// K -> even(K + a) + b or K -> K + a, a family closed under composition
+// (even(even(y) + k) = even(y) + even(k)), so a tile is one block-wide scan of
+// these maps applied to the tile's starting K -- up to the first element that
+// leaves the binade or meets a subnormal-range x.  That element (and, while
+// the parallel form keeps stopping early -- the first doublings of x -- a
+// growing run after it) is added by one thread with the plain RN add.  Every
+// accepted value is the double with exponent E and mantissa K, so the result
+// is bit-identical to the sequential loop.  Tiles of 8192 elements are
+// staged in shared memory (coalesced loads and stores; each thread owns 8
+// contiguous elements).
+constexpr int kChainE = 8;                         // elements per thread per tile
+constexpr int kChainTile = kSusThreads * kChainE;  // 8192
+constexpr uint64_t kChainSat = 1ull << 60;         // saturation (any K >= 2^52 is out of the binade)
+constexpr int kChainGoodRun = 64;                  // a parallel run this long resets the scalar budget
+constexpr int kChainWarm = 2048;                   // plain adds at least this far (a parallel attempt costs ~1.5k)
+constexpr int kChainMaxBudget = 1 << 16;
+
+// Dynamic shared memory of a kernel calling exact_chain_block: one padded tile.
+constexpr size_t kChainSmem = (size_t)(kChainTile + kChainTile / 8) * sizeof(double);
+__device__ __forceinline__ int chain_pad(int i) { return i + (i >> 3); }  // rows of 8, stride 9: conflict-free
+
+__device__ __forceinline__ uint64_t chain_sat(uint64_t v) { return v > kChainSat ? kChainSat : v; }
+__device__ __forceinline__ uint64_t chain_even(uint64_t v) { return v + (v & 1); }
+
+// K -> e ? even(K + a) + b : K + a
+struct ChainMap {
+  uint64_t a, b;
+  bool e;
+};
+__device__ __forceinline__ ChainMap chain_then(const ChainMap& f1, const ChainMap& f2) {  // f1, then f2
+  if (!f2.e) return f1.e ? ChainMap{f1.a, chain_sat(f1.b + f2.a), true} : ChainMap{chain_sat(f1.a + f2.a), 0, false};
+  if (!f1.e) return ChainMap{chain_sat(f1.a + f2.a), f2.b, true};
+  return ChainMap{f1.a, chain_sat(chain_even(f1.b + f2.a) + f2.b), true};
+}
+__device__ __forceinline__ uint64_t chain_apply(const ChainMap& f, uint64_t K) {
+  return f.e ? chain_sat(chain_even(chain_sat(K + f.a)) + f.b) : chain_sat(K + f.a);
+}
+__device__ __forceinline__ ChainMap chain_shfl_up(const ChainMap& m, int o) {
+  ChainMap r;
+  r.a = __shfl_up_sync(0xffffffffu, m.a, o);
+  r.b = __shfl_up_sync(0xffffffffu, m.b, o);
+  r.e = __shfl_up_sync(0xffffffffu, (int)m.e, o) != 0;
+  return r;
+}
+
+#ifdef ISQ_SUS_PROFILE
+// per block: parallel attempts, scalar elements, parallel cycles, scalar cycles
+__device__ unsigned long long g_sus_prof[2][4];
+#define SUS_PROF(k, v) \
+  if (threadIdx.x == 0) atomicAdd(&g_sus_prof[blockIdx.x & 1][k], (unsigned long long)(v))
+#else
+#define SUS_PROF(k, v)
+#endif
+
+// `sbuf`: kChainSmem bytes of shared memory.
+__device__ inline void exact_chain_block(const double* f, double fconst, int64_t n, double x0, double* out,
+                                         double* sbuf) {
+  __shared__ ChainMap s_warp[kSusThreads / 32];
+  __shared__ int s_stop, s_pos, s_budget;
+  __shared__ bool s_warm;
+  __shared__ double s_x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double x = x0;
+  int budget = 1;   // elements still to add on one thread before the next parallel attempt
+  int grow = 16;    // the budget after a short parallel run (doubles while they stay short)
+  bool warm = true; // the first doublings of x: plain adds (see the scalar branch)
+  bool warm_done = false;
+  for (int64_t j = 0; j < n; j += kChainTile) {
+    const int len = (int)(n - j < kChainTile ? n - j : kChainTile);
+#pragma unroll
+    for (int k = 0; k < kChainE; ++k) {  // coalesced tile load (the constant chain stages nothing)
+      const int i = k * kSusThreads + tid;
+      if (f != nullptr && i < len) sbuf[chain_pad(i)] = f[j + i];
     }
-  };
-  if (tid >= 64 && ntiles > 0) load(0, 0);
-  __syncthreads();
-  double c = 0.0, p = pointer;
-  for (int64_t t = 0; t < ntiles; ++t) {
-    const int b = (int)(t & 1);
-    const int64_t base = t * kSusTile;
-    if (tid == 0) {
-      const int m = (int)(nf - base < kSusTile ? (nf - base > 0 ? nf - base : 0) : kSusTile);
-      int i = 0;
-      for (; i + 8 <= m; i += 8) {
-        double x[8];
+    __syncthreads();
+    int pos = 0;
+    while (pos < len) {
+      if (budget > 0) {  // plain adds on thread 0, in shared memory
+#ifdef ISQ_SUS_PROFILE
+        const long long t0 = clock64();
+#endif
+        if (tid == 0) {
+          int end = pos + budget < len ? pos + budget : len;
+          int i = pos;
+          if (warm) {  // warm-up: to the first binade change after kChainWarm elements (a parallel
+                       // attempt then starts a binade and covers as many elements as came before)
+            const int e0 = (int)((uint64_t)__double_as_longlong(x) >> 52);
+            end = len;
+            for (; i < len; ++i) {
+              x = __dadd_rn(x, f ? sbuf[chain_pad(i)] : fconst);
+              sbuf[chain_pad(i)] = x;
+              if (j + i + 1 >= kChainWarm && (int)((uint64_t)__double_as_longlong(x) >> 52) != e0) {
+                ++i;
+                end = i;
+                warm_done = true;
+                break;
+              }
+            }
+          }
+          for (; i + 8 <= end; i += 8) {
+            double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = X[b][i + u];
+            for (int k = 0; k < 8; ++k) v[k] = f ? sbuf[chain_pad(i + k)] : fconst;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          c = __dadd_rn(c, x[u]);
-          X[b][i + u] = c;
+            for (int k = 0; k < 8; ++k) {
+              x = __dadd_rn(x, v[k]);
+              sbuf[chain_pad(i + k)] = x;
+            }
+          }
+          for (; i < end; ++i) {
+            x = __dadd_rn(x, f ? sbuf[chain_pad(i)] : fconst);
+            sbuf[chain_pad(i)] = x;
+          }
+          s_x = x;
+          s_pos = end;
+          s_budget = warm ? (warm_done ? 0 : 1) : budget - (end - pos);
+          s_warm = warm && !warm_done;
+        }
+        __syncthreads();
+        SUS_PROF(1, s_pos - pos);
+        SUS_PROF(3, clock64() - t0);
+        x = s_x;
+        pos = s_pos;
+        budget = s_budget;
+        warm = s_warm;
+        __syncthreads();
+        continue;
+      }
+      // parallel attempt on [pos, len)
+#ifdef ISQ_SUS_PROFILE
+      const long long t1 = clock64();
+#endif
+      const bool par = x >= 0x1p-900;  // block-uniform
+      const uint64_t xb = (uint64_t)__double_as_longlong(x);
+      const int E = (int)((xb >> 52) & 0x7ff);
+      const int ue = E - 1075;                          // u = 2^ue
+      const uint64_t K0 = xb & ((1ull << 52) - 1);
+      if (tid == 0) s_stop = par ? len : pos;
+      const int i0 = tid * kChainE;
+      ChainMap op[kChainE];
+      uint64_t F2[kChainE];  // floor(2 f/u)
+      ChainMap mine{0, 0, false};
+      int my_stop = INT32_MAX;
+#pragma unroll
+      for (int e = 0; e < kChainE; ++e) {
+        const int i = i0 + e;
+        op[e] = ChainMap{0, 0, false};
+        F2[e] = 0;
+        if (par && i >= pos && i < len) {
+          const uint64_t fb = (uint64_t)__double_as_longlong(f ? sbuf[chain_pad(i)] : fconst);
+          const int ex = (int)((fb >> 52) & 0x7ff);
+          const uint64_t m = (fb & ((1ull << 52) - 1)) | (ex ? (1ull << 52) : 0ull);  // f = m 2^(ex-1075)
+          const int shift = ue - (ex ? ex - 1075 : -1074);
+          if (ex == 0x7ff || (m != 0 && shift <= 0)) {
+            my_stop = min(my_stop, i);  // inf / nan, or f >= 2^52 u: leaves the binade
+          } else if (m != 0 && shift < 64) {
+            const uint64_t g0 = m >> shift, rem = m & ((1ull << shift) - 1), half = 1ull << (shift - 1);
+            if (g0 >= (1ull << 52)) my_stop = min(my_stop, i);
+            op[e] = rem == half ? ChainMap{g0, 0, true} : ChainMap{g0 + (rem > half ? 1u : 0u), 0, false};
+            F2[e] = m >> (shift - 1);
+          }  // shift >= 64: f < u / 2^10, the identity map
+          mine = chain_then(mine, op[e]);
         }
       }
-      for (; i < m; ++i) {
-        c = __dadd_rn(c, X[b][i]);
-        X[b][i] = c;
+      // exclusive block scan of the per-thread maps
+      ChainMap incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const ChainMap v = chain_shfl_up(incl, o);
+        if (lane >= o) incl = chain_then(v, incl);
       }
-    } else if (tid == 32) {
-      const int m = (int)(np - base < kSusTile ? (np - base > 0 ? np - base : 0) : kSusTile);
-      for (int i = 0; i < m; ++i) {
-        Y[b][i] = p;
-        p = __dadd_rn(p, spacing);
+      if (lane == 31) s_warp[wid] = incl;
+      ChainMap excl = chain_shfl_up(incl, 1);
+      if (lane == 0) excl = ChainMap{0, 0, false};
+      __syncthreads();
+      if (wid == 0) {  // exclusive scan of the warp totals
+        ChainMap w = lane < kSusThreads / 32 ? s_warp[lane] : ChainMap{0, 0, false};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const ChainMap v = chain_shfl_up(w, o);
+          if (lane >= o) w = chain_then(v, w);
+        }
+        ChainMap ex = chain_shfl_up(w, 1);
+        if (lane == 0) ex = ChainMap{0, 0, false};
+        if (lane < kSusThreads / 32) s_warp[lane] = ex;
       }
-    } else if (tid >= 64) {
-      if (t >= 1) store(t - 1, b ^ 1);
-      if (t + 1 < ntiles) load(t + 1, b ^ 1);
+      __syncthreads();
+      const ChainMap pre = chain_then(s_warp[wid], excl);
+      // binade check on each element's starting K: x[i] + f[i] < 2^(E-1022) - u/2
+      //   <=>  floor(2 f/u) < 2^53 - 1 - 2 K[i]
+      uint64_t Kst = chain_apply(pre, K0);
+      if (par) {
+        uint64_t k = Kst;
+#pragma unroll
+        for (int e = 0; e < kChainE; ++e) {
+          const int i = i0 + e;
+          if (i >= pos && i < len && i < my_stop) {
+            if (k >= (1ull << 52) || F2[e] >= (1ull << 53) - 1 - 2 * k) my_stop = min(my_stop, i);
+            k = chain_apply(op[e], k);
+            F2[e] = k;  // K[i+1], for the accept pass
+          }
+        }
+        if (my_stop < len) atomicMin(&s_stop, my_stop);
+      }
+      __syncthreads();
+      const int stop = s_stop;
+      if (par) {  // accepted [pos, stop) (all checked above: stop <= every my_stop): exponent E, mantissa K[i+1]
+#pragma unroll
+        for (int e = 0; e < kChainE; ++e) {
+          const int i = i0 + e;
+          if (i >= pos && i < stop) {
+            const double v = __longlong_as_double((long long)(((uint64_t)E << 52) | F2[e]));
+            sbuf[chain_pad(i)] = v;
+            if (i == stop - 1) s_x = v;
+          }
+        }
+      }
+      __syncthreads();
+      if (stop > pos) x = s_x;
+      // a stop: its element on thread 0 next, with a run after it that grows
+      // while the parallel form keeps stopping early
+      if (stop < len) {
+        if (stop - pos >= kChainGoodRun) {
+          grow = 16;
+          budget = 1;
+        } else {
+          grow = min(2 * grow, kChainMaxBudget);
+          budget = grow;
+        }
+      }
+      pos = stop;
+      __syncthreads();
+      SUS_PROF(0, 1);
+      SUS_PROF(2, clock64() - t1);
+    }
+#pragma unroll
+    for (int k = 0; k < kChainE; ++k) {  // coalesced store of the tile
+      const int i = k * kSusThreads + tid;
+      if (i < len) out[j + i] = sbuf[chain_pad(i)];
     }
     __syncthreads();
   }
-  if (tid >= 64 && ntiles > 0) store(ntiles - 1, (int)((ntiles - 1) & 1));
-  __syncthreads();
+#ifdef ISQ_SUS_PROFILE
+  if (tid == 0)
+    printf("exact_chain_block n=%lld const=%d: attempts %llu scalar %llu par_cycles %llu scalar_cycles %llu\n",
+           (long long)n, f == nullptr, g_sus_prof[blockIdx.x & 1][0], g_sus_prof[blockIdx.x & 1][1],
+           g_sus_prof[blockIdx.x & 1][2], g_sus_prof[blockIdx.x & 1][3]);
+#endif
+}
+
+// The same recurrence with a constant increment (the SUS pointers,
+// x[k+1] = RN(x[k] + spacing)): inside a binade every step applies the same
+// map, so K after i steps is closed-form -- K[1] = map(K[0]), then + d per
+// step (d = G, or even(g) for an exact tie: K[1] is even then) -- and the
+// steps that stay in the binade are a prefix counted directly.  One round per
+// binade (plus one plain add for the step that leaves it), the values written
+// by the whole block.
+__device__ inline void exact_const_chain_block(double inc, int64_t n, double x0, double* out) {
+  __shared__ double s_x;
+  __shared__ int64_t s_j, s_m;
+  __shared__ uint64_t s_K1, s_d;
+  __shared__ int s_E;
+  const int tid = threadIdx.x;
+  double x = x0;
+  int64_t j = 0;
+  while (j < n) {
+    if (tid == 0) {
+      int64_t m = 0;
+      uint64_t K1 = 0, d = 0;
+      const uint64_t xb = (uint64_t)__double_as_longlong(x);
+      const int E = (int)((xb >> 52) & 0x7ff);
+      const uint64_t fb = (uint64_t)__double_as_longlong(inc);
+      const int ex = (int)((fb >> 52) & 0x7ff);
+      if (x >= 0x1p-900 && ex != 0x7ff) {
+        const uint64_t K0 = xb & ((1ull << 52) - 1);
+        const uint64_t mm = (fb & ((1ull << 52) - 1)) | (ex ? (1ull << 52) : 0ull);
+        const int shift = (E - 1075) - (ex ? ex - 1075 : -1074);
+        uint64_t F2 = 0;
+        bool ok = true;
+        ChainMap op{0, 0, false};
+        if (mm != 0 && shift <= 0) {
+          ok = false;
+        } else if (mm != 0 && shift < 64) {
+          const uint64_t g0 = mm >> shift, rem = mm & ((1ull << shift) - 1), half = 1ull << (shift - 1);
+          ok = g0 < (1ull << 52);
+          op = rem == half ? ChainMap{g0, 0, true} : ChainMap{g0 + (rem > half ? 1u : 0u), 0, false};
+          F2 = mm >> (shift - 1);
+        }
+        if (ok && F2 < (1ull << 53) - 1) {
+          const uint64_t Kmax = ((1ull << 53) - 2 - F2) / 2;  // a step from K stays inside iff K <= Kmax
+          if (K0 <= Kmax && K0 < (1ull << 52)) {
+            K1 = chain_apply(op, K0);
+            d = op.e ? chain_even(op.a) : op.a;
+            const int64_t rest = n - j;
+            if (K1 > Kmax) {
+              m = 1;
+            } else if (d == 0) {
+              m = rest;
+            } else {
+              const uint64_t more = (Kmax - K1) / d + 1;  // steps 1 .. more start at or below Kmax
+              m = more + 1 >= (uint64_t)rest ? rest : (int64_t)(more + 1);
+            }
+            if (m > rest) m = rest;
+          }
+        }
+        s_E = E;
+      }
+      s_m = m;
+      s_K1 = K1;
+      s_d = d;
+      if (m == 0) {  // the step leaves the binade (or x is in the subnormal range): the plain add
+        x = __dadd_rn(x, inc);
+        out[j] = x;
+        s_x = x;
+      } else {
+        s_x = __longlong_as_double((long long)(((uint64_t)s_E << 52) | (K1 + (uint64_t)(m - 1) * d)));
+      }
+    }
+    __syncthreads();
+    const int64_t m = s_m;
+    if (m > 0) {
+      const uint64_t K1 = s_K1, d = s_d, Eb = (uint64_t)s_E << 52;
+      for (int64_t i = tid; i < m; i += kSusThreads)
+        out[j + i] = __longlong_as_double((long long)(Eb | (K1 + (uint64_t)i * d)));
+    }
+    x = s_x;
+    j += m > 0 ? m : 1;
+    __syncthreads();
+  }
 }
 
 // picks[k] = first j in [0, nC) with C[j] > p[k], else nC (nC = P - 1): where
