@@ -211,7 +211,7 @@ def test_oracle_sus_select_matches_reference_at_large_populations():
     from oracle.targets import sus_fitness
 
     g, names = _sus_cases()
-    assert len(names) == 5
+    assert len(names) == 9
     for name in names:
         P, count, seed, gen = (int(x) for x in g[name + "_meta"])
         f = sus_fitness(P, seed, str(g[name + "_kind"]))
