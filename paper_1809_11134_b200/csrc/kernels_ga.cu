@@ -318,23 +318,19 @@ struct GeneDraw {
   int code;
   double delta;
 };
-__device__ __forceinline__ GeneDraw ga_breed_draw(const GaArgs& a, int64_t t, uint64_t g) {
-  GeneDraw d;
-  d.p = d.q = d.mut = d.code = 0;
-  d.delta = 0.0;
-  const int64_t i = a.div_L.div((uint32_t)t);
-  const int j = (int)(t - i * a.L);
-  if (i == 0) return d;
-  const int64_t k = (i - 1) >> 1;
-  // two_point_crossover: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
+// two_point_crossover cuts of pair k: p, q = sorted(integers(0, L + 1, size=2)); none for L < 2
+__device__ __forceinline__ void ga_pair_cuts(const GaArgs& a, int64_t k, uint64_t g, int& p, int& q) {
+  p = q = 0;
   if (a.L >= 2) {
     NpStream cs;
     cs.init(a.seed, DOM_GA_PAIR, g, (uint64_t)k, 0);
     const int x = (int)cs.integers(a.L + 1), y = (int)cs.integers(a.L + 1);
-    d.p = x < y ? x : y;
-    d.q = x < y ? y : x;
+    p = x < y ? x : y;
+    q = x < y ? y : x;
   }
-  // ga_mutate for this gene (ga.py:126-137)
+}
+// ga_mutate for gene j of child i (ga.py:126-137)
+__device__ __forceinline__ void ga_gene_mutation(const GaArgs& a, int64_t i, int j, uint64_t g, GeneDraw& d) {
   NpStream ms;
   ms.init(a.seed, DOM_GA_MUT, g, (uint64_t)i, (uint64_t)j);
   if (ms.random() < a.rate) {
@@ -346,6 +342,16 @@ __device__ __forceinline__ GeneDraw ga_breed_draw(const GaArgs& a, int64_t t, ui
       d.delta = ms.uniform(-a.mrange, a.mrange);
     }
   }
+}
+__device__ __forceinline__ GeneDraw ga_breed_draw(const GaArgs& a, int64_t t, uint64_t g) {
+  GeneDraw d;
+  d.p = d.q = d.mut = d.code = 0;
+  d.delta = 0.0;
+  const int64_t i = a.div_L.div((uint32_t)t);
+  const int j = (int)(t - i * a.L);
+  if (i == 0) return d;
+  ga_pair_cuts(a, (i - 1) >> 1, g, d.p, d.q);
+  ga_gene_mutation(a, i, j, g, d);
   return d;
 }
 __device__ __forceinline__ void ga_breed_apply(const GaArgs& a, int64_t t, int cur, int64_t elite,
@@ -377,15 +383,44 @@ __device__ __forceinline__ void ga_breed_gene(const GaArgs& a, int64_t t, uint64
   ga_breed_apply(a, t, cur, elite, ga_breed_draw(a, t, g));
 }
 
-__global__ void ga_breed_kernel(GaArgs a) {
+// Large populations: chunks of 256 genes; the crossover cuts of the chunk's
+// pairs are drawn once per pair into shared memory (not once per gene: the
+// pair stream was half of this kernel's Philox work).
+constexpr int kBreedThreads = 256;
+__global__ void __launch_bounds__(kBreedThreads) ga_breed_kernel(GaArgs a) {
+  __shared__ int2 s_cut[kBreedThreads / 2 + 2];
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   const int cur = ga_cur(a);
   const int64_t total = a.P * a.L;
   const int64_t elite = a.st->elite;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x)
-    ga_breed_gene(a, t, g, cur, elite);
+  for (int64_t t0 = (int64_t)blockIdx.x * kBreedThreads; t0 < total; t0 += (int64_t)gridDim.x * kBreedThreads) {
+    const int64_t i_lo = a.div_L.div((uint32_t)t0);
+    const int64_t i_hi = a.div_L.div((uint32_t)min(total - 1, t0 + kBreedThreads - 1));
+    const int64_t k_lo = i_lo >= 1 ? (i_lo - 1) >> 1 : 0;
+    const int npairs = i_hi >= 1 ? (int)(((i_hi - 1) >> 1) - k_lo + 1) : 0;
+    __syncthreads();  // the previous chunk's readers
+    for (int r = threadIdx.x; r < npairs; r += kBreedThreads) {
+      int p, q;
+      ga_pair_cuts(a, k_lo + r, g, p, q);
+      s_cut[r] = make_int2(p, q);
+    }
+    __syncthreads();
+    const int64_t t = t0 + threadIdx.x;
+    if (t < total) {
+      GeneDraw d;
+      d.p = d.q = d.mut = d.code = 0;
+      d.delta = 0.0;
+      const int64_t i = a.div_L.div((uint32_t)t);
+      if (i > 0) {
+        const int2 c = s_cut[((i - 1) >> 1) - k_lo];
+        d.p = c.x;
+        d.q = c.y;
+        ga_gene_mutation(a, i, (int)(t - i * a.L), g, d);
+      }
+      ga_breed_apply(a, t, cur, elite, d);
+    }
+  }
 }
 
 __device__ __forceinline__ void ga_advance_body(const GaArgs& a) {
@@ -874,7 +909,7 @@ static isq_status ga_launch_finish(const GaArgs& a, cudaStream_t s) {
   } else {
     ga_reduce_sus_kernel<<<1, kGaRed, 0, s>>>(a);
   }
-  ga_breed_kernel<<<ga_blocks(a.P * a.L), 256, 0, s>>>(a);
+  ga_breed_kernel<<<ga_blocks(a.P * a.L), kBreedThreads, 0, s>>>(a);
   ga_advance_kernel<<<1, 1, 0, s>>>(a);
   ISQ_CUDA_TRY(cudaGetLastError());
   return ISQ_OK;
