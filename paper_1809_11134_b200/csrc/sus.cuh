@@ -101,7 +101,7 @@ constexpr int kChainE = 8;                         // elements per thread per ti
 constexpr int kChainTile = kSusThreads * kChainE;  // 8192
 constexpr uint64_t kChainSat = 1ull << 60;         // saturation (any K >= 2^52 is out of the binade)
 constexpr int kChainGoodRun = 64;                  // a parallel run this long resets the scalar budget
-constexpr int kChainWarm = 2048;                   // plain adds at least this far (a parallel attempt costs ~1.5k)
+constexpr int kChainWarm = 1024;                   // plain adds at least this far (an attempt costs ~14k cycles)
 constexpr int kChainMaxBudget = 1 << 16;
 
 // Dynamic shared memory of a kernel calling exact_chain_block: one padded tile.
@@ -172,19 +172,31 @@ __device__ inline void exact_chain_block(const double* f, double fconst, int64_t
           int end = pos + budget < len ? pos + budget : len;
           int i = pos;
           if (warm) {  // warm-up: to the first binade change after kChainWarm elements (a parallel
-                       // attempt then starts a binade and covers as many elements as came before)
-            const int e0 = (int)((uint64_t)__double_as_longlong(x) >> 52);
-            end = len;
-            for (; i < len; ++i) {
+                       // attempt then starts near a binade's start and covers about as many
+                       // elements as came before)
+            bool more = true;
+            while (more && i + 8 <= len) {  // groups of 8: the loads ahead of the dependent adds
+              const int eb = (int)((uint64_t)__double_as_longlong(x) >> 52);
+              double v[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) v[k] = f ? sbuf[chain_pad(i + k)] : fconst;
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                x = __dadd_rn(x, v[k]);
+                sbuf[chain_pad(i + k)] = x;
+              }
+              i += 8;
+              more = j + i < kChainWarm || (int)((uint64_t)__double_as_longlong(x) >> 52) == eb;
+            }
+            while (more && i < len) {
+              const int eb = (int)((uint64_t)__double_as_longlong(x) >> 52);
               x = __dadd_rn(x, f ? sbuf[chain_pad(i)] : fconst);
               sbuf[chain_pad(i)] = x;
-              if (j + i + 1 >= kChainWarm && (int)((uint64_t)__double_as_longlong(x) >> 52) != e0) {
-                ++i;
-                end = i;
-                warm_done = true;
-                break;
-              }
+              ++i;
+              more = j + i < kChainWarm || (int)((uint64_t)__double_as_longlong(x) >> 52) == eb;
             }
+            end = i;
+            warm_done = !more;
           }
           for (; i + 8 <= end; i += 8) {
             double v[8];
@@ -346,7 +358,7 @@ __device__ inline void exact_chain_block(const double* f, double fconst, int64_t
 // by the whole block.
 __device__ inline void exact_const_chain_block(double inc, int64_t n, double x0, double* out) {
   __shared__ double s_x;
-  __shared__ int64_t s_j, s_m;
+  __shared__ int64_t s_m;
   __shared__ uint64_t s_K1, s_d;
   __shared__ int s_E;
   const int tid = threadIdx.x;
