@@ -1,3 +1,5 @@
+"""Criterion 2 (GA synthesizes CNOT) over seeds 1..40 on the device GA: the
+success count beside the reference's 34/40 (tests/golden/ga_cnot_outcomes_reference.json)."""
 import math, sys, json
 sys.path.insert(0, '.')
 from paper_1809_11134_b200 import GaConfig, GaEngine, target_matrix
