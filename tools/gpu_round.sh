@@ -15,6 +15,8 @@ ISQ_BENCH_SHARE_GPU=1 timeout 600 python bench.py --gpus 2 --steps 2 --warmup 3 
 timeout 600 python tools/kbench.py > $OUT/kbench.json 2>&1
 timeout 300 python tools/small_bench.py > $OUT/small_bench.txt 2>&1
 timeout 900 python tools/acceptance.py > $OUT/acceptance.json 2> $OUT/acceptance.err
+timeout 300 python tools/ga_large.py > $OUT/ga_large.txt 2>&1
+[ -x tools/susbench.bin ] && { tools/susbench.bin 1048576; tools/susbench.bin 65536; } > $OUT/susbench.txt 2>&1
 if [ "${PROFILE:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $OUT/bench_launches.csv python bench.py --steps 2 --warmup 3 --skip-e2e --skip-fp32 --skip-extras > $OUT/bench_ncu.log 2>&1
