@@ -390,6 +390,38 @@ isq_status isq_ga_mutate_genomes(const isq_ga_config* cfg, uint64_t generation, 
  * on `device` (roofline denominator of the fitness kernel). */
 isq_status isq_fma_peak(int32_t fp64, int32_t device, double* flops_per_s);
 
+/* ----------------------------------------------------------------------
+ * encoding.py's per-unit operators (encoding.py:40-132), batched: element i
+ * is unit `first + i` of the streams the engines draw from -- the mutation
+ * stream after the engine's mask and coin draws (mutate_angle / mutate_qutrit:
+ * the step mutate_population gives that slot), the measurement stream
+ * (estimate_axis, as construct_segments), (MEASURE, sub 1) for
+ * measure_qutrit, the init stream (random_angle / random_qutrit).  Qutrits
+ * are count x 3 complex128.  The Born entries return ISQ_ERR_INVARIANT
+ * (InvariantViolation) when a norm² deviates from 1 by more than 1e-6.
+ * ---------------------------------------------------------------------- */
+/* mutate_angle (encoding.py:45-53): out[i] = (theta + sign (1 - f) range) mod 2 pi. */
+isq_status isq_mutate_angles(int64_t count, const double* thetas, const double* segment_fitness,
+                             double mutation_range, uint64_t seed, uint64_t generation, int64_t first, double* out,
+                             int32_t device);
+/* mutate_qutrit (encoding.py:119-132): one SU(3) parameter scaled by (1 - f), renormalised. */
+isq_status isq_mutate_qutrits(int64_t count, const double* qutrits, const double* segment_fitness, uint64_t seed,
+                              uint64_t generation, int64_t first, double* out, int32_t device);
+/* born_probabilities (encoding.py:66-71): probs[count][3]. */
+isq_status isq_born_probabilities(int64_t count, const double* qutrits, double* probs, int32_t device);
+/* estimate_axis (encoding.py:80-84): plurality of multinomial(n_meas, born), ties to the lower axis. */
+isq_status isq_estimate_axes(int64_t count, const double* qutrits, int32_t n_meas, uint64_t seed, uint64_t generation,
+                             int64_t first, int8_t* axes, int32_t device);
+/* measure_qutrit (encoding.py:74-77): Generator.choice(3, p=born). */
+isq_status isq_measure_qutrits(int64_t count, const double* qutrits, uint64_t seed, uint64_t generation,
+                               int64_t first, int8_t* axes, int32_t device);
+/* su3_operator (encoding.py:87-116): params[count][8] (theta1..3, phi1..5) -> out[count][3][3] complex128. */
+isq_status isq_su3_operators(int64_t count, const double* params, double* out, int32_t device);
+/* random_angle / random_qutrit (encoding.py:56-63) on the init streams: thetas[count] (bit-exact
+ * uniform(0, 2 pi)), and with with_qutrit a normalised complex Gaussian (Box-Muller) per unit. */
+isq_status isq_init_slots(int64_t count, uint64_t seed, int64_t first, int32_t with_qutrit, double* thetas,
+                          double* qutrits, int32_t device);
+
 #ifdef __cplusplus
 }
 #endif

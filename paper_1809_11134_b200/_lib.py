@@ -177,6 +177,13 @@ SIGNATURES: dict[str, tuple] = {
     "isq_table_read": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "isq_table_set_slot_max": (c_i32, [c_vp, c_vp]),
     "isq_apply_gates": (c_i32, [c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "isq_mutate_angles": (c_i32, [c_i64, c_vp, c_vp, c_dbl, c_u64, c_u64, c_i64, c_vp, c_i32]),
+    "isq_mutate_qutrits": (c_i32, [c_i64, c_vp, c_vp, c_u64, c_u64, c_i64, c_vp, c_i32]),
+    "isq_born_probabilities": (c_i32, [c_i64, c_vp, c_vp, c_i32]),
+    "isq_estimate_axes": (c_i32, [c_i64, c_vp, c_i32, c_u64, c_u64, c_i64, c_vp, c_i32]),
+    "isq_measure_qutrits": (c_i32, [c_i64, c_vp, c_u64, c_u64, c_i64, c_vp, c_i32]),
+    "isq_su3_operators": (c_i32, [c_i64, c_vp, c_vp, c_i32]),
+    "isq_init_slots": (c_i32, [c_i64, c_u64, c_i64, c_i32, c_vp, c_vp, c_i32]),
     "isq_ga_random_genomes": (c_i32, [c_i32, c_i32, c_u64, c_i64, c_i64, c_vp, c_vp, c_i32]),
     "isq_ga_sus_select": (c_i32, [c_i64, c_vp, c_i64, c_u64, c_u64, c_vp, c_i32]),
     "isq_ga_crossover_cuts": (c_i32, [c_i32, c_u64, c_u64, c_i64, c_i64, c_vp, c_i32]),

@@ -637,3 +637,270 @@ isq_status isq_ga_mutate_genomes(const isq_ga_config* cfg, uint64_t generation, 
 }
 
 }  // extern "C"
+
+// ===================================================================
+// encoding.py's per-unit operators (encoding.py:40-132), batched: element i
+// is unit `first + i` of the counter streams the engines use --
+//   mutate_angle / mutate_qutrit: the slot's mutation stream (seed, MUTATE,
+//     generation, slot) after the engine's mask and coin draws (engine.py:
+//     241-242), i.e. exactly the step mutate_population gives that slot;
+//   estimate_axis: the slot's measurement stream (seed, MEASURE, generation,
+//     slot), as construct_segments;
+//   measure_qutrit (not drawn by the engines): (seed, MEASURE, generation,
+//     slot, sub = 1);
+//   random_angle / random_qutrit: the slot's init stream (init_population).
+// ===================================================================
+namespace isq_enc {  // (named: a second anonymous namespace confuses the kernel stubs)
+
+__global__ void enc_mutate_angles_kernel(int64_t count, const double* th, const double* f, double range,
+                                         uint64_t seed, uint64_t g, int64_t first, double* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w[4];
+    stream_block(seed, DOM_MUTATE, g, (uint64_t)(first + i), 0, 1, w);
+    const double sign = u64_to_double(w[2]) < 0.5 ? 1.0 : -1.0;  // encoding.py:51
+    const double step = __dmul_rn(__dmul_rn(sign, __dsub_rn(1.0, f[i])), range);
+    out[i] = py_mod(__dadd_rn(th[i], step), kTwoPiD);
+  }
+}
+
+__global__ void enc_mutate_qutrits_kernel(int64_t count, const double2* q, const double* f, uint64_t seed, uint64_t g,
+                                          int64_t first, double2* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w[4];
+    stream_block(seed, DOM_MUTATE, g, (uint64_t)(first + i), 0, 1, w);
+    const int which = (int)((uint32_t)(w[2] & 0xffffffffULL) >> 29);  // integers(8): Lemire, bound 8
+    const double range = which < 3 ? kHalfPiD : kTwoPiD;               // SU3_RANGES (encoding.py:23)
+    const double value = __dadd_rn(0.0, __dmul_rn(__dmul_rn(range, __dsub_rn(1.0, f[i])), u64_to_double(w[3])));
+    double2 v[3] = {q[3 * i], q[3 * i + 1], q[3 * i + 2]};
+    su3_one_param(which, value, v);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out[3 * i + k] = v[k];
+  }
+}
+
+// born_probabilities (encoding.py:66-71): numpy |q|^2, the left-to-right sum,
+// the 1e-6 norm invariant, the division.
+__device__ __forceinline__ bool enc_born(const double2* q, double pr[3]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double a = np_cabs(q[k].x, q[k].y);
+    pr[k] = __dmul_rn(a, a);
+  }
+  const double norm = __dadd_rn(__dadd_rn(pr[0], pr[1]), pr[2]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) pr[k] = __ddiv_rn(pr[k], norm);
+  return !(fabs(__dsub_rn(norm, 1.0)) > 1e-6);
+}
+
+__global__ void enc_born_kernel(int64_t count, const double2* q, double* probs, int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double pr[3];
+    if (!enc_born(q + 3 * i, pr)) atomicOr(bad, 1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) probs[3 * i + k] = pr[k];
+  }
+}
+
+__global__ void enc_estimate_axes_kernel(int64_t count, const double2* q, int n_meas, uint64_t seed, uint64_t g,
+                                         int64_t first, int8_t* axes, int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double pr[3];
+    if (!enc_born(q + 3 * i, pr)) atomicOr(bad, 1);
+    const double re[3] = {q[3 * i].x, q[3 * i + 1].x, q[3 * i + 2].x};
+    const double im[3] = {q[3 * i].y, q[3 * i + 1].y, q[3 * i + 2].y};
+    NpStream st;
+    st.init(seed, DOM_MEASURE, g, (uint64_t)(first + i), 0);
+    bool ok = true;
+    axes[i] = (int8_t)measure_axis(re, im, n_meas, st, &ok);
+  }
+}
+
+// measure_qutrit (encoding.py:74-77): Generator.choice(3, p=probs) -- cdf =
+// cumsum(p), cdf /= cdf[-1], one random(), searchsorted(side='right').
+__global__ void enc_measure_qutrits_kernel(int64_t count, const double2* q, uint64_t seed, uint64_t g, int64_t first,
+                                           int8_t* axes, int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double pr[3];
+    if (!enc_born(q + 3 * i, pr)) atomicOr(bad, 1);
+    const double c0 = pr[0], c1 = __dadd_rn(c0, pr[1]), c2 = __dadd_rn(c1, pr[2]);
+    const double d0 = __ddiv_rn(c0, c2), d1 = __ddiv_rn(c1, c2), d2 = __ddiv_rn(c2, c2);
+    uint64_t w[4];
+    stream_block(seed, DOM_MEASURE, g, (uint64_t)(first + i), 1, 1, w);
+    const double u = u64_to_double(w[0]);
+    axes[i] = (int8_t)((d0 <= u) + (d1 <= u) + (d2 <= u));
+  }
+}
+
+// su3_operator (encoding.py:87-116) for general parameters (theta1..3,
+// phi1..5): the engines only ever need one nonzero parameter
+// (su3_one_param); this is the full template, entry by entry.
+__device__ __forceinline__ double2 enc_cis(double a) {  // e^{i a}
+  double s, c;
+  sincos(a, &s, &c);
+  return make_double2(c, s);
+}
+__device__ __forceinline__ double2 enc_scale(double2 z, double r) { return make_double2(z.x * r, z.y * r); }
+__device__ __forceinline__ double2 enc_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+__global__ void enc_su3_kernel(int64_t count, const double* prm, double2* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const double* p = prm + 8 * i;
+    double s1, c1, s2, c2, s3, c3;
+    sincos(p[0], &s1, &c1);
+    sincos(p[1], &s2, &c2);
+    sincos(p[2], &s3, &c3);
+    const double f1 = p[3], f2 = p[4], f3 = p[5], f4 = p[6], f5 = p[7];
+    double2* u = out + 9 * i;
+    u[0] = enc_scale(enc_scale(enc_cis(f1), c1), c2);
+    u[1] = enc_scale(enc_cis(f3), s1);
+    u[2] = enc_scale(enc_scale(enc_cis(f4), c1), s2);
+    u[3] = enc_sub(enc_scale(enc_scale(enc_cis(-f4 - f5), s2), s3), enc_scale(enc_scale(enc_scale(enc_cis(f1 + f2 - f3), s1), c2), c3));
+    u[4] = enc_scale(enc_scale(enc_cis(f2), c1), c3);
+    u[5] = enc_sub(enc_scale(enc_scale(enc_cis(-f1 - f5), -c2), s3), enc_scale(enc_scale(enc_scale(enc_cis(f2 - f3 + f4), s1), s2), c3));
+    u[6] = enc_sub(enc_scale(enc_scale(enc_cis(-f2 - f4), -s2), c3), enc_scale(enc_scale(enc_scale(enc_cis(f1 - f3 + f5), s1), c2), s3));
+    u[7] = enc_scale(enc_scale(enc_cis(f5), c1), s3);
+    u[8] = enc_sub(enc_scale(enc_scale(enc_cis(-f1 - f2), c2), c3), enc_scale(enc_scale(enc_scale(enc_cis(-f3 + f4 + f5), s1), s2), s3));
+  }
+}
+
+__global__ void enc_init_slots_kernel(int64_t count, uint64_t seed, int64_t first, int with_qutrit, double* th,
+                                      double2* q) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double t;
+    double2 v[3];
+    init_slot_value(seed, first + i, with_qutrit != 0, t, v);
+    th[i] = t;
+    if (with_qutrit) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) q[3 * i + k] = v[k];
+    }
+  }
+}
+
+isq_status enc_range(int64_t count, int64_t first) {
+  if (count < 0 || first < 0) return bad_config("unit range out of bounds");
+  return ISQ_OK;
+}
+
+// Shared host side of the three Born-rule entries: `kind` 0 born, 1 estimate, 2 measure.
+isq_status enc_born_call(int kind, int64_t count, const double* qutrits, int32_t n_meas, uint64_t seed,
+                         uint64_t generation, int64_t first, void* out, int32_t device) {
+  isq_status st = enc_range(count, first);
+  if (st != ISQ_OK || count == 0) return st;
+  if (kind == 1 && n_meas < 1) return bad_config("nMeas must be ≥ 1");
+  TRYF(cudaSetDevice(device));
+  DevBuf dq, dout, dbad;
+  const size_t ob = kind == 0 ? (size_t)count * 24 : (size_t)count;
+  TRYF(dq.alloc(count * 48));
+  TRYF(dout.alloc(ob));
+  TRYF(dbad.alloc(sizeof(int)));
+  TRYF(cudaMemset(dbad.p, 0, sizeof(int)));
+  TRYF(cudaMemcpy(dq.p, qutrits, count * 48, cudaMemcpyHostToDevice));
+  if (kind == 0)
+    enc_born_kernel<<<grid_for(count), 256>>>(count, dq.as<double2>(), dout.as<double>(), dbad.as<int>());
+  else if (kind == 1)
+    enc_estimate_axes_kernel<<<grid_for(count), 256>>>(count, dq.as<double2>(), n_meas, seed, generation, first,
+                                                       dout.as<int8_t>(), dbad.as<int>());
+  else
+    enc_measure_qutrits_kernel<<<grid_for(count), 256>>>(count, dq.as<double2>(), seed, generation, first,
+                                                         dout.as<int8_t>(), dbad.as<int>());
+  TRYF(cudaGetLastError());
+  int bad = 0;
+  TRYF(cudaMemcpy(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) {
+    set_error("qutrit norm² deviates from 1 by more than 1e-6");
+    return ISQ_ERR_INVARIANT;
+  }
+  TRYF(cudaMemcpy(out, dout.p, ob, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+}  // namespace isq_enc
+
+using namespace isq_enc;
+
+extern "C" {
+
+isq_status isq_mutate_angles(int64_t count, const double* thetas, const double* segment_fitness,
+                             double mutation_range, uint64_t seed, uint64_t generation, int64_t first, double* out,
+                             int32_t device) {
+  isq_status st = enc_range(count, first);
+  if (st != ISQ_OK || count == 0) return st;
+  TRYF(cudaSetDevice(device));
+  DevBuf dt, df, dout;
+  TRYF(dt.alloc(count * 8));
+  TRYF(df.alloc(count * 8));
+  TRYF(dout.alloc(count * 8));
+  TRYF(cudaMemcpy(dt.p, thetas, count * 8, cudaMemcpyHostToDevice));
+  TRYF(cudaMemcpy(df.p, segment_fitness, count * 8, cudaMemcpyHostToDevice));
+  enc_mutate_angles_kernel<<<grid_for(count), 256>>>(count, dt.as<double>(), df.as<double>(), mutation_range, seed,
+                                                     generation, first, dout.as<double>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(out, dout.p, count * 8, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_mutate_qutrits(int64_t count, const double* qutrits, const double* segment_fitness, uint64_t seed,
+                              uint64_t generation, int64_t first, double* out, int32_t device) {
+  isq_status st = enc_range(count, first);
+  if (st != ISQ_OK || count == 0) return st;
+  TRYF(cudaSetDevice(device));
+  DevBuf dq, df, dout;
+  TRYF(dq.alloc(count * 48));
+  TRYF(df.alloc(count * 8));
+  TRYF(dout.alloc(count * 48));
+  TRYF(cudaMemcpy(dq.p, qutrits, count * 48, cudaMemcpyHostToDevice));
+  TRYF(cudaMemcpy(df.p, segment_fitness, count * 8, cudaMemcpyHostToDevice));
+  enc_mutate_qutrits_kernel<<<grid_for(count), 256>>>(count, dq.as<double2>(), df.as<double>(), seed, generation,
+                                                      first, dout.as<double2>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(out, dout.p, count * 48, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+
+isq_status isq_born_probabilities(int64_t count, const double* qutrits, double* probs, int32_t device) {
+  return enc_born_call(0, count, qutrits, 1, 0, 0, 0, probs, device);
+}
+
+isq_status isq_estimate_axes(int64_t count, const double* qutrits, int32_t n_meas, uint64_t seed, uint64_t generation,
+                             int64_t first, int8_t* axes, int32_t device) {
+  return enc_born_call(1, count, qutrits, n_meas, seed, generation, first, axes, device);
+}
+
+isq_status isq_measure_qutrits(int64_t count, const double* qutrits, uint64_t seed, uint64_t generation,
+                               int64_t first, int8_t* axes, int32_t device) {
+  return enc_born_call(2, count, qutrits, 1, seed, generation, first, axes, device);
+}
+
+isq_status isq_su3_operators(int64_t count, const double* params, double* out, int32_t device) {
+  isq_status st = enc_range(count, 0);
+  if (st != ISQ_OK || count == 0) return st;
+  TRYF(cudaSetDevice(device));
+  DevBuf dp, dout;
+  TRYF(dp.alloc(count * 64));
+  TRYF(dout.alloc(count * 144));
+  TRYF(cudaMemcpy(dp.p, params, count * 64, cudaMemcpyHostToDevice));
+  enc_su3_kernel<<<grid_for(count), 256>>>(count, dp.as<double>(), dout.as<double2>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(out, dout.p, count * 144, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+isq_status isq_init_slots(int64_t count, uint64_t seed, int64_t first, int32_t with_qutrit, double* thetas,
+                          double* qutrits, int32_t device) {
+  isq_status st = enc_range(count, first);
+  if (st != ISQ_OK || count == 0) return st;
+  if (with_qutrit && qutrits == nullptr) return bad_config("qutrits output missing");
+  TRYF(cudaSetDevice(device));
+  DevBuf dt, dq;
+  TRYF(dt.alloc(count * 8));
+  TRYF(dq.alloc(with_qutrit ? count * 48 : 16));
+  enc_init_slots_kernel<<<grid_for(count), 256>>>(count, seed, first, with_qutrit, dt.as<double>(),
+                                                  dq.as<double2>());
+  TRYF(cudaGetLastError());
+  TRYF(cudaMemcpy(thetas, dt.p, count * 8, cudaMemcpyDeviceToHost));
+  if (with_qutrit) TRYF(cudaMemcpy(qutrits, dq.p, count * 48, cudaMemcpyDeviceToHost));
+  return ISQ_OK;
+}
+
+}  // extern "C"
