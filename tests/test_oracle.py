@@ -218,3 +218,30 @@ def test_oracle_sus_select_matches_reference_at_large_populations():
         assert float(np.sum(list(map(float, f)))) == float(g[name + "_total"])
         picks = np.asarray(OG.sus_select(list(map(float, f)), count, stream(seed, DOM_GA_SUS, gen)), dtype=np.int64)
         assert hashlib.sha256(picks.astype("<i8").tobytes()).hexdigest() == str(g[name + "_sha"]), name
+
+
+def test_oracle_encoding_matches_reference_goldens():
+    """The oracle's encoding restatement (mutate_angle, mutate_qutrit,
+    su3_operator) and the measurement recipe it uses against the reference's
+    own functions on the same streams (tests/golden/encoding.npz)."""
+    from oracle.streams import DOM_MEASURE, DOM_MUTATE
+
+    g = golden("encoding")
+    seed, first = (int(x) for x in g["meta"])
+    th, q, f = g["thetas"], g["qutrits"], g["fits"]
+    for gen in (0, 7):
+        ma, mq = [], []
+        for i in range(th.size):
+            st = stream(seed, DOM_MUTATE, gen, first + i)
+            st.random(), st.random()
+            ma.append(O.mutate_angle(float(th[i]), float(f[i]), 0.7, st))
+            st = stream(seed, DOM_MUTATE, gen, first + i)
+            st.random(), st.random()
+            mq.append(O.mutate_qutrit(q[i], float(f[i]), st))
+        assert np.array_equal(np.array(ma), g[f"g{gen}_mutate_angle"])
+        np.testing.assert_allclose(np.array(mq), g[f"g{gen}_mutate_qutrit"], rtol=0, atol=1e-15)
+        for nm in (1, 11, 1000):
+            want = [int(np.argmax(stream(seed, DOM_MEASURE, gen, first + i).multinomial(
+                nm, np.abs(q[i]) ** 2 / (np.abs(q[i]) ** 2).sum()))) for i in range(th.size)]
+            assert np.array_equal(np.array(want), g[f"g{gen}_estimate_nm{nm}"])
+    np.testing.assert_allclose(np.array([O.su3_operator(p) for p in g["su3_params"]]), g["su3"], rtol=0, atol=0)
