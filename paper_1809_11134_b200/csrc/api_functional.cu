@@ -296,7 +296,12 @@ __global__ void __launch_bounds__(kSusThreads)
     exact_chain_block(f, 0.0, P - 1, 0.0, C, chain_smem);
     return;
   }
-  const double total = np_pairwise_sum_block<kSusThreads>(f, P, sm);
+  __shared__ int s_neg;
+  if (threadIdx.x == 0) s_neg = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < P; i += blockDim.x)
+    if (!(f[i] >= 0.0)) s_neg = 1;  // negative or NaN: the sums are not monotone
+  const double total = np_pairwise_sum_block<kSusThreads>(f, P, sm);  // syncs first
   NpStream rs;
   rs.init(seed, DOM_GA_SUS, g, 0, 0);
   if (total <= 0.0) {
@@ -308,6 +313,22 @@ __global__ void __launch_bounds__(kSusThreads)
   }
   const double spacing = __ddiv_rn(total, (double)count);
   const double pointer = rs.uniform(0.0, spacing);
+  if (s_neg) {  // the reference's walk itself, on one thread (engine fitness is never negative)
+    if (threadIdx.x == 0) {
+      double p = pointer, cumulative = 0.0;
+      int64_t index = 0;
+      for (int64_t k = 0; k < count; ++k) {
+        while (index < P - 1 && __dadd_rn(cumulative, f[index]) <= p) {
+          cumulative = __dadd_rn(cumulative, f[index]);
+          ++index;
+        }
+        picks[k] = index;
+        p = __dadd_rn(p, spacing);
+      }
+      *flag = 0;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     Pt[0] = pointer;
     *flag = 1;

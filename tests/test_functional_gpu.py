@@ -274,17 +274,19 @@ def test_sus_select_at_large_populations_matches_reference():
 
 
 @pytest.mark.parametrize("P,count,kind", [(1, 1, "one"), (1, 7, "one"), (2, 5, "u"), (3, 1, "u"), (700, 700, "zero"),
-                                           (9000, 3, "u"), (5, 9000, "u"), (4096, 4096, "spike")])
+                                           (9000, 3, "u"), (5, 9000, "u"), (4096, 4096, "spike"), (900, 900, "neg")])
 def test_sus_select_edge_shapes_match_the_walk(P, count, kind):
     """Single values, more pointers than values and the reverse, all-zero
-    fitness at a size above the shared-memory walk, one dominant value."""
+    fitness at a size above the shared-memory walk, one dominant value, and
+    negative values (non-monotone sums: the walk itself runs)."""
     from oracle.ga import sus_select as walk
     from oracle.streams import DOM_GA_SUS
     from paper_1809_11134_b200 import CounterStreams, sus_select
 
     r = np.random.default_rng(P + count)
     f = {"one": np.array([0.3] * P), "u": r.random(P), "zero": np.zeros(P),
-         "spike": np.where(np.arange(P) == P // 3, 1.0, 1e-9 * r.random(P))}[kind]
+         "spike": np.where(np.arange(P) == P // 3, 1.0, 1e-9 * r.random(P)),
+         "neg": r.random(P) - 0.2}[kind]  # not a fitness, but the reference's walk accepts it
     want = walk(list(map(float, f)), count, stream(8, DOM_GA_SUS, 2))
     assert sus_select(f, count, CounterStreams(8, 2)) == want
 
