@@ -16,9 +16,11 @@
 //     the recursion's top levels are expanded into up to 2^10 subtrees, one
 //     per thread (np_pairwise_sum, iterative), then combined level by level
 //     in the recursion's own order -- bit-identical to the sequential sum;
-//   * the two recurrences are evaluated exactly in parallel (exact_chain_block:
-//     integer prefix sums on each binade's grid, plain adds only where the
-//     grid form does not hold), one block each;
+//   * the two recurrences are evaluated exactly in parallel, one block each:
+//     the cumulative sum by exact_chain_block (a block-wide scan of the
+//     mantissa maps of each binade's grid, plain adds only where the grid
+//     form does not hold), the pointers by exact_const_chain_block (a
+//     constant increment: closed form inside each binade);
 //   * the picks are a grid-wide binary search over C (sus_search_kernel).
 #pragma once
 
