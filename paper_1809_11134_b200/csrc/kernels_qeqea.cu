@@ -444,19 +444,15 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_partials(QeqeaArgs a
 // Final reduction, best-so-far update (strict >, first circuit on ties,
 // engine.py:341-343), the generation record, and capture of the new best
 // circuit's gates by warp 0.  All threads of the block call it.
-__device__ __forceinline__ void reduce_final_body(const QeqeaArgs& a, int* s_improved, int64_t* s_best) {
+// Thread 0: the generation's (max, first argmax, sum) -> best-so-far,
+// record; every thread then syncs and warp 0 captures an improved best's
+// gates from (codes, thetas) (the circuit-side arrays, or the single-block
+// kernel's shared-memory copies).
+__device__ __forceinline__ void reduce_final_core(const QeqeaArgs& a, double m, double sum, int64_t arg,
+                                                  int* s_improved, int64_t* s_best, const uint8_t* codes,
+                                                  const double* thetas) {
   QeqeaDevState* st = a.st;
   if (threadIdx.x == 0) {
-    double m = -1.0, sum = 0.0;
-    int64_t arg = INT64_MAX;
-    for (int i = 0; i < a.n_parts; ++i) {
-      const double pm = a.part_max[i];
-      if (pm > m || (pm == m && a.part_arg[i] < arg)) {
-        m = pm;
-        arg = a.part_arg[i];
-      }
-      sum += a.part_sum[i];
-    }
     const double mean = sum / (double)a.P;
     st->gen_best = m;
     st->gen_mean = mean;
@@ -483,8 +479,8 @@ __device__ __forceinline__ void reduce_final_body(const QeqeaArgs& a, int* s_imp
       if (a.world == 1) {
         // the generation's gate codes / live angles of every circuit are still
         // in place (do not recompute them from the bank: the commit rewrites it)
-        a.best_codes[p] = a.gate_codes[best * a.L + p];
-        a.best_thetas[p] = a.gate_thetas[best * a.L + p];
+        a.best_codes[p] = codes[best * a.L + p];
+        a.best_thetas[p] = thetas[best * a.L + p];
       } else {
         // gathered elite record of the rank that scored the best circuit
         const double* e = a.elite + (best / a.S) * a.elite_len;
@@ -493,6 +489,22 @@ __device__ __forceinline__ void reduce_final_body(const QeqeaArgs& a, int* s_imp
       }
     }
   }
+}
+
+__device__ __forceinline__ void reduce_final_body(const QeqeaArgs& a, int* s_improved, int64_t* s_best) {
+  double m = -1.0, sum = 0.0;
+  int64_t arg = INT64_MAX;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.n_parts; ++i) {
+      const double pm = a.part_max[i];
+      if (pm > m || (pm == m && a.part_arg[i] < arg)) {
+        m = pm;
+        arg = a.part_arg[i];
+      }
+      sum += a.part_sum[i];
+    }
+  }
+  reduce_final_core(a, m, sum, arg, s_improved, s_best, a.gate_codes, a.gate_thetas);
 }
 
 __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
@@ -515,13 +527,13 @@ constexpr int kCommitThreads = 256;
 // max over its touches (u64 atomicMax; fitness >= 0, so integer order ==
 // double order).  The values kernel recorded each touch's starting slot_max
 // and pending-mutation flag, so only improving touches do random bank traffic.
-__device__ __forceinline__ void commit_touch(const QeqeaArgs& a, int64_t t, uint64_t g) {
-  const double fit = a.fitness[a.div_Lr.div((uint32_t)t)];
-  const double fb = a.touch_fbefore[t];
+// The commit of touch t from its values: `fit` its circuit's fitness, `fb`
+// the slot_max it started from, `s` its slot, `mf` its mutation flags,
+// `theta` its live angle.
+__device__ __forceinline__ void commit_touch_core(const QeqeaArgs& a, int64_t t, double fit, double fb, uint32_t s,
+                                                  uint8_t mf, double theta) {
   if (!(fit > fb)) return;
-  const uint32_t s = a.owner_flats[t];
   const int64_t loc = slot_local(a, s);
-  const uint8_t mf = a.touch_mutated[t];
   if (mf & 2) {
     // qutrit mutation: the live qutrit the values kernel derived (the same
     // value in every touch of the slot, so concurrent stores agree); theta
@@ -536,12 +548,18 @@ __device__ __forceinline__ void commit_touch(const QeqeaArgs& a, int64_t t, uint
     // angle mutation: every improving touch holds the same live angle
     // (values kernel), so the idempotent store needs no arbitration
     if (loc < a.Qtloc)
-      a.rot[loc].theta = a.owner_thetas[t];
+      a.rot[loc].theta = theta;
     else
-      a.inter[loc - a.Qtloc].theta = a.owner_thetas[t];
+      a.inter[loc - a.Qtloc].theta = theta;
   }
   atomicMax(reinterpret_cast<unsigned long long*>(smax_ptr(a, loc)),
             (unsigned long long)__double_as_longlong(fit));
+}
+__device__ __forceinline__ void commit_touch(const QeqeaArgs& a, int64_t t, uint64_t g) {
+  const double fit = a.fitness[a.div_Lr.div((uint32_t)t)];
+  const double fb = a.touch_fbefore[t];
+  if (!(fit > fb)) return;
+  commit_touch_core(a, t, fit, fb, a.owner_flats[t], a.touch_mutated[t], a.owner_thetas[t]);
 }
 
 __global__ void __launch_bounds__(kCommitThreads) qeqea_commit_table_kernel(QeqeaArgs a, int64_t t1) {
@@ -668,7 +686,34 @@ __global__ void __launch_bounds__(kThreadsPerBlock)
 // Launch-bound populations (C1-C3: P*L of a few hundred touches): n whole
 // generations in one single-block launch, every phase a block-wide loop over
 // the same device bodies the multi-kernel generation uses (identical
-// results), separated by __syncthreads.
+// results), separated by __syncthreads.  The generation's intermediates --
+// blueprints, gate codes / live angles, starting slot_max and mutation flags
+// per touch, fitness -- stay in (dynamic) shared memory: at these sizes a
+// phase is a few hundred cycles of work, and reading the previous phase's
+// output back through L2 cost about as much again per phase (ncu: ~half the
+// warp stall samples of a C1 generation sat on those loads).
+struct SmallMirror {
+  double* th;       // live angle per touch
+  double* fb;       // slot_max the touch started from
+  double* fit;      // fitness per circuit
+  uint32_t* flats;  // blueprint per touch
+  uint8_t* code;    // gate code per touch
+  uint8_t* mut;     // mutation flags per touch
+};
+__host__ __device__ inline size_t small_mirror_bytes(int64_t touches, int64_t P) {
+  return (size_t)touches * (8 + 8 + 4 + 1 + 1) + (size_t)P * 8 + 16;
+}
+__device__ __forceinline__ SmallMirror small_mirror(unsigned char* base, int64_t touches, int64_t P) {
+  SmallMirror m;
+  m.th = reinterpret_cast<double*>(base);
+  m.fb = m.th + touches;
+  m.fit = m.fb + touches;
+  m.flats = reinterpret_cast<uint32_t*>(m.fit + P);
+  m.code = reinterpret_cast<uint8_t*>(m.flats + touches);
+  m.mut = m.code + touches;
+  return m;
+}
+
 template <int NQ>
 __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a, int n_gens) {
   using G = Geo<NQ>;
@@ -676,81 +721,93 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
   __shared__ double2 Ts[G::D * G::D];
   __shared__ FitScratch<NQ, double, kSmallNR> sh[kWarps];
   __shared__ uint64_t blk[kWarps][36];
-  __shared__ double smax[kRedThreads], ssum[kRedThreads];
-  __shared__ int64_t sarg[kRedThreads];
   __shared__ int s_improved;
   __shared__ int64_t s_best;
+  __shared__ double s_m, s_sum;
+  __shared__ int64_t s_arg;
+  extern __shared__ __align__(16) unsigned char small_dyn[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < G::D * G::D; i += kRedThreads) Ts[i] = a.target[i];
   const int64_t touches = a.P * a.L;
+  const SmallMirror mi = small_mirror(small_dyn, touches, a.P);
   for (int it = 0; it < n_gens; ++it) {
     __syncthreads();
     if (a.st->stop) return;  // uniform: written by thread 0 before the barrier
     const uint64_t g = a.st->generation;
-    for (int64_t c = wib; c < a.P; c += kWarps) sample_circuit_warp(a, g, c, a.flats + c * a.L, blk[wib], lane);
+    for (int64_t c = wib; c < a.P; c += kWarps) sample_circuit_warp(a, g, c, mi.flats + c * a.L, blk[wib], lane);
     __syncthreads();
     for (int64_t t = threadIdx.x; t < touches; t += kRedThreads) {
-      const uint32_t s = a.owner_flats[t];
+      // values (value_touch_from + the measurement), into shared memory
+      const uint32_t s = mi.flats[t];
       // the measurement stream's first block depends only on (g, s): start it
-      // before the record load and the mutation (latency-bound tiny populations)
+      // before the record load and the mutation
       NpStream ms;
       ms.init(a.seed, DOM_MEASURE, g, (uint64_t)s, 0);
-      if (slot_kind(a, s) < a.n) ms.prime();
+      const int64_t kind = slot_kind(a, s);
+      if (kind < a.n) ms.prime();
       LiveSlot v;
-      int which;
-      double value;
-      if (value_touch_from(a, t, g, s, v, which, value)) {
-        if (which >= 0) {
+      const double f = load_committed(a, slot_local(a, s), v);
+      int which = -1;
+      double value = 0.0;
+      const int m = g > 0 ? mutate_decide(a, s, g - 1, f, v, which, value) : MUT_NONE;
+      mi.th[t] = v.theta;
+      if constexpr (!kFitMulti<NQ>) a.gate_thetas[t] = v.theta;  // FastEval stages gates with cp.async (global)
+      mi.fb[t] = f;
+      mi.mut[t] = (uint8_t)((m != MUT_NONE ? 1 : 0) | (m == MUT_QUTRIT ? 2 : 0));
+      if (kind < a.n) {
+        if (m == MUT_QUTRIT) {
           su3_one_param(which, value, v.q);
 #pragma unroll
           for (int k = 0; k < 3; ++k) a.qlive[3 * t + k] = v.q[k];
         }
         double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
         double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
-        emit_code(a, t, measure_code_on(a, s, ms, re, im));
+        mi.code[t] = measure_code_on(a, s, ms, re, im);
+      } else {
+        mi.code[t] = (uint8_t)(3 * a.n + (kind - a.n));
       }
+      if constexpr (!kFitMulti<NQ>) a.gate_codes[t] = mi.code[t];
     }
     __syncthreads();
-    fitness_rows_fast<NQ, double, kSmallNR, true>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, a.fitness, kWarps,
-                                            nullptr, nullptr, small_cpw<NQ>(a.P, kWarps));
+    if constexpr (kFitMulti<NQ>)  // n <= 3: plain loads of the gates, from shared memory
+      fitness_rows_fast<NQ, double, kSmallNR, true>(a.P, a.L, mi.code, mi.th, Ts, sh, mi.fit, kWarps, nullptr,
+                                                    nullptr, small_cpw<NQ>(a.P, kWarps));
+    else
+      fitness_rows_fast<NQ, double, kSmallNR, true>(a.P, a.L, a.gate_codes, a.gate_thetas, Ts, sh, mi.fit, kWarps,
+                                                    nullptr, nullptr, small_cpw<NQ>(a.P, kWarps));
     __syncthreads();
-    if (a.P <= 32 && a.n_parts == 1) {
-      // one warp: the same pairwise tree as reduce_partial_body (its upper
-      // levels only add zeros), as shuffles instead of 8 block barriers
-      if (wib == 0) {
-        double m = -1.0, sum = 0.0;
-        int64_t arg = INT64_MAX;
-        if (lane < a.P) {
-          m = sum = a.fitness[lane];
-          arg = lane;
-        }
+    // reductions: the same pairwise tree as reduce_partial_body (P <= 32: its
+    // upper levels only add zeros), as shuffles
+    if (wib == 0) {
+      double m = -1.0, sum = 0.0;
+      int64_t arg = INT64_MAX;
+      if (lane < a.P) {
+        m = sum = mi.fit[lane];
+        arg = lane;
+        a.fitness[lane] = m;  // host readback (isq_qeqea_fitness)
+      }
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-          const double m2 = __shfl_down_sync(0xffffffffu, m, off);
-          const int64_t a2 = __shfl_down_sync(0xffffffffu, arg, off);
-          const double s2 = __shfl_down_sync(0xffffffffu, sum, off);
-          if (m2 > m || (m2 == m && a2 < arg)) {
-            m = m2;
-            arg = a2;
-          }
-          sum += s2;
+      for (int off = 16; off >= 1; off >>= 1) {
+        const double m2 = __shfl_down_sync(0xffffffffu, m, off);
+        const int64_t a2 = __shfl_down_sync(0xffffffffu, arg, off);
+        const double s2 = __shfl_down_sync(0xffffffffu, sum, off);
+        if (m2 > m || (m2 == m && a2 < arg)) {
+          m = m2;
+          arg = a2;
         }
-        if (lane == 0) {
-          a.part_max[0] = m;
-          a.part_sum[0] = sum;
-          a.part_arg[0] = arg;
-        }
+        sum += s2;
       }
-      __syncthreads();
-    } else {
-      for (int part = 0; part < a.n_parts; ++part) {
-        reduce_partial_body(a, part, smax, ssum, sarg);
-        __syncthreads();
+      if (lane == 0) {
+        s_m = m;
+        s_sum = sum;
+        s_arg = arg;
       }
     }
-    reduce_final_body(a, &s_improved, &s_best);
     __syncthreads();
-    for (int64_t t = threadIdx.x; t < touches; t += kRedThreads) commit_touch(a, t, g);
+    reduce_final_core(a, s_m, s_sum, s_arg, &s_improved, &s_best, mi.code, mi.th);
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < touches; t += kRedThreads)
+      commit_touch_core(a, t, mi.fit[a.div_Lr.div((uint32_t)t)], mi.fb[t], mi.flats[t], mi.mut[t], mi.th[t]);
     __syncthreads();
     if (threadIdx.x == 0) advance_body(a);
   }
@@ -883,17 +940,31 @@ isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s) {
     set_error("the fused single-block generation is single-rank fp64 only");
     return ISQ_ERR_CONFIG;
   }
+  if (a.P > 32 || a.P * a.L > kSmallTouches) {
+    set_error("the fused single-block generation needs sizeOfPopulation <= 32 and P * L <= 4096");
+    return ISQ_ERR_UNSUPPORTED;
+  }
+  const size_t dyn = small_mirror_bytes(a.P * a.L, a.P);
+  auto go = [&](auto kernel) -> isq_status {
+    static bool sized[6] = {};
+    if (!sized[a.n]) {  // the shared-memory copies of the generation exceed the 48 KB default
+      ISQ_CUDA_TRY(cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)small_mirror_bytes(kSmallTouches, 32)));
+      sized[a.n] = true;
+    }
+    kernel<<<1, kRedThreads, dyn, s>>>(a, n_gens);
+    ISQ_CUDA_TRY(cudaGetLastError());
+    return ISQ_OK;
+  };
   switch (a.n) {
-    case 2: qeqea_small_kernel<2><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
-    case 3: qeqea_small_kernel<3><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
-    case 4: qeqea_small_kernel<4><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
-    case 5: qeqea_small_kernel<5><<<1, kRedThreads, 0, s>>>(a, n_gens); break;
+    case 2: return go(qeqea_small_kernel<2>);
+    case 3: return go(qeqea_small_kernel<3>);
+    case 4: return go(qeqea_small_kernel<4>);
+    case 5: return go(qeqea_small_kernel<5>);
     default:
       set_error("the fused single-block generation supports numberOfWires <= 5");
       return ISQ_ERR_UNSUPPORTED;
   }
-  ISQ_CUDA_TRY(cudaGetLastError());
-  return ISQ_OK;
 }
 
 isq_status qeqea_launch_init(const QeqeaArgs& a, cudaStream_t s) {
