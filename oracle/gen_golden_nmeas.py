@@ -1,0 +1,25 @@
+"""QEQEA trajectories with nMeas above numpy's inversion range (the BTPE
+binomial branch in the Born measurement, engine.py:167-170), from the
+REFERENCE itself (TEST INFRASTRUCTURE ONLY; build container):
+
+  traj_qeqea_nmeas100.npz   n = 3, L = 12, P = 5, nMeas = 100, 20 generations
+  traj_qeqea_nmeas61_n4.npz n = 4, L = 8,  P = 6, nMeas = 61, 15 generations
+
+Usage:  python oracle/gen_golden_nmeas.py
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+import gen_golden as G  # noqa: E402  (imports the reference)
+
+
+def main():
+    G.gen_qeqea_traj("nmeas100", 3, 12, 5, G.target_for(3, "Toffoli"), 20, 21, n_meas=100,
+                     probability_of_mutation=0.5)
+    G.gen_qeqea_traj("nmeas61_n4", 4, 8, 6, G.target_for(4, "CCCNOT"), 15, 22, n_meas=61)
+    print("wrote traj_qeqea_nmeas100.npz, traj_qeqea_nmeas61_n4.npz")
+
+
+if __name__ == "__main__":
+    main()

@@ -82,7 +82,8 @@ def test_oracle_mutation_matches_reference():
         np.testing.assert_allclose(eng.qutrits, g[f"g{gen}_qutrits"], rtol=0, atol=1e-15)
 
 
-@pytest.mark.parametrize("name", ["cnot", "toffoli_c1", "fredkin_c3", "cccnot", "haar5", "identity_conv"])
+@pytest.mark.parametrize("name", ["cnot", "toffoli_c1", "fredkin_c3", "cccnot", "haar5", "identity_conv", "nmeas100",
+                                  "nmeas61_n4"])
 def test_oracle_qeqea_trajectory_matches_reference(name):
     g = golden(f"traj_qeqea_{name}")
     lay = O.Layout(int(g["n"]), int(g["L"]), int(g["P"]), p_mut=float(g["p_mut"]),
