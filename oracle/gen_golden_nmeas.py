@@ -4,6 +4,8 @@ REFERENCE itself (TEST INFRASTRUCTURE ONLY; build container):
 
   traj_qeqea_nmeas100.npz   n = 3, L = 12, P = 5, nMeas = 100, 20 generations
   traj_qeqea_nmeas61_n4.npz n = 4, L = 8,  P = 6, nMeas = 61, 15 generations
+  traj_qeqea_long.npz       n = 3, L = 150, P = 4, 6 generations (L > 128: the
+                            warp-per-circuit sampling path, several fitness chunks)
 
 Usage:  python oracle/gen_golden_nmeas.py
 """
@@ -18,7 +20,8 @@ def main():
     G.gen_qeqea_traj("nmeas100", 3, 12, 5, G.target_for(3, "Toffoli"), 20, 21, n_meas=100,
                      probability_of_mutation=0.5)
     G.gen_qeqea_traj("nmeas61_n4", 4, 8, 6, G.target_for(4, "CCCNOT"), 15, 22, n_meas=61)
-    print("wrote traj_qeqea_nmeas100.npz, traj_qeqea_nmeas61_n4.npz")
+    G.gen_qeqea_traj("long", 3, 150, 4, G.target_for(3, "Toffoli"), 6, 23)
+    print("wrote traj_qeqea_nmeas100.npz, traj_qeqea_nmeas61_n4.npz, traj_qeqea_long.npz")
 
 
 if __name__ == "__main__":

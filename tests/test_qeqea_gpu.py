@@ -16,7 +16,7 @@ from oracle import qeqea as O
 
 pytestmark = pytest.mark.gpu
 
-TRAJ = ["cnot", "toffoli_c1", "fredkin_c3", "cccnot", "haar5", "identity_conv", "nmeas100", "nmeas61_n4"]
+TRAJ = ["cnot", "toffoli_c1", "fredkin_c3", "cccnot", "haar5", "identity_conv", "nmeas100", "nmeas61_n4", "long"]
 
 
 def _engine_from_golden(g, **kw):
