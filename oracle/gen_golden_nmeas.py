@@ -7,7 +7,9 @@ REFERENCE itself (TEST INFRASTRUCTURE ONLY; build container):
   traj_qeqea_long.npz       n = 3, L = 150, P = 4, 6 generations (L > 128: the
                             warp-per-circuit sampling path, several fitness chunks)
 
-Usage:  python oracle/gen_golden_nmeas.py
+  traj_ga_l1.npz / traj_ga_long.npz   GA at L = 1 and L = 100 (`... ga`)
+
+Usage:  python oracle/gen_golden_nmeas.py; python oracle/gen_golden_nmeas.py ga
 """
 import sys
 from pathlib import Path
@@ -24,5 +26,17 @@ def main():
     print("wrote traj_qeqea_nmeas100.npz, traj_qeqea_nmeas61_n4.npz, traj_qeqea_long.npz")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def ga_edges():
+    """GA trajectories at the genome-length edges: L = 1 (no crossover draw,
+    ga.py:85-86) and L = 100."""
+    G.gen_ga_traj("l1", 2, 1, 6, G.target_for(2, "CNOT"), 12, 24)
+    G.gen_ga_traj("long", 3, 100, 20, G.target_for(3, "Toffoli"), 8, 25)
+    print("wrote traj_ga_l1.npz, traj_ga_long.npz")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ga":
+    ga_edges()
