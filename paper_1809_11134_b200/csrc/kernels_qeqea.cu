@@ -714,7 +714,9 @@ __device__ __forceinline__ SmallMirror small_mirror(unsigned char* base, int64_t
   return m;
 }
 
-template <int NQ>
+// BIG: nMeas > kInversionMaxMeas (numpy's BTPE branch compiled in; without
+// it the kernel is 8.5k instead of 19k instructions)
+template <int NQ, bool BIG>
 __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a, int n_gens) {
   using G = Geo<NQ>;
   constexpr int kWarps = kRedThreads / 32;
@@ -762,7 +764,7 @@ __global__ void __launch_bounds__(kRedThreads, 1) qeqea_small_kernel(QeqeaArgs a
         }
         double re[3] = {v.q[0].x, v.q[1].x, v.q[2].x};
         double im[3] = {v.q[0].y, v.q[1].y, v.q[2].y};
-        mi.code[t] = measure_code_on(a, s, ms, re, im);
+        mi.code[t] = measure_code_on<BIG>(a, s, ms, re, im);
       } else {
         mi.code[t] = (uint8_t)(3 * a.n + (kind - a.n));
       }
@@ -945,22 +947,23 @@ isq_status qeqea_launch_small(const QeqeaArgs& a, int n_gens, cudaStream_t s) {
     return ISQ_ERR_UNSUPPORTED;
   }
   const size_t dyn = small_mirror_bytes(a.P * a.L, a.P);
+  const bool big = a.n_meas > kInversionMaxMeas;
   auto go = [&](auto kernel) -> isq_status {
-    static bool sized[6] = {};
-    if (!sized[a.n]) {  // the shared-memory copies of the generation exceed the 48 KB default
+    static bool sized[6][2] = {};
+    if (!sized[a.n][big]) {  // the shared-memory copies of the generation exceed the 48 KB default
       ISQ_CUDA_TRY(cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)small_mirror_bytes(kSmallTouches, 32)));
-      sized[a.n] = true;
+      sized[a.n][big] = true;
     }
     kernel<<<1, kRedThreads, dyn, s>>>(a, n_gens);
     ISQ_CUDA_TRY(cudaGetLastError());
     return ISQ_OK;
   };
   switch (a.n) {
-    case 2: return go(qeqea_small_kernel<2>);
-    case 3: return go(qeqea_small_kernel<3>);
-    case 4: return go(qeqea_small_kernel<4>);
-    case 5: return go(qeqea_small_kernel<5>);
+    case 2: return big ? go(qeqea_small_kernel<2, true>) : go(qeqea_small_kernel<2, false>);
+    case 3: return big ? go(qeqea_small_kernel<3, true>) : go(qeqea_small_kernel<3, false>);
+    case 4: return big ? go(qeqea_small_kernel<4, true>) : go(qeqea_small_kernel<4, false>);
+    case 5: return big ? go(qeqea_small_kernel<5, true>) : go(qeqea_small_kernel<5, false>);
     default:
       set_error("the fused single-block generation supports numberOfWires <= 5");
       return ISQ_ERR_UNSUPPORTED;
