@@ -124,3 +124,28 @@ def test_c_host_example_compiles_against_the_header(tmp_path):
     subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-I", str(ROOT / "include"),
                     str(ROOT / "examples" / "qeqea_host.c"), "-L", str(lib), "-lisq", f"-Wl,-rpath,{lib}",
                     "-o", str(tmp_path / "qeqea_host")], check=True)
+
+
+def test_encoding_module_mirrors_the_reference_names_without_a_device():
+    """encoding.py's public names, constants and argument checks (no device
+    call: the Generator refusal and the nMeas check come first)."""
+    import math
+
+    import numpy as np
+
+    from paper_1809_11134_b200 import encoding as E
+    from paper_1809_11134_b200.errors import ConfigurationError
+
+    for name in ("TWO_PI", "SU3_RANGES", "SU3Params", "read_angle", "mutate_angle", "random_angle", "random_qutrit",
+                 "born_probabilities", "measure_qutrit", "estimate_axis", "su3_operator", "mutate_qutrit"):
+        assert hasattr(E, name), name
+    assert E.TWO_PI == 2.0 * math.pi
+    assert np.array_equal(E.SU3_RANGES, np.array([math.pi / 2] * 3 + [2.0 * math.pi] * 5))
+    assert E.SU3Params().theta1 == 0.0 and len(E.SU3Params.__dataclass_fields__) == 8
+    assert E.read_angle(1.25) == 1.25
+    with pytest.raises(TypeError):
+        E.mutate_angle(1.0, 0.5, 0.7, np.random.default_rng(1))
+    with pytest.raises(TypeError):
+        E.mutate_qutrit(np.array([1, 0, 0], dtype=complex), 0.5, np.random.default_rng(1))
+    with pytest.raises(ConfigurationError):
+        E.estimate_axis(np.array([1, 0, 0], dtype=complex), 0, E.CounterStreams(1))
