@@ -162,6 +162,18 @@ isq_status isq_qeqea_create(const isq_qeqea_config* cfg, const double* target, i
   const int64_t nc = a.S * a.L;                  // circuit-side touches
   const int64_t no = (int64_t)a.world * a.S * a.Lr;  // owner-side touches
   TRYA(cudaSetDevice(device));
+  {  // the bank and the per-touch arrays must fit: a clear error instead of a failed allocation
+    const double need = (double)a.Qtloc * sizeof(RotRec) + (double)(a.Qloc - a.Qtloc) * sizeof(IntRec) +
+                        (double)nc * (4 + 1 + 8) + (double)no * (8 + 1 + 48) +
+                        (a.world > 1 ? (double)no * 13 + (double)nc * 13 : 0.0) + (double)D * D * 16;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && need > (double)free_b) {
+      set_error("this configuration needs " + std::to_string((int64_t)(need / 1e9)) + " GB of device memory, " +
+                std::to_string((int64_t)(free_b / 1000000000ull)) + " GB are free (shard it over more GPUs)");
+      free_handle(h);
+      return ISQ_ERR_UNSUPPORTED;
+    }
+  }
   if (qeqea_configure_device() != ISQ_OK) {
     free_handle(h);
     return ISQ_ERR_CUDA;

@@ -278,3 +278,14 @@ def test_device_measurement_matches_reference_goldens(n_meas):
             checked += int(rot.sum())
         eng.step()
     assert checked > 100
+
+
+def test_configuration_larger_than_the_device_is_refused_up_front():
+    """A bank that cannot fit (n = 2, L = 4096, P = 300k: ≈262 GB with the
+    per-touch arrays) is a ConfigurationError naming the sizes, raised before
+    any allocation -- never a CPU fallback."""
+    from paper_1809_11134_b200 import PopulationConfig, QeqeaEngine
+    from paper_1809_11134_b200.errors import ConfigurationError
+
+    with pytest.raises(ConfigurationError, match="GB of device memory"):
+        QeqeaEngine(PopulationConfig(2, 4096, 300_000), np.eye(4, dtype=np.complex128), 1)
