@@ -33,7 +33,7 @@ isq_status bad_config(const std::string& m) {
 
 isq_status check_layout(int n, int L, int64_t P) {
   if (n < ISQ_MIN_WIRES || n > ISQ_MAX_WIRES) {
-    set_error("numberOfWires=" + std::to_string(n) + " is outside the compiled range 2..5");
+    set_error("numberOfWires=" + std::to_string(n) + " is outside the supported range 2..13");
     return ISQ_ERR_UNSUPPORTED;
   }
   if (L < 1 || P < 1) return bad_config("sizeOfIndividual and sizeOfPopulation must be ≥ 1");
@@ -548,7 +548,7 @@ isq_status isq_table_set_slot_max(void* handle, const double* slot_max) {
 isq_status isq_apply_gates(int32_t n, int32_t length, int64_t count, const uint8_t* codes, const double* thetas,
                            const double* acc_in, double* acc_out, int32_t device) {
   if (n < ISQ_MIN_WIRES || n > ISQ_MAX_WIRES) {
-    set_error("numberOfWires=" + std::to_string(n) + " is outside the supported range 2..10");
+    set_error("numberOfWires=" + std::to_string(n) + " is outside the supported range 2..13");
     return n < 2 ? ISQ_ERR_CONFIG : ISQ_ERR_UNSUPPORTED;
   }
   if (length < 0 || count < 0) return bad_config("negative circuit length or count");

@@ -152,7 +152,7 @@ isq_status launch_overlap_fitness(int64_t D, int64_t count, const double* S, con
   return ISQ_OK;
 }
 
-// ------------------------------------------------------ n = 6 .. 10 ---
+// ------------------------------------------------------ n = 6 .. 13 ---
 // numberOfWires above the register-resident kernels (the reference allows up
 // to its 4^n <= 2^26 cap, engine.py:43,60-63): one block per circuit with
 // the 2^n x 2^n state in global scratch (L1 / L2 resident per block), every
@@ -432,7 +432,7 @@ isq_status launch_fitness_batch_stoppable(int n, int L, int64_t count, const uin
     default:
       if (n > ISQ_MAX_FAST_WIRES && n <= ISQ_MAX_WIRES)  // fp64 only (the fp32 variant is a fast-kernel option)
         return launch_fitness_generic(n, L, count, codes, thetas, target, fitness, nullptr, stop, stream, bc);
-      set_error("numberOfWires outside the compiled range 2..5");
+      set_error("numberOfWires outside the supported range 2..13");
       return ISQ_ERR_UNSUPPORTED;
   }
 }
@@ -453,7 +453,7 @@ isq_status launch_fitness_batch(int n, int L, int64_t count, const uint8_t* code
       if (n > ISQ_MAX_FAST_WIRES && n <= ISQ_MAX_WIRES)
         return launch_fitness_generic(n, L, count, codes, thetas, target, fitness, unitary, nullptr, stream,
                                       bad_code);
-      set_error("numberOfWires=" + std::to_string(n) + " is outside the compiled range 2..5");
+      set_error("numberOfWires=" + std::to_string(n) + " is outside the supported range 2..13");
       return ISQ_ERR_UNSUPPORTED;
   }
 }

@@ -562,7 +562,7 @@ static isq_status ga_launch_eval(const GaArgs& a, int64_t c0, int64_t c1, cudaSt
                                       reinterpret_cast<const double*>(a.target), a.fitness + c0, nullptr,
                                       &a.st->stop, s, nullptr, a.codes[1] + c0 * a.L, a.thetas[1] + c0 * a.L,
                                       &a.st->generation);
-      set_error("numberOfWires outside the compiled range 2..5");
+      set_error("numberOfWires outside the supported range 2..13");
       return ISQ_ERR_UNSUPPORTED;
   }
 }
@@ -849,7 +849,7 @@ static isq_status ga_launch_coop(const GaArgs& a, int n_gens, cudaStream_t s) {
     case 4: return ga_launch_coop_nq<4>(a, n_gens, s);
     case 5: return ga_launch_coop_nq<5>(a, n_gens, s);
     default:
-      set_error("numberOfWires outside the compiled range 2..5");
+      set_error("numberOfWires outside the supported range 2..13");
       return ISQ_ERR_UNSUPPORTED;
   }
 }
@@ -864,7 +864,7 @@ static isq_status ga_launch_small(const GaArgs& a, int n_gens, cudaStream_t s) {
     case 4: ga_small_kernel<4><<<1, kGaRed, 0, s>>>(a, n_gens); break;
     case 5: ga_small_kernel<5><<<1, kGaRed, 0, s>>>(a, n_gens); break;
     default:
-      set_error("numberOfWires outside the compiled range 2..5");
+      set_error("numberOfWires outside the supported range 2..13");
       return ISQ_ERR_UNSUPPORTED;
   }
   ISQ_CUDA_TRY(cudaGetLastError());
