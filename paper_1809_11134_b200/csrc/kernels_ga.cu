@@ -589,6 +589,13 @@ __device__ __forceinline__ int ga_select_local(const GaArgs& a, uint64_t g, int 
                                                int64_t* sarg, int32_t* spar, int64_t* s_elite, Idle idle) {
   __shared__ double sfit[kGaRed];
   __shared__ int s_search, s_stop, s_improved;
+  // the SUS stream's first block depends only on (seed, g): thread 0 computes
+  // it now, under the reduction's barriers, not on the walk's critical path
+  NpStream rs;
+  if (threadIdx.x == 0) {
+    rs.init(a.seed, DOM_GA_SUS, g, 0, 0);
+    rs.prime();
+  }
   // generation best / first argmax / sum (ga_reduce_partial_body + the combine of ga_reduce_sus_body)
   double m = -1.0, sum = 0.0;
   int64_t arg = INT64_MAX;
@@ -649,8 +656,6 @@ __device__ __forceinline__ int ga_select_local(const GaArgs& a, uint64_t g, int 
     s_improved = improved;
     s_stop = stop;
     // sus_select (ga.py:95-116), the parallel-search form of ga_reduce_sus_body
-    NpStream rs;
-    rs.init(a.seed, DOM_GA_SUS, g, 0, 0);
     const double total = np_pairwise_sum(sfit, a.P);
     int search = 0;
     if (total <= 0.0) {
@@ -662,9 +667,22 @@ __device__ __forceinline__ int ga_select_local(const GaArgs& a, uint64_t g, int 
       const double spacing = __ddiv_rn(total, (double)a.P);
       double pointer = rs.uniform(0.0, spacing);
       double cumulative = 0.0;
-      for (int k = 0; k < (int)a.P; ++k) {
+      int k = 0;
+      for (; k + 8 <= (int)a.P; k += 8) {  // the loads ahead of the two dependent chains
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = sfit[k + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          cumulative = __dadd_rn(cumulative, v[u]);
+          sfit[k + u] = cumulative;  // C[k + 1]
+          ssum[k + u] = pointer;
+          pointer = __dadd_rn(pointer, spacing);
+        }
+      }
+      for (; k < (int)a.P; ++k) {
         cumulative = __dadd_rn(cumulative, sfit[k]);
-        sfit[k] = cumulative;  // C[k + 1]
+        sfit[k] = cumulative;
         ssum[k] = pointer;
         pointer = __dadd_rn(pointer, spacing);
       }
