@@ -501,6 +501,9 @@ __device__ __forceinline__ void stage_chunk(Chunk& sm, int64_t count, int L, con
 #define ISQ_FIT_GRAB 4
 #endif
 constexpr int kFitGrab = ISQ_FIT_GRAB;  // measured: 4 best (1: +1 %, 2 and 8: +0.2 %)
+#ifndef ISQ_FIT_GUIDED
+#define ISQ_FIT_GUIDED 1
+#endif
 template <int NQ, class R = double, int NR = kFitNR>
 __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t* __restrict__ codes,
                                              const double* __restrict__ thetas,
@@ -511,16 +514,25 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
   const int wib = threadIdx.x >> 5;
   FastChunkT<R, NR>& cs = sh[wib];
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_block;
-  auto grab = [&]() -> int64_t {
+  auto grab = [&](int sz) -> int64_t {
     unsigned long long v = 0;
-    if (lane == 0) v = atomicAdd(dyn, (unsigned long long)kFitGrab);
+    if (lane == 0) v = atomicAdd(dyn, (unsigned long long)sz);
     return (int64_t)__shfl_sync(0xffffffffu, v, 0);
   };
+#if ISQ_FIT_GUIDED
+  // batches of kFitGrab until the last two rounds of the grid, then single
+  // circuits: a shorter tail at C4-sized launches (~22 circuits per warp)
+  auto size_for = [&](int64_t seen) -> int { return seen + 2 * kFitGrab * nwarps < count ? kFitGrab : 1; };
+#else
+  auto size_for = [&](int64_t) -> int { return kFitGrab; };
+#endif
   int64_t c, cend = 0, ahead = 0;
+  int ahead_sz = kFitGrab;
   if (dyn) {
-    c = grab();
+    c = grab(kFitGrab);
     cend = c + kFitGrab;
-    ahead = grab();  // the batch after this one, known early for the prefetch
+    ahead_sz = size_for(c);
+    ahead = grab(ahead_sz);  // the batch after this one, known early for the prefetch
   } else {
     c = (int64_t)blockIdx.x * warps_per_block + wib;
   }
@@ -556,8 +568,9 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
       if (bad && bad_code) atomicOr(bad_code, 1);
     }
     if (dyn && !(c + 1 < cend)) {  // moved on to the batch grabbed ahead
-      cend = ahead + kFitGrab;
-      ahead = grab();
+      cend = ahead + ahead_sz;
+      ahead_sz = size_for(ahead);
+      ahead = grab(ahead_sz);
     }
     c = cn;
   }
