@@ -289,11 +289,11 @@ __global__ void fn_ga_random_genomes_kernel(int L, int ncodes, uint64_t seed, in
 // uniform draws when every fitness is zero: *flag = 0 skips the search).
 __global__ void __launch_bounds__(kSusThreads)
     fn_ga_sus_kernel(const double* f, int64_t P, int64_t count, uint64_t seed, uint64_t g, int64_t* picks,
-                     double* C, double* Pt, int* flag) {
+                     double* C, double* Pt, int* flag, void* grid) {
   __shared__ double sm[kSusThreads];
   extern __shared__ double chain_smem[];
   if (blockIdx.x == 0) {
-    exact_chain_block(f, 0.0, P - 1, 0.0, C, chain_smem);
+    if (grid == nullptr) exact_chain_block(f, 0.0, P - 1, 0.0, C, chain_smem);
     return;
   }
   __shared__ int s_neg;
@@ -301,7 +301,10 @@ __global__ void __launch_bounds__(kSusThreads)
   __syncthreads();
   for (int64_t i = threadIdx.x; i < P; i += blockDim.x)
     if (!(f[i] >= 0.0)) s_neg = 1;  // negative or NaN: the sums are not monotone
-  const double total = np_pairwise_sum_block<kSusThreads>(f, P, sm);  // syncs first
+  const double total = grid != nullptr  // syncs first
+                           ? np_pairwise_combine_block<kSusThreads>(chain_grid_scratch(grid, P - 1).parts,
+                                                                    pairwise_grid_depth(P), chain_smem)
+                           : np_pairwise_sum_block<kSusThreads>(f, P, sm);
   NpStream rs;
   rs.init(seed, DOM_GA_SUS, g, 0, 0);
   if (total <= 0.0) {
@@ -612,8 +615,16 @@ isq_status isq_ga_sus_select(int64_t P, const double* fitness, int64_t count, ui
   TRYF(dflag.alloc(sizeof(int)));
   TRYF(cudaFuncSetAttribute((const void*)fn_ga_sus_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kChainSmem));
+  const bool grid = chain_grid_worth(P - 1);  // the running sums over the whole GPU (sus.cuh)
+  DevBuf dg;
+  if (grid) {
+    TRYF(prepare_exact_chain_grid());
+    TRYF(dg.alloc(chain_grid_scratch_bytes(P - 1)));
+    TRYF(launch_pairwise_parts(df.as<double>(), P, dg.p, P - 1, nullptr));
+    TRYF(launch_exact_chain_grid(df.as<double>(), P - 1, 0.0, dC.as<double>(), dg.p, nullptr));
+  }
   fn_ga_sus_kernel<<<2, kSusThreads, kChainSmem>>>(df.as<double>(), P, count, seed, generation, dp.as<int64_t>(),
-                                       dC.as<double>(), dP.as<double>(), dflag.as<int>());
+                                       dC.as<double>(), dP.as<double>(), dflag.as<int>(), grid ? dg.p : nullptr);
   TRYF(cudaGetLastError());
   sus_search_kernel<int64_t><<<grid_for(count), 256>>>(dC.as<double>(), P - 1, dP.as<double>(), count,
                                                        dp.as<int64_t>(), dflag.as<int>(), nullptr);

@@ -59,6 +59,7 @@ struct GaArgs {
   double* sus_C;  // P > kSusCache: the walk's running sums (sus.cuh)
   double* sus_P;
   int* sus_flag;
+  void* sus_grid;  // P - 1 >= chain_grid_worth: scratch of the grid-wide chain (else null)
   int precision;  // fitness arithmetic: ISQ_PRECISION_FP64 / _FP32
   FastDiv div_L, div_P;  // gene index -> genome; pair index mod P (P * L < 2^32)
 };
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(kSusThreads) ga_reduce_sus_large_kernel(GaArgs
   if (a.st->stop) return;
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0) ga_reduce_final(a, s_improved, s_elite);
-    exact_chain_block(a.fitness, 0.0, a.P - 1, 0.0, a.sus_C, chain_smem);
+    if (a.sus_grid == nullptr) exact_chain_block(a.fitness, 0.0, a.P - 1, 0.0, a.sus_C, chain_smem);
     __syncthreads();  // s_improved / s_elite
     if (s_improved && threadIdx.x < 32) {
       const int cur = ga_cur(a);
@@ -286,7 +287,11 @@ __global__ void __launch_bounds__(kSusThreads) ga_reduce_sus_large_kernel(GaArgs
     }
     return;
   }
-  const double total = np_pairwise_sum_block<kSusThreads>(a.fitness, a.P, sm);
+  const double total =
+      a.sus_grid != nullptr
+          ? np_pairwise_combine_block<kSusThreads>(chain_grid_scratch(a.sus_grid, a.P - 1).parts,
+                                                   pairwise_grid_depth(a.P), chain_smem)
+          : np_pairwise_sum_block<kSusThreads>(a.fitness, a.P, sm);
   NpStream rs;
   rs.init(a.seed, DOM_GA_SUS, a.st->generation, 0, 0);
   if (total <= 0.0) {
@@ -523,6 +528,7 @@ static void ga_free(GaHandle* h) {
   cudaFree(a.sus_C);
   cudaFree(a.sus_P);
   cudaFree(a.sus_flag);
+  cudaFree(a.sus_grid);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -921,6 +927,10 @@ static isq_status ga_launch_finish(const GaArgs& a, cudaStream_t s) {
   }
   ga_reduce_partials<<<a.n_parts, kGaRed, 0, s>>>(a);
   if (a.P > kSusCache) {
+    if (a.sus_grid != nullptr) {  // the running sums and numpy's total over the whole GPU (sus.cuh)
+      ISQ_CUDA_TRY(launch_pairwise_parts(a.fitness, a.P, a.sus_grid, a.P - 1, s));
+      ISQ_CUDA_TRY(launch_exact_chain_grid(a.fitness, a.P - 1, 0.0, a.sus_C, a.sus_grid, s));
+    }
     ga_reduce_sus_large_kernel<<<2, kSusThreads, kChainSmem, s>>>(a);
     sus_search_kernel<int32_t><<<ga_blocks(a.P), 256, 0, s>>>(a.sus_C, a.P - 1, a.sus_P, a.P, a.parents,
                                                               a.sus_flag, &a.st->stop);
@@ -1030,6 +1040,10 @@ isq_status isq_ga_create(const isq_ga_config* cfg, const double* target, int32_t
     GA_TRY(cudaMalloc((void**)&a.sus_C, a.P * 8));
     GA_TRY(cudaMalloc((void**)&a.sus_P, a.P * 8));
     GA_TRY(cudaMalloc((void**)&a.sus_flag, sizeof(int)));
+    if (chain_grid_worth(a.P - 1)) {  // the running sums over the whole GPU (sus.cuh)
+      GA_TRY(prepare_exact_chain_grid());
+      GA_TRY(cudaMalloc(&a.sus_grid, chain_grid_scratch_bytes(a.P - 1)));
+    }
   }
   GA_TRY(cudaMemcpy((void*)a.target, target, D * D * 16, cudaMemcpyHostToDevice));
   GaDevState s0;

@@ -115,10 +115,11 @@ def test_ga_batched_steps_equal_single_steps(mode):
     assert np.array_equal(ca, cb) and np.array_equal(ta, tb)
 
 
-@pytest.mark.parametrize("P", [513, 1 << 17])
+@pytest.mark.parametrize("P", [513, 1 << 17, (1 << 17) + 2])
 def test_large_population_parents_match_the_oracle_walk(P):
     """P > 512 selects on the block SUS + search kernels (kernels_ga.cu
-    ga_reduce_sus_large_kernel); its parents must be the sequential walk's
+    ga_reduce_sus_large_kernel; from P - 1 = 2^17 the running sums and the
+    total are grid-wide, sus.cuh launch_exact_chain_grid); its parents must be the sequential walk's
     (oracle/ga.sus_select, pinned to the reference by tests/golden/sus_large)
     on the engine's own fitness, generation by generation."""
     from oracle.ga import sus_select
