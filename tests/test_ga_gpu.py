@@ -115,7 +115,7 @@ def test_ga_batched_steps_equal_single_steps(mode):
     assert np.array_equal(ca, cb) and np.array_equal(ta, tb)
 
 
-@pytest.mark.parametrize("P", [513, 1 << 17, (1 << 17) + 2])
+@pytest.mark.parametrize("P", [513, 1 << 17, (1 << 17) + 2, 1 << 20])
 def test_large_population_parents_match_the_oracle_walk(P):
     """P > 512 selects on the block SUS + search kernels (kernels_ga.cu
     ga_reduce_sus_large_kernel; from P - 1 = 2^17 the running sums and the
