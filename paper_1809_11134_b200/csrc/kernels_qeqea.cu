@@ -119,11 +119,16 @@ __global__ void qeqea_unroute_kernel(QeqeaArgs a) {
 #ifndef ISQ_VAL_PREDRAW
 #define ISQ_VAL_PREDRAW 1
 #endif
-constexpr int kValThreads = 256;
-#ifndef ISQ_VAL_PER_THREAD
-#define ISQ_VAL_PER_THREAD 3
+#ifndef ISQ_VAL_THREADS
+#define ISQ_VAL_THREADS 256
 #endif
-constexpr int kValPerThread = ISQ_VAL_PER_THREAD;  // touches per thread per tile: ~1 measurement task per thread
+constexpr int kValThreads = ISQ_VAL_THREADS;
+#ifndef ISQ_VAL_PER_THREAD
+#define ISQ_VAL_PER_THREAD 2
+#endif
+// touches per thread per tile (measured, C4 / C5 generations: 256 x 2 2.88k gen/s / 15.15 ms, 256 x 3 2.73k /
+// 15.39, 256 x 1 2.74k / 15.86, 256 x 4 2.56k / 15.94, 128 x 2 2.86k / 15.17, 512 x 1 2.66k / 16.09)
+constexpr int kValPerThread = ISQ_VAL_PER_THREAD;
 constexpr int kValTile = kValThreads * kValPerThread;
 
 // Per tile: the touches' committed records, staged by cp.async (no registers
