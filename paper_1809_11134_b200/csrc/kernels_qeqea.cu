@@ -29,7 +29,10 @@ namespace isq {
 // keep each one's hot code inside the instruction cache and give the random
 // bank gathers thread-level memory parallelism.
 
-constexpr int kSampleRun = 64;  // circuits per warp task of the batched sampler
+#ifndef ISQ_SAMPLE_RUN
+#define ISQ_SAMPLE_RUN 16
+#endif
+constexpr int kSampleRun = ISQ_SAMPLE_RUN;  // circuits per warp task of the batched sampler (64: a partial last wave)
 #ifndef ISQ_FIT_DYNAMIC
 #define ISQ_FIT_DYNAMIC 1
 #endif
@@ -38,7 +41,7 @@ constexpr int kSampleRun = 64;  // circuits per warp task of the batched sampler
 #endif
 
 __global__ void __launch_bounds__(kThreadsPerBlock) qeqea_sample_flats_kernel(QeqeaArgs a) {
-  __shared__ uint64_t blk[kWarpsPerBlock][128];
+  __shared__ uint64_t blk[kWarpsPerBlock][128 * kSampleIlp];
   if (a.st->stop) return;
   const uint64_t g = a.st->generation;
   const int lane = threadIdx.x & 31;
