@@ -411,7 +411,22 @@ __device__ __forceinline__ void reduce_partial_body(const QeqeaArgs& a, int part
   const int64_t hi = min(a.P, lo + per);
   double m = -1.0, sum = 0.0;
   int64_t arg = INT64_MAX;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kRedThreads) {
+  int64_t i = lo + threadIdx.x;
+  constexpr int kBatch = 8;  // loads issued together, then folded in index order (same sums)
+  for (; i + (kBatch - 1) * kRedThreads < hi; i += kBatch * kRedThreads) {
+    double f[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) f[k] = a.fitness[i + k * kRedThreads];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      sum += f[k];
+      if (f[k] > m) {
+        m = f[k];
+        arg = i + k * kRedThreads;
+      }
+    }
+  }
+  for (; i < hi; i += kRedThreads) {
     const double f = a.fitness[i];
     sum += f;
     if (f > m) {
@@ -500,16 +515,26 @@ __device__ __forceinline__ void reduce_final_core(const QeqeaArgs& a, double m, 
 }
 
 __device__ __forceinline__ void reduce_final_body(const QeqeaArgs& a, int* s_improved, int64_t* s_best) {
+  // the partials staged by the whole block (one round trip), then folded by
+  // thread 0 in part order (the same result as a serial walk over them)
+  __shared__ double s_pm[1024], s_ps[1024];
+  __shared__ int64_t s_pa[1024];
+  for (int i = threadIdx.x; i < a.n_parts; i += blockDim.x) {
+    s_pm[i] = a.part_max[i];
+    s_ps[i] = a.part_sum[i];
+    s_pa[i] = a.part_arg[i];
+  }
+  __syncthreads();
   double m = -1.0, sum = 0.0;
   int64_t arg = INT64_MAX;
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.n_parts; ++i) {
-      const double pm = a.part_max[i];
-      if (pm > m || (pm == m && a.part_arg[i] < arg)) {
+      const double pm = s_pm[i];
+      if (pm > m || (pm == m && s_pa[i] < arg)) {
         m = pm;
-        arg = a.part_arg[i];
+        arg = s_pa[i];
       }
-      sum += a.part_sum[i];
+      sum += s_ps[i];
     }
   }
   reduce_final_core(a, m, sum, arg, s_improved, s_best, a.gate_codes, a.gate_thetas);
