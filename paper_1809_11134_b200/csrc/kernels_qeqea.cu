@@ -549,7 +549,10 @@ __global__ void __launch_bounds__(kRedThreads) qeqea_reduce_final(QeqeaArgs a) {
 
 // -------------------------------------------------------------- commit ---
 
-constexpr int kCommitThreads = 256;
+#ifndef ISQ_COMMIT_THREADS
+#define ISQ_COMMIT_THREADS 256
+#endif
+constexpr int kCommitThreads = ISQ_COMMIT_THREADS;
 #ifndef ISQ_COMMIT_FULL_GRID
 #define ISQ_COMMIT_FULL_GRID 1
 #endif
