@@ -291,6 +291,29 @@ def test_sus_select_edge_shapes_match_the_walk(P, count, kind):
     assert sus_select(f, count, CounterStreams(8, 2)) == want
 
 
+@pytest.mark.parametrize("kind", ["zero_prefix", "dyadic", "spikes", "wide", "tiny"])
+def test_sus_select_grid_wide_sums_match_the_walk(kind):
+    """From P - 1 = 2^17 values the running sums and numpy's total run over
+    the whole GPU (sus.cuh launch_exact_chain_grid / launch_pairwise_parts):
+    tiles advanced by their composite map where the binade provably holds,
+    the rest (binade crossings, a zero or subnormal-range running sum) by
+    the exact block form.  Families that exercise each branch."""
+    from oracle.ga import sus_select as walk
+    from oracle.streams import DOM_GA_SUS
+    from paper_1809_11134_b200 import CounterStreams, sus_select
+
+    P = (1 << 17) + 3 * 8192 + 5
+    r = np.random.default_rng(42)
+    u = r.random(P)
+    f = {"zero_prefix": np.where(np.arange(P) < P // 2, 0.0, u),
+         "dyadic": np.floor(u * 64) / 64,
+         "spikes": np.where(u < 0.3, 0.0, np.where(u > 0.9999, 1e6 * u, u)),
+         "wide": np.ldexp(u, (np.arange(P) % 40) - 20),
+         "tiny": 1e-310 * u}[kind]
+    want = walk(list(map(float, f)), P, stream(9, DOM_GA_SUS, 4))
+    assert sus_select(f, P, CounterStreams(9, 4)) == want
+
+
 def test_sus_all_zero_falls_back_to_uniform_draws():
     from paper_1809_11134_b200 import CounterStreams, sus_select
 
