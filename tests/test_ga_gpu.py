@@ -115,6 +115,27 @@ def test_ga_batched_steps_equal_single_steps(mode):
     assert np.array_equal(ca, cb) and np.array_equal(ta, tb)
 
 
+@pytest.mark.parametrize("mode", ["graph", "auto"])
+def test_large_population_graph_modes_equal_plain_kernels(mode):
+    """The grid-wide SUS (P - 1 >= 2^17: tile sums, maps, serial carry, apply,
+    pairwise parts) captured into the generation graphs gives the plain
+    launches' parents and genomes."""
+    from paper_1809_11134_b200 import GaConfig, GaEngine, target_matrix
+
+    P = (1 << 17) + 2
+    a = GaEngine(GaConfig(2, 4, P, max_generations=100, target_fitness=1.0), target_matrix("CNOT"), 6)
+    b = GaEngine(GaConfig(2, 4, P, max_generations=100, target_fitness=1.0), target_matrix("CNOT"), 6)
+    a.set_launch_mode("kernels")
+    b.set_launch_mode(mode)
+    ra = [a.step() for _ in range(4)]
+    rb = b.steps(4)
+    assert [x[0] for x in ra] == list(rb["gen_best"]) and [x[1] for x in ra] == list(rb["gen_mean"])
+    assert np.array_equal(a.last_parents(), b.last_parents())
+    ca, ta = a.genome_arrays()
+    cb, tb = b.genome_arrays()
+    assert np.array_equal(ca, cb) and np.array_equal(ta, tb)
+
+
 @pytest.mark.parametrize("P", [513, 1 << 17, (1 << 17) + 2, 1 << 20])
 def test_large_population_parents_match_the_oracle_walk(P):
     """P > 512 selects on the block SUS + search kernels (kernels_ga.cu
