@@ -25,7 +25,7 @@ def _engine(g):
     return GaEngine(cfg, TargetSpec("golden", cfg.number_of_wires, g["target"]), int(g["seed"]))
 
 
-@pytest.mark.parametrize("name", ["cnot", "toffoli_c2", "odd13", "p300", "p1024", "l1", "long"])
+@pytest.mark.parametrize("name", ["cnot", "toffoli_c2", "odd13", "p300", "p1024", "l1", "long", "n4", "n5"])
 @pytest.mark.parametrize("mode", ["auto", "kernels", "fused"])
 def test_ga_trajectory_matches_reference(name, mode):
     g = golden(f"traj_ga_{name}")

@@ -112,7 +112,7 @@ def test_oracle_qeqea_trajectory_matches_reference(name):
     np.testing.assert_allclose(eng.best_thetas, g["best_thetas"], rtol=1e-12, atol=1e-13)
 
 
-@pytest.mark.parametrize("name", ["cnot", "toffoli_c2", "odd13", "l1", "long"])
+@pytest.mark.parametrize("name", ["cnot", "toffoli_c2", "odd13", "l1", "long", "n4", "n5"])
 def test_oracle_ga_trajectory_matches_reference(name):
     g = golden(f"traj_ga_{name}")
     cfg = OG.GaLayout(int(g["n"]), int(g["L"]), int(g["P"]), rate=float(g["rate"]),
