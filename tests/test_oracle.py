@@ -83,7 +83,7 @@ def test_oracle_mutation_matches_reference():
 
 
 @pytest.mark.parametrize("name", ["cnot", "toffoli_c1", "fredkin_c3", "cccnot", "haar5", "identity_conv", "nmeas100",
-                                  "nmeas61_n4", "long"])
+                                  "nmeas61_n4", "long", "n5_l64"])
 def test_oracle_qeqea_trajectory_matches_reference(name):
     g = golden(f"traj_qeqea_{name}")
     lay = O.Layout(int(g["n"]), int(g["L"]), int(g["P"]), p_mut=float(g["p_mut"]),

@@ -16,7 +16,8 @@ from oracle import qeqea as O
 
 pytestmark = pytest.mark.gpu
 
-TRAJ = ["cnot", "toffoli_c1", "fredkin_c3", "cccnot", "haar5", "identity_conv", "nmeas100", "nmeas61_n4", "long"]
+TRAJ = ["cnot", "toffoli_c1", "fredkin_c3", "cccnot", "haar5", "identity_conv", "nmeas100", "nmeas61_n4", "long",
+        "n5_l64"]
 
 
 def _engine_from_golden(g, **kw):
