@@ -136,7 +136,7 @@ def test_large_population_graph_modes_equal_plain_kernels(mode):
     assert np.array_equal(ca, cb) and np.array_equal(ta, tb)
 
 
-@pytest.mark.parametrize("P", [513, 1 << 17, (1 << 17) + 2, 1 << 20])
+@pytest.mark.parametrize("P", [513, 1 << 17, (1 << 17) + 1, (1 << 17) + 2, 1 << 20])
 def test_large_population_parents_match_the_oracle_walk(P):
     """P > 512 selects on the block SUS + search kernels (kernels_ga.cu
     ga_reduce_sus_large_kernel; from P - 1 = 2^17 the running sums and the
