@@ -83,3 +83,39 @@ def test_multiblock_generations_match_reference(name, mode):
     bc, bt = encode_gates(eng.best_gates, cfg.number_of_wires)
     assert list(bc) == list(g["best_codes"])
     np.testing.assert_allclose(bt, g["best_thetas"], rtol=1e-11, atol=1e-12)
+
+
+def test_c5_run_invariants():
+    """BASELINE config 5 (n = 5, L = 64, P = 2^20, 36 GB bank) for 40
+    generations through the engine's batched steps: the records are
+    consistent (best-so-far = running max of the generation bests, fitness
+    values in [0, 1], mean <= best), `steps(k)` and the stop rule agree, and
+    circuits of generation 25 sampled on their own (`sample`, the gates the
+    generation evaluates) and rescored with fitness_batch give the fitness
+    the generation recorded."""
+    from paper_1809_11134_b200.engine import PopulationConfig, QeqeaEngine
+    from paper_1809_11134_b200.fitness import TargetSpec, fitness_batch
+    from paper_1809_11134_b200.synthetic import haar_target
+
+    n, L, P, gens = 5, 64, 1 << 20, 40
+    T = haar_target(n)
+    eng = QeqeaEngine(PopulationConfig(n, L, P, max_generations=gens, target_fitness=1.0),
+                      TargetSpec("haar", n, T), 7)
+    rec = eng.steps(25)
+    c0 = P // 3
+    _, codes, thetas = eng.sample(c0, c0 + 48)
+    gb, gm = eng.step()
+    again = fitness_batch(codes, thetas, T, n)
+    assert fit_close(again, eng.last_fitness()[c0:c0 + 48]).all()
+    rec2 = eng.steps(100)  # stops at the generation limit
+    assert len(rec) == 25 and len(rec2) == gens - 26
+    assert eng.done and eng.stop_reason == "generation-limit" and eng.generation == gens
+    best = np.concatenate([rec["gen_best"], [gb], rec2["gen_best"]])
+    mean = np.concatenate([rec["gen_mean"], [gm], rec2["gen_mean"]])
+    bsf = np.concatenate([rec["best_fitness"], [max(rec["best_fitness"][-1], gb)], rec2["best_fitness"]])
+    assert np.all((best >= 0) & (best <= 1)) and np.all(mean <= best) and np.all(mean >= 0)
+    assert np.array_equal(bsf, np.maximum.accumulate(best))
+    assert eng.best_fitness == bsf[-1]
+    fit = eng.last_fitness()
+    assert fit.shape == (P,) and fit.max() == best[-1]
+    eng.close()
