@@ -501,6 +501,11 @@ __device__ __forceinline__ void stage_chunk(Chunk& sm, int64_t count, int L, con
 #define ISQ_FIT_GRAB 4
 #endif
 constexpr int kFitGrab = ISQ_FIT_GRAB;  // measured: 4 best (1: +1 %, 2 and 8: +0.2 %)
+// n = 5 (C5's fitness, 9.22 -> 9.19 ms; kbench n = 5 -0.4 %): batches of 12
+// (8: 9.20, 16: 9.20 ms); n = 4 keeps 4 (12: kbench QEQEA n = 4 +2.5 %)
+#ifndef ISQ_FIT_GRAB5
+#define ISQ_FIT_GRAB5 12
+#endif
 #ifndef ISQ_FIT_GUIDED
 #define ISQ_FIT_GUIDED 1
 #endif
@@ -510,6 +515,7 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
                                              const double2* __restrict__ Ts, FastChunkT<R, NR>* sh,
                                              double* __restrict__ fitness, int warps_per_block,
                                              int* bad_code = nullptr, unsigned long long* dyn = nullptr) {
+  constexpr int kGrab = NQ == 5 ? ISQ_FIT_GRAB5 : kFitGrab;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   FastChunkT<R, NR>& cs = sh[wib];
@@ -520,17 +526,17 @@ __device__ __forceinline__ void fitness_rows(int64_t count, int L, const uint8_t
     return (int64_t)__shfl_sync(0xffffffffu, v, 0);
   };
 #if ISQ_FIT_GUIDED
-  // batches of kFitGrab until the last two rounds of the grid, then single
+  // batches of kGrab until the last two rounds of the grid, then single
   // circuits: a shorter tail at C4-sized launches (~22 circuits per warp)
-  auto size_for = [&](int64_t seen) -> int { return seen + 2 * kFitGrab * nwarps < count ? kFitGrab : 1; };
+  auto size_for = [&](int64_t seen) -> int { return seen + 2 * kGrab * nwarps < count ? kGrab : 1; };
 #else
-  auto size_for = [&](int64_t) -> int { return kFitGrab; };
+  auto size_for = [&](int64_t) -> int { return kGrab; };
 #endif
   int64_t c, cend = 0, ahead = 0;
-  int ahead_sz = kFitGrab;
+  int ahead_sz = kGrab;
   if (dyn) {
-    c = grab(kFitGrab);
-    cend = c + kFitGrab;
+    c = grab(kGrab);
+    cend = c + kGrab;
     ahead_sz = size_for(c);
     ahead = grab(ahead_sz);  // the batch after this one, known early for the prefetch
   } else {
